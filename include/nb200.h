@@ -1,0 +1,246 @@
+/*
+ * nb200 -- C ABI of the B200-native hot path of arXiv 2102.06599
+ * ("NAS as program transformation exploration", reference library `nestopt`).
+ *
+ * The reference exposes no FFI: its operator API is the header-only C++
+ * namespace `nestopt` (/root/reference/proj/include/nestopt).  This header is
+ * the drop-in boundary a maintainer binds from that C++ host (see
+ * INTEGRATION.md and integration/nestopt_b200.hpp): every entry point below
+ * replaces one reference function, cited as I/<file>:<line> where
+ * I/ = proj/include/nestopt/.
+ *
+ * Conventions (mirroring the reference's):
+ *  - plain C types only; host buffers are caller-owned, fp64 and in the
+ *    reference's layouts (per image (C,H,W) row-major, weights
+ *    (Co_eff,Ci,Kh,Kw), head [num_classes][C_last]); they are never retained
+ *    after a call returns.  Device memory is owned by the context.
+ *  - errors: every call returns an nb_status whose values map 1:1 onto the
+ *    nestopt exception classes (I/errors.hpp); nb_last_error() returns the
+ *    message of the last failing call on the calling thread.
+ *  - threading: calls on one context are serialized internally; different
+ *    contexts (one per GPU) run concurrently.
+ *  - there is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with NB_ERR_NO_DEVICE.
+ */
+#ifndef NB200_H
+#define NB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NB200_ABI_VERSION 1
+
+typedef enum nb_status {
+  NB_OK = 0,
+  NB_ERR_INVALID_SPEC = 1,    /* nestopt::InvalidSpec   I/errors.hpp:11 */
+  NB_ERR_CONFIG = 2,          /* nestopt::ConfigError   I/errors.hpp:64 */
+  NB_ERR_SHAPE_MISMATCH = 3,  /* nestopt::ShapeMismatch I/errors.hpp:60 */
+  NB_ERR_CAP_EXCEEDED = 4,    /* nestopt::CapExceeded   I/errors.hpp:17 (host gate only) */
+  NB_ERR_TRANSFORM = 5,       /* nestopt::TransformError I/errors.hpp:22 */
+  NB_ERR_PARSE = 6,           /* nestopt::ParseError    I/errors.hpp:46 */
+  NB_ERR_IO = 7,              /* nestopt::IoError       I/errors.hpp:67 */
+  NB_ERR_GENERIC = 8,         /* nestopt::Error         I/errors.hpp:8  */
+  NB_ERR_CUDA = 100,          /* CUDA runtime / launch failure */
+  NB_ERR_NO_DEVICE = 101,     /* no usable sm_100 device: no CPU fallback exists */
+  NB_ERR_OUT_OF_MEMORY = 102,
+  NB_ERR_UNSUPPORTED = 103,
+  NB_ERR_INTERNAL = 199
+} nb_status;
+
+/* Arithmetic mode of the conv kernels.  Head, softmax and the Fisher
+ * reduction always run in fp64. */
+typedef enum nb_precision {
+  NB_PREC_FP32 = 0, /* fp32-accurate (default, used for legality decisions):
+                       3xTF32 tcgen05 implicit GEMM for tensor-core-shaped
+                       ranges, fp32 FFMA for the rest */
+  NB_PREC_TF32 = 1, /* 1xTF32 tcgen05 throughput mode (looser tolerance) */
+  NB_PREC_SIMT = 2  /* fp32 FFMA kernels only (parity baseline) */
+} nb_precision;
+
+/* ChannelSplit, I/ir.hpp:20-24 */
+typedef struct nb_channel_split {
+  int64_t begin, end, groups;
+} nb_channel_split;
+
+/* ConvSpec, I/ir.hpp:26-87 (field for field). */
+typedef struct nb_conv_spec {
+  int64_t ci, co, h, w, kh, kw, stride, pad, groups, bottleneck_out,
+      spatial_div_h, spatial_div_w;
+  int64_t num_splits;             /* 0 = single range {0, co_eff, groups} */
+  const nb_channel_split* splits; /* num_splits entries */
+} nb_conv_spec;
+
+/* Layer, I/nnet.hpp:23-26 */
+typedef struct nb_layer {
+  nb_conv_spec spec;
+  int32_t relu;
+  int32_t reserved;
+} nb_layer;
+
+/* Network, I/nnet.hpp:28-79, without its weight tensors: weights are either
+ * drawn exactly as Network::init_weights does (I/nnet.hpp:58-79, from
+ * `seed`), or passed explicitly through nb_weights. */
+typedef struct nb_network {
+  int64_t num_layers;
+  const nb_layer* layers;
+  int64_t num_classes;
+  uint64_t seed;
+} nb_network;
+
+/* Explicit Network::weights / Network::head.  NULL (or NULL members) =
+ * init_weights(seed). */
+typedef struct nb_weights {
+  const double* const* layer; /* num_layers pointers, (Co_eff,Ci,Kh,Kw) each */
+  const double* head;         /* [num_classes][C_last] */
+} nb_weights;
+
+/* Batch, I/nnet.hpp:81-85.  inputs == NULL => make_batch(net, n, seed)
+ * (I/nnet.hpp:87-101), drawn bit-identically on the host. */
+typedef struct nb_batch {
+  int64_t n;
+  const double* inputs;  /* n x (Ci,H,W) of layer 0, or NULL */
+  const int32_t* labels; /* n, or NULL when inputs == NULL */
+  uint64_t seed;
+} nb_batch;
+
+/* FisherReport, I/nnet.hpp:272-277, plus the forward loss. */
+typedef struct nb_fisher_out {
+  double* per_channel; /* sum_l Co_eff(l) doubles (layer-major), or NULL */
+  double* per_layer;   /* num_layers doubles, or NULL */
+  double total;
+  uint64_t seed;       /* batch seed the scores were computed under */
+  double loss;         /* mean cross-entropy of the forward pass */
+  double* probs;       /* n x num_classes softmax, or NULL */
+} nb_fisher_out;
+
+typedef struct nb_ctx nb_ctx;         /* one per GPU: stream, arena, caches */
+typedef struct nb_session nb_session; /* a context + one HBM-resident batch */
+
+/* Per-kernel-family device time, recorded with CUDA events on the launching
+ * stream while profiling is enabled (nb_ctx_set_profiling). */
+typedef struct nb_kernel_stat {
+  char name[48];
+  int64_t launches;
+  double ms;          /* summed event time */
+  double flops;       /* algorithmic FLOPs (2 x count_macs-style MACs) */
+  double bytes;       /* algorithmic HBM bytes (read once + write once) */
+} nb_kernel_stat;
+
+/* Scheduler statistics of one nb_evaluate call. */
+typedef struct nb_eval_stats {
+  int64_t evaluated;     /* distinct networks run on a device */
+  int64_t deduplicated;  /* candidates answered from an identical network */
+  double est_flops[16];  /* per context: LPT-assigned estimated FLOPs */
+  double busy_ms[16];    /* per context: wall time of its worker */
+} nb_eval_stats;
+
+/* ---- library ---------------------------------------------------------- */
+const char* nb_version(void);
+int nb_abi_version(void);
+int nb_device_count(void);
+const char* nb_last_error(void);
+
+/* ---- host-side descriptors (no device needed) ------------------------- */
+/* ConvSpec::validate, I/ir.hpp:59-86 */
+nb_status nb_validate_spec(const nb_conv_spec* spec);
+/* Network::validate, I/nnet.hpp:40-55 */
+nb_status nb_validate_network(const nb_network* net);
+/* count_macs(conv_nest(spec)), I/interp.hpp:190-202 + I/ir.hpp:427 */
+nb_status nb_conv_macs(const nb_conv_spec* spec, int64_t* macs);
+/* network_macs, I/search.hpp:84-88 */
+nb_status nb_network_macs(const nb_network* net, int64_t* macs);
+/* repair_network shape propagation, I/nnet.hpp:372-382 (in place on a
+ * caller-owned layer array; weights are redrawn lazily on the device). */
+nb_status nb_repair_network(int64_t num_layers, nb_layer* layers);
+/* Longest-processing-time-first assignment of `count` jobs of estimated
+ * cost to `bins` workers (ties broken by index); deterministic. */
+nb_status nb_schedule_lpt(const double* cost, int64_t count, int32_t bins,
+                          int32_t* assignment);
+/* Estimated FLOPs of one Fisher evaluation: 2*N*(fprop MACs + dgrad MACs). */
+nb_status nb_fisher_flops(const nb_network* net, int64_t n, double* flops);
+/* Network::init_weights, I/nnet.hpp:58-79 (host, bit-identical draws):
+ * weights = concatenation of the per-layer (Co_eff,Ci,Kh,Kw) tensors. */
+nb_status nb_init_weights(const nb_network* net, double* weights, double* head);
+/* make_batch, I/nnet.hpp:87-101 (host, bit-identical draws). */
+nb_status nb_make_batch(const nb_network* net, int64_t n, uint64_t seed,
+                        double* inputs, int32_t* labels);
+
+/* ---- contexts ------------------------------------------------------------ */
+nb_status nb_ctx_create(int device, nb_ctx** out);
+nb_status nb_ctx_destroy(nb_ctx* ctx);
+/* The CUDA stream (cudaStream_t) all of the context's kernels run on. */
+void* nb_ctx_stream(nb_ctx* ctx);
+nb_status nb_ctx_set_profiling(nb_ctx* ctx, int enable);
+/* Copies up to `cap` stats, returns the number of families in *count. */
+nb_status nb_ctx_kernel_stats(nb_ctx* ctx, nb_kernel_stat* stats, int32_t cap,
+                              int32_t* count);
+nb_status nb_ctx_reset_stats(nb_ctx* ctx);
+/* Number of nb200 kernel launches issued by this context so far. */
+int64_t nb_ctx_launch_count(nb_ctx* ctx);
+
+/* ---- single conv layer (reference_conv / layer_forward) ------------------ */
+/* reference_conv<double> (I/interp.hpp:151-186) / layer_forward
+ * (I/nnet.hpp:130-141) over n images: x n x (Ci,H,W), w (Co_eff,Ci,Kh,Kw),
+ * y n x (Co_eff,out_h,out_w); relu != 0 applies the layer's ReLU. */
+nb_status nb_conv_forward(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n,
+                          const double* x, const double* w, double* y,
+                          int32_t relu, nb_precision prec);
+/* The dgrad step of activation_gradients (I/nnet.hpp:235-243): dx n x
+ * (Ci,H,W) = sum over for_each_conv_mac of W * dy, dy n x (Co_eff,oh,ow). */
+nb_status nb_conv_dgrad(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n,
+                        const double* dy, const double* w, double* dx,
+                        nb_precision prec);
+
+/* ---- network-level entry points ----------------------------------------- */
+/* forward, I/nnet.hpp:180-197: probs n x classes, example_loss n, loss. */
+nb_status nb_forward(nb_ctx* ctx, const nb_network* net, const nb_weights* w,
+                     const nb_batch* batch, nb_precision prec, double* probs,
+                     double* example_loss, double* loss);
+/* forward + activation_gradients, I/nnet.hpp:180-247: acts/grads laid out
+ * for l in [0,L): for n: (C,H,W) of layer l's post-activation output. */
+nb_status nb_activation_gradients(nb_ctx* ctx, const nb_network* net,
+                                  const nb_weights* w, const nb_batch* batch,
+                                  nb_precision prec, double* acts,
+                                  double* grads);
+/* fisher_potential, I/nnet.hpp:321-352. */
+nb_status nb_fisher_potential(nb_ctx* ctx, const nb_network* net,
+                              const nb_weights* w, const nb_batch* batch,
+                              nb_precision prec, nb_fisher_out* out);
+/* fisher_accepts, I/nnet.hpp:356-359 (candidate.total >= original.total). */
+int nb_fisher_accepts(const nb_fisher_out* original,
+                      const nb_fisher_out* candidate);
+
+/* ---- sessions: a batch kept resident in HBM ------------------------------ */
+nb_status nb_session_create(nb_ctx* ctx, const nb_network* shape_net,
+                            const nb_batch* batch, nb_session** out);
+nb_status nb_session_destroy(nb_session* s);
+nb_ctx* nb_session_ctx(nb_session* s);
+nb_status nb_session_fisher(nb_session* s, const nb_network* net,
+                            const nb_weights* w, nb_precision prec,
+                            nb_fisher_out* out);
+/* forward only (transformed-net inference): probs n x classes, loss. */
+nb_status nb_session_forward(nb_session* s, const nb_network* net,
+                             const nb_weights* w, nb_precision prec,
+                             double* probs, double* loss);
+
+/* ---- candidate scheduler (evaluate_all, I/search.hpp:315-334) ------------ */
+/* Scores `count` candidate networks (all drawn with init_weights) on the
+ * given sessions -- one per GPU, all holding the same batch.  Identical
+ * networks are evaluated once; the rest are assigned to sessions by LPT on
+ * nb_fisher_flops and run by one host worker thread per session.  Results
+ * land in outs[i] regardless of assignment, so the output is independent of
+ * the number of sessions (the reference's jobs=k == jobs=1 guarantee,
+ * T/test_search.cpp:83-94). */
+nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessions,
+                      const nb_network* nets, int64_t count, nb_precision prec,
+                      nb_fisher_out* outs, nb_eval_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NB200_H */

@@ -1,0 +1,729 @@
+// nb200 engine: contexts, sessions, lowering and the Fisher / forward
+// pipelines behind the C ABI (include/nb200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace nb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear sticky-free errors
+  nb_status s = NB_ERR_CUDA;
+  if (e == cudaErrorMemoryAllocation) s = NB_ERR_OUT_OF_MEMORY;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+      e == cudaErrorNoKernelImageForDevice)
+    s = NB_ERR_NO_DEVICE;
+  fail(s, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (p) {
+    NB_CUDA(cudaDeviceSynchronize());
+    NB_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+  }
+  n = std::max<size_t>(n, 256);
+  NB_CUDA(cudaMalloc(&p, n));
+  bytes = n;
+}
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+void PinnedBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (p) {
+    NB_CUDA(cudaDeviceSynchronize());
+    cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  n = std::max<size_t>(n, 4096);
+  NB_CUDA(cudaMallocHost(&p, n));
+  bytes = n;
+}
+
+PinnedBuf::~PinnedBuf() {
+  if (p) cudaFreeHost(p);
+}
+
+cudaEvent_t Profiler::get() {
+  if (!pool_.empty()) {
+    cudaEvent_t e = pool_.back();
+    pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  NB_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Profiler::begin(cudaStream_t st) {
+  if (!on) return;
+  cur_ = get();
+  NB_CUDA(cudaEventRecord(cur_, st));
+}
+
+void Profiler::end(cudaStream_t st, const char* fam, double flops, double bytes) {
+  if (!on || !cur_) return;
+  cudaEvent_t b = get();
+  NB_CUDA(cudaEventRecord(b, st));
+  pending_.push_back({cur_, b, fam, flops, bytes});
+  cur_ = nullptr;
+}
+
+void Profiler::resolve() {
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    NB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    KStat& k = stats[p.fam];
+    k.launches += 1;
+    k.ms += ms;
+    k.flops += p.flops;
+    k.bytes += p.bytes;
+    pool_.push_back(p.a);
+    pool_.push_back(p.b);
+  }
+  pending_.clear();
+}
+
+Profiler::~Profiler() {
+  for (auto e : pool_) cudaEventDestroy(e);
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+}
+
+namespace {
+int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
+}  // namespace
+
+// Lowering of a (derived, repaired) network to kernel plans: per layer the
+// ConvSpec ranges (I/ir.hpp:54-57) become RangeDescs with packed-weight
+// offsets, each range gets a kernel family, and activations / Fisher
+// partials get arena offsets.
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
+  (void)prec;
+  NetPlan P;
+  const int64_t L = net.L();
+  for (int64_t l = 0; l < L; ++l) {
+    const Spec& s = net.specs[l];
+    LayerPlan lp;
+    ConvGeom& g = lp.geom;
+    g.N = int(n);
+    g.H = int(s.h);
+    g.W = int(s.w);
+    g.Ci = int(s.ci);
+    g.OH = int(s.oh());
+    g.OW = int(s.ow());
+    g.Co = int(s.co_eff());
+    g.KH = int(s.kh);
+    g.KW = int(s.kw);
+    g.S = int(s.stride);
+    g.P = int(s.pad);
+    auto rs = s.ranges();
+    if (int(rs.size()) > kMaxRanges)
+      fail(NB_ERR_UNSUPPORTED, "more than 16 channel ranges in one layer");
+    g.nranges = int(rs.size());
+    int64_t off = 0;
+    const int64_t taps = s.kh * s.kw;
+    for (int i = 0; i < g.nranges; ++i) {
+      RangeDesc& r = g.r[i];
+      r.b = int(rs[i].begin);
+      r.len = int(rs[i].end - rs[i].begin);
+      r.groups = int(rs[i].groups);
+      r.slice_co = r.len / r.groups;
+      r.slice_ci = int(s.ci / rs[i].groups);
+      r.wf_off = off;
+      r.wd_off = off;
+      off += align64(int64_t(r.len) * r.slice_ci * taps);
+      lp.family[i] = Family::Direct;
+    }
+    lp.wpack_floats = off;
+    lp.w_off = P.w_total;
+    P.w_total += off;
+    lp.act_floats = n * s.co_eff() * s.oh() * s.ow();
+    lp.act_off = P.act_total;
+    P.act_total += align64(lp.act_floats);
+    lp.tiles = (l == L - 1) ? 1 : dgrad_tiles(int(s.oh()), int(s.ow()));
+    lp.part_off = P.part_total;
+    P.part_total += align64(n * lp.tiles * s.co_eff());
+    P.dpre_floats = std::max(P.dpre_floats, lp.act_floats);
+    P.ch_total += s.co_eff();
+    lp.fprop_flops = 2.0 * double(n) * double(s.macs());
+    lp.dgrad_flops = l > 0 ? 2.0 * double(n) * double(s.macs()) : 0.0;
+    P.layers.push_back(lp);
+  }
+  return P;
+}
+
+void ctx_activate(nb_ctx* c) { NB_CUDA(cudaSetDevice(c->device)); }
+
+namespace {
+
+const double* ensure_z(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) {
+  auto key = std::make_pair(seed, stream);
+  auto& buf = c->zdev[key];
+  if (!buf) buf = std::make_unique<DevBuf>();
+  int64_t& have = c->zlen[key];
+  if (have < count) {
+    const std::vector<double>& z = z_stream(seed, stream, count);
+    buf->ensure(size_t(count) * 8);
+    NB_CUDA(cudaMemcpy(buf->p, z.data(), size_t(count) * 8, cudaMemcpyHostToDevice));
+    have = count;
+  }
+  return buf->as<double>();
+}
+
+}  // namespace
+
+void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
+                 bool backward, const RunOut& out) {
+  nb_ctx* c = s->ctx;
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  ctx_activate(c);
+  const Spec& s0 = net.specs.front();
+  if (s0.ci != s->ci || s0.h != s->h || s0.w != s->w)
+    fail(NB_ERR_SHAPE_MISMATCH, "network input shape does not match the session batch");
+  if (net.num_classes != s->num_classes)
+    fail(NB_ERR_CONFIG, "network class count does not match the session batch");
+  const int64_t N = s->n, L = net.L(), K = net.num_classes;
+  cudaStream_t st = c->stream;
+  NetPlan P = lower(net, N, prec);
+  const bool want_grads = out.grads != nullptr;
+
+  c->act.ensure(size_t(P.act_total) * 4);
+  c->wpack_f.ensure(size_t(P.w_total) * 4);
+  c->wpack_d.ensure(size_t(P.w_total) * 4);
+  c->part.ensure(size_t(P.part_total) * 8);
+  c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
+  c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
+  if (want_grads) c->gtmp.ensure(size_t(P.act_total) * 4);
+  // misc: probs N*K | ex_loss N | per_channel sum C | fisher table L
+  const int64_t misc_doubles = align64(N * K) + align64(N) + align64(P.ch_total) +
+                               align64(int64_t(L) * int64_t(sizeof(FisherLayer)) / 8 + 1);
+  c->misc.ensure(size_t(misc_doubles) * 8);
+  double* d_probs = c->misc.as<double>();
+  double* d_exloss = d_probs + align64(N * K);
+  double* d_perch = d_exloss + align64(N);
+  FisherLayer* d_ftab = reinterpret_cast<FisherLayer*>(d_perch + align64(P.ch_total));
+  float* act = c->act.as<float>();
+  float* wf = c->wpack_f.as<float>();
+  float* wd = c->wpack_d.as<float>();
+  double* part = c->part.as<double>();
+
+  // ---- weights: z-stream prefix (init_weights) or explicit, packed on device
+  int64_t wsrc_need = 0;
+  if (w && w->layer)
+    for (int64_t l = 0; l < L; ++l) wsrc_need += align64(net.specs[l].weight_count());
+  if (w && w->head) wsrc_need += align64(K * net.c_last());
+  if (wsrc_need) c->wsrc.ensure(size_t(wsrc_need) * 8);
+  int64_t wsrc_off = 0;
+  for (int64_t l = 0; l < L; ++l) {
+    const Spec& sp = net.specs[l];
+    const double* src;
+    double scale;
+    if (w && w->layer) {
+      double* dst = c->wsrc.as<double>() + wsrc_off;
+      NB_CUDA(cudaMemcpyAsync(dst, w->layer[l], size_t(sp.weight_count()) * 8,
+                              cudaMemcpyHostToDevice, st));
+      wsrc_off += align64(sp.weight_count());
+      src = dst;
+      scale = 1.0;
+    } else {
+      src = ensure_z(c, net.seed, l, sp.weight_count());
+      scale = 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw));  // I/nnet.hpp:65
+    }
+    const LayerPlan& lp = P.layers[l];
+    for (int r = 0; r < lp.geom.nranges; ++r) {
+      launch_pack_weights(src, scale, lp.geom, r, wf + lp.w_off, wd + lp.w_off, st);
+      c->launches++;
+    }
+  }
+  const double* head_src;
+  double head_scale;
+  if (w && w->head) {
+    double* dst = c->wsrc.as<double>() + wsrc_off;
+    NB_CUDA(cudaMemcpyAsync(dst, w->head, size_t(K * net.c_last()) * 8,
+                            cudaMemcpyHostToDevice, st));
+    head_src = dst;
+    head_scale = 1.0;
+  } else {
+    head_src = ensure_z(c, net.seed, L, K * net.c_last());
+    head_scale = 1.0 / std::sqrt(double(net.c_last()));  // I/nnet.hpp:72-73
+  }
+
+  // ---- forward (I/nnet.hpp:180-197)
+  const float* x = s->x.as<float>();
+  for (int64_t l = 0; l < L; ++l) {
+    const LayerPlan& lp = P.layers[l];
+    float* y = act + lp.act_off;
+    for (int r = 0; r < lp.geom.nranges; ++r) {
+      const RangeDesc& rd = lp.geom.r[r];
+      const double fl = 2.0 * double(N) * rd.len * lp.geom.OH * lp.geom.OW * rd.slice_ci *
+                        lp.geom.KH * lp.geom.KW;
+      const double by = 4.0 * (double(N) * lp.geom.H * lp.geom.W * lp.geom.Ci +
+                               double(rd.len) * rd.slice_ci * lp.geom.KH * lp.geom.KW +
+                               double(N) * lp.geom.OH * lp.geom.OW * rd.len);
+      c->prof.begin(st);
+      launch_fprop_direct(lp.geom, r, x, wf + lp.w_off, y, net.relu[l], st);
+      c->prof.end(st, "conv_fprop_direct", fl, by);
+      c->launches++;
+    }
+    x = y;
+  }
+
+  // ---- head (+ backward start)
+  const LayerPlan& last = P.layers[L - 1];
+  HeadArgs ha{};
+  ha.act = act + last.act_off;
+  ha.N = int(N);
+  ha.HW = last.geom.OH * last.geom.OW;
+  ha.C = last.geom.Co;
+  ha.K = int(K);
+  ha.head_src = head_src;
+  ha.head_scale = head_scale;
+  ha.labels = s->labels.as<int32_t>();
+  ha.probs = d_probs;
+  ha.ex_loss = d_exloss;
+  ha.backward = backward;
+  ha.relu_last = net.relu[L - 1];
+  ha.partial = backward ? part + last.part_off : nullptr;
+  ha.dpre = (backward && L > 1) ? c->dpre[0].as<float>() : nullptr;
+  ha.g_out = (backward && want_grads) ? c->gtmp.as<float>() + last.act_off : nullptr;
+  c->prof.begin(st);
+  launch_head(ha, st);
+  c->prof.end(st, "head", 0.0, 4.0 * double(last.act_floats) * (backward ? 3 : 1));
+  c->launches++;
+
+  if (backward) {
+    // ---- activation gradients with the fused Fisher epilogue (I/nnet.hpp:225-243)
+    int cur = 0;
+    for (int64_t l = L - 1; l >= 1; --l) {
+      const LayerPlan& lp = P.layers[l];
+      const LayerPlan& prev = P.layers[l - 1];
+      float* dpre_out = (l - 1 >= 1) ? c->dpre[cur ^ 1].as<float>() : nullptr;
+      float* g_out = want_grads ? c->gtmp.as<float>() + prev.act_off : nullptr;
+      const double by = 4.0 * (double(N) * lp.geom.OH * lp.geom.OW * lp.geom.Co +
+                               double(lp.wpack_floats) + 2.0 * double(prev.act_floats) +
+                               (dpre_out ? double(prev.act_floats) : 0.0));
+      c->prof.begin(st);
+      launch_dgrad_direct(lp.geom, c->dpre[cur].as<float>(), wd + lp.w_off,
+                          act + prev.act_off, net.relu[l - 1], dpre_out, g_out,
+                          part + prev.part_off, st);
+      c->prof.end(st, "conv_dgrad_direct_fisher", lp.dgrad_flops, by);
+      c->launches++;
+      cur ^= 1;
+    }
+    // ---- Fisher reduction (I/nnet.hpp:330-350)
+    c->host_io.ensure(size_t(L) * sizeof(FisherLayer));
+    FisherLayer* ht = c->host_io.as<FisherLayer>();
+    int64_t off = 0;
+    int max_c = 1;
+    for (int64_t l = 0; l < L; ++l) {
+      const LayerPlan& lp = P.layers[l];
+      ht[l] = FisherLayer{part + lp.part_off, lp.geom.Co, lp.tiles, off};
+      off += lp.geom.Co;
+      max_c = std::max(max_c, lp.geom.Co);
+    }
+    NB_CUDA(cudaMemcpyAsync(d_ftab, ht, size_t(L) * sizeof(FisherLayer),
+                            cudaMemcpyHostToDevice, st));
+    c->prof.begin(st);
+    launch_fisher_reduce(d_ftab, int(L), max_c, int(N), d_perch, st);
+    c->prof.end(st, "fisher_reduce", 0.0, 8.0 * double(P.part_total));
+    c->launches++;
+  }
+
+  // ---- results back to the host
+  std::vector<double> probs(static_cast<size_t>(N * K)), exl(static_cast<size_t>(N)),
+      perch(static_cast<size_t>(P.ch_total));
+  NB_CUDA(cudaMemcpyAsync(probs.data(), d_probs, probs.size() * 8, cudaMemcpyDeviceToHost, st));
+  NB_CUDA(cudaMemcpyAsync(exl.data(), d_exloss, exl.size() * 8, cudaMemcpyDeviceToHost, st));
+  if (backward)
+    NB_CUDA(cudaMemcpyAsync(perch.data(), d_perch, perch.size() * 8, cudaMemcpyDeviceToHost,
+                            st));
+  if (out.acts || out.grads) {
+    c->io.ensure(size_t(P.dpre_floats) * 8);
+    int64_t o = 0;
+    for (int64_t l = 0; l < L; ++l) {
+      const LayerPlan& lp = P.layers[l];
+      const ConvGeom& g = lp.geom;
+      for (int which = 0; which < 2; ++which) {
+        double* dst = which == 0 ? out.acts : out.grads;
+        if (!dst) continue;
+        const float* src =
+            (which == 0 ? act : c->gtmp.as<float>()) + lp.act_off;
+        launch_nhwc32_to_nchw64(src, c->io.as<double>(), N, g.Co, g.OH, g.OW, st);
+        c->launches++;
+        NB_CUDA(cudaMemcpyAsync(dst + o, c->io.p, size_t(lp.act_floats) * 8,
+                                cudaMemcpyDeviceToHost, st));
+      }
+      o += lp.act_floats;
+    }
+  }
+  NB_CUDA(cudaGetLastError());
+  NB_CUDA(cudaStreamSynchronize(st));
+  c->prof.resolve();
+
+  double lsum = 0.0;
+  for (int64_t i = 0; i < N; ++i) lsum += exl[size_t(i)];
+  if (out.loss) *out.loss = lsum / double(N);
+  if (out.probs) std::memcpy(out.probs, probs.data(), probs.size() * 8);
+  if (out.ex_loss) std::memcpy(out.ex_loss, exl.data(), exl.size() * 8);
+  if (backward) {
+    // per_layer / total in the reference's order (I/nnet.hpp:345-349)
+    double tot = 0.0;
+    int64_t o = 0;
+    for (int64_t l = 0; l < L; ++l) {
+      double layer = 0.0;
+      for (int64_t ch = 0; ch < P.layers[l].geom.Co; ++ch) layer += perch[size_t(o + ch)];
+      if (out.per_layer) out.per_layer[l] = layer;
+      o += P.layers[l].geom.Co;
+      tot += layer;
+    }
+    if (out.per_channel) std::memcpy(out.per_channel, perch.data(), perch.size() * 8);
+    if (out.total) *out.total = tot;
+  }
+}
+
+}  // namespace nb
+
+using namespace nb;
+
+namespace {
+
+nb_session* make_session(nb_ctx* c, const NetDesc& net, const nb_batch* b) {
+  if (!b || b->n < 1) fail(NB_ERR_CONFIG, "batch must hold at least one example");
+  const Spec& s0 = net.specs.front();
+  const int64_t per = s0.ci * s0.h * s0.w;
+  std::vector<double> xs;
+  std::vector<int32_t> ls;
+  const double* xp = b->inputs;
+  const int32_t* lp = b->labels;
+  if (!xp) {
+    xs.resize(size_t(b->n * per));
+    ls.resize(size_t(b->n));
+    make_batch(net, b->n, b->seed, xs.data(), ls.data());
+    xp = xs.data();
+    lp = ls.data();
+  } else {
+    if (!lp) fail(NB_ERR_CONFIG, "explicit batch inputs need labels");
+    for (int64_t i = 0; i < b->n; ++i)
+      if (lp[i] < 0 || lp[i] >= net.num_classes) fail(NB_ERR_CONFIG, "label out of range");
+  }
+  auto s = std::make_unique<nb_session>();
+  s->ctx = c;
+  s->n = b->n;
+  s->ci = s0.ci;
+  s->h = s0.h;
+  s->w = s0.w;
+  s->num_classes = net.num_classes;
+  s->seed = b->seed;
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  ctx_activate(c);
+  s->x.ensure(size_t(b->n * per) * 4);
+  s->labels.ensure(size_t(b->n) * 4);
+  c->io.ensure(size_t(b->n * per) * 8);
+  NB_CUDA(cudaMemcpyAsync(c->io.p, xp, size_t(b->n * per) * 8, cudaMemcpyHostToDevice,
+                          c->stream));
+  launch_nchw64_to_nhwc32(c->io.as<double>(), s->x.as<float>(), b->n, int(s0.ci), int(s0.h),
+                          int(s0.w), c->stream);
+  c->launches++;
+  NB_CUDA(cudaMemcpyAsync(s->labels.p, lp, size_t(b->n) * 4, cudaMemcpyHostToDevice,
+                          c->stream));
+  NB_CUDA(cudaStreamSynchronize(c->stream));
+  return s.release();
+}
+
+void need(const void* p, const char* what) {
+  if (!p) fail(NB_ERR_CONFIG, std::string("null ") + what);
+}
+
+// A one-layer network around a bare ConvSpec (for nb_conv_forward/dgrad).
+struct OneLayer {
+  nb_layer layer;
+  nb_network net;
+  explicit OneLayer(const nb_conv_spec* spec, int relu) {
+    layer.spec = *spec;
+    layer.relu = relu;
+    layer.reserved = 0;
+    net = nb_network{1, &layer, 2, 0};
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int nb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+nb_status nb_ctx_create(int device, nb_ctx** out) {
+  return guard([&] {
+    need(out, "output pointer");
+    int n = nb_device_count();
+    if (n < 1) fail(NB_ERR_NO_DEVICE, "no CUDA device visible: nb200 has no CPU fallback");
+    if (device < 0 || device >= n) fail(NB_ERR_NO_DEVICE, "device index out of range");
+    cudaDeviceProp prop{};
+    NB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+      fail(NB_ERR_NO_DEVICE, std::string("nb200 is built for sm_100a (B200); device is ") +
+                                 prop.name);
+    auto c = std::make_unique<nb_ctx>();
+    c->device = device;
+    NB_CUDA(cudaSetDevice(device));
+    NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c.release();
+  });
+}
+
+nb_status nb_ctx_destroy(nb_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStream_t st = ctx->stream;
+    delete ctx;
+    cudaStreamDestroy(st);
+  });
+}
+
+void* nb_ctx_stream(nb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+nb_status nb_ctx_set_profiling(nb_ctx* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "context");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx->prof.on = enable != 0;
+  });
+}
+
+nb_status nb_ctx_kernel_stats(nb_ctx* ctx, nb_kernel_stat* stats, int32_t cap, int32_t* count) {
+  return guard([&] {
+    need(ctx, "context");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    int32_t i = 0;
+    for (const auto& [name, k] : ctx->prof.stats) {
+      if (i < cap && stats) {
+        nb_kernel_stat& o = stats[i];
+        std::memset(&o, 0, sizeof(o));
+        std::strncpy(o.name, name.c_str(), sizeof(o.name) - 1);
+        o.launches = k.launches;
+        o.ms = k.ms;
+        o.flops = k.flops;
+        o.bytes = k.bytes;
+      }
+      ++i;
+    }
+    if (count) *count = i;
+  });
+}
+
+nb_status nb_ctx_reset_stats(nb_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "context");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx->prof.stats.clear();
+  });
+}
+
+int64_t nb_ctx_launch_count(nb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nb_status nb_session_create(nb_ctx* ctx, const nb_network* shape_net, const nb_batch* batch,
+                            nb_session** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output pointer");
+    NetDesc d = NetDesc::from(shape_net);
+    *out = make_session(ctx, d, batch);
+  });
+}
+
+nb_status nb_session_destroy(nb_session* s) {
+  return guard([&] {
+    if (!s) return;
+    std::lock_guard<std::recursive_mutex> lk(s->ctx->mu);
+    ctx_activate(s->ctx);
+    delete s;
+  });
+}
+
+nb_ctx* nb_session_ctx(nb_session* s) { return s ? s->ctx : nullptr; }
+
+nb_status nb_session_fisher(nb_session* s, const nb_network* net, const nb_weights* w,
+                            nb_precision prec, nb_fisher_out* out) {
+  return guard([&] {
+    need(s, "session");
+    need(out, "output");
+    NetDesc d = NetDesc::from(net);
+    RunOut ro;
+    ro.per_channel = out->per_channel;
+    ro.per_layer = out->per_layer;
+    ro.total = &out->total;
+    ro.loss = &out->loss;
+    ro.probs = out->probs;
+    run_network(s, d, w, prec, true, ro);
+    out->seed = s->seed;
+  });
+}
+
+nb_status nb_session_forward(nb_session* s, const nb_network* net, const nb_weights* w,
+                             nb_precision prec, double* probs, double* loss) {
+  return guard([&] {
+    need(s, "session");
+    NetDesc d = NetDesc::from(net);
+    RunOut ro;
+    ro.probs = probs;
+    ro.loss = loss;
+    run_network(s, d, w, prec, false, ro);
+  });
+}
+
+nb_status nb_fisher_potential(nb_ctx* ctx, const nb_network* net, const nb_weights* w,
+                              const nb_batch* batch, nb_precision prec, nb_fisher_out* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output");
+    NetDesc d = NetDesc::from(net);
+    std::unique_ptr<nb_session> s(make_session(ctx, d, batch));
+    RunOut ro;
+    ro.per_channel = out->per_channel;
+    ro.per_layer = out->per_layer;
+    ro.total = &out->total;
+    ro.loss = &out->loss;
+    ro.probs = out->probs;
+    run_network(s.get(), d, w, prec, true, ro);
+    out->seed = batch->seed;
+  });
+}
+
+nb_status nb_forward(nb_ctx* ctx, const nb_network* net, const nb_weights* w,
+                     const nb_batch* batch, nb_precision prec, double* probs,
+                     double* example_loss, double* loss) {
+  return guard([&] {
+    need(ctx, "context");
+    NetDesc d = NetDesc::from(net);
+    std::unique_ptr<nb_session> s(make_session(ctx, d, batch));
+    RunOut ro;
+    ro.probs = probs;
+    ro.ex_loss = example_loss;
+    ro.loss = loss;
+    run_network(s.get(), d, w, prec, false, ro);
+  });
+}
+
+nb_status nb_activation_gradients(nb_ctx* ctx, const nb_network* net, const nb_weights* w,
+                                  const nb_batch* batch, nb_precision prec, double* acts,
+                                  double* grads) {
+  return guard([&] {
+    need(ctx, "context");
+    NetDesc d = NetDesc::from(net);
+    std::unique_ptr<nb_session> s(make_session(ctx, d, batch));
+    RunOut ro;
+    ro.acts = acts;
+    ro.grads = grads;
+    run_network(s.get(), d, w, prec, grads != nullptr, ro);
+  });
+}
+
+// reference_conv / layer_forward over n images through the same fprop
+// kernels the network pipeline uses.
+nb_status nb_conv_forward(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* x,
+                          const double* w, double* y, int32_t relu, nb_precision prec) {
+  return guard([&] {
+    need(ctx, "context");
+    need(spec, "spec");
+    need(x, "input");
+    need(w, "weights");
+    need(y, "output");
+    OneLayer one(spec, relu);
+    NetDesc d = NetDesc::from(&one.net);
+    const Spec& s = d.specs[0];
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx_activate(ctx);
+    cudaStream_t st = ctx->stream;
+    NetPlan P = lower(d, n, prec);
+    const LayerPlan& lp = P.layers[0];
+    const int64_t in_cnt = n * s.ci * s.h * s.w, out_cnt = lp.act_floats;
+    ctx->io.ensure(size_t(std::max(in_cnt, out_cnt)) * 8);
+    ctx->gtmp.ensure(size_t(align64(in_cnt) + align64(out_cnt)) * 4);
+    ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
+    ctx->wpack_f.ensure(size_t(P.w_total) * 4);
+    ctx->wpack_d.ensure(size_t(P.w_total) * 4);
+    float* xin = ctx->gtmp.as<float>();
+    float* yout = xin + align64(in_cnt);
+    NB_CUDA(cudaMemcpyAsync(ctx->io.p, x, size_t(in_cnt) * 8, cudaMemcpyHostToDevice, st));
+    launch_nchw64_to_nhwc32(ctx->io.as<double>(), xin, n, int(s.ci), int(s.h), int(s.w), st);
+    NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8,
+                            cudaMemcpyHostToDevice, st));
+    for (int r = 0; r < lp.geom.nranges; ++r)
+      launch_pack_weights(ctx->wsrc.as<double>(), 1.0, lp.geom, r, ctx->wpack_f.as<float>(),
+                          ctx->wpack_d.as<float>(), st);
+    for (int r = 0; r < lp.geom.nranges; ++r) {
+      launch_fprop_direct(lp.geom, r, xin, ctx->wpack_f.as<float>(), yout, relu != 0, st);
+      ctx->launches++;
+    }
+    launch_nhwc32_to_nchw64(yout, ctx->io.as<double>(), n, lp.geom.Co, lp.geom.OH, lp.geom.OW,
+                            st);
+    NB_CUDA(cudaMemcpyAsync(y, ctx->io.p, size_t(out_cnt) * 8, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaGetLastError());
+    NB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+nb_status nb_conv_dgrad(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* dy,
+                        const double* w, double* dx, nb_precision prec) {
+  return guard([&] {
+    need(ctx, "context");
+    need(spec, "spec");
+    need(dy, "dy");
+    need(w, "weights");
+    need(dx, "dx");
+    OneLayer one(spec, 0);
+    NetDesc d = NetDesc::from(&one.net);
+    const Spec& s = d.specs[0];
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx_activate(ctx);
+    cudaStream_t st = ctx->stream;
+    NetPlan P = lower(d, n, prec);
+    const LayerPlan& lp = P.layers[0];
+    const int64_t in_cnt = n * s.ci * s.h * s.w, out_cnt = lp.act_floats;
+    ctx->io.ensure(size_t(std::max(in_cnt, out_cnt)) * 8);
+    ctx->gtmp.ensure(size_t(align64(in_cnt) + align64(out_cnt)) * 4);
+    ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
+    ctx->wpack_f.ensure(size_t(P.w_total) * 4);
+    ctx->wpack_d.ensure(size_t(P.w_total) * 4);
+    float* dxo = ctx->gtmp.as<float>();
+    float* dyi = dxo + align64(in_cnt);
+    NB_CUDA(cudaMemcpyAsync(ctx->io.p, dy, size_t(out_cnt) * 8, cudaMemcpyHostToDevice, st));
+    launch_nchw64_to_nhwc32(ctx->io.as<double>(), dyi, n, lp.geom.Co, lp.geom.OH, lp.geom.OW,
+                            st);
+    NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8,
+                            cudaMemcpyHostToDevice, st));
+    for (int r = 0; r < lp.geom.nranges; ++r)
+      launch_pack_weights(ctx->wsrc.as<double>(), 1.0, lp.geom, r, ctx->wpack_f.as<float>(),
+                          ctx->wpack_d.as<float>(), st);
+    launch_dgrad_direct(lp.geom, dyi, ctx->wpack_d.as<float>(), nullptr, false, nullptr, dxo,
+                        nullptr, st);
+    ctx->launches++;
+    launch_nhwc32_to_nchw64(dxo, ctx->io.as<double>(), n, int(s.ci), int(s.h), int(s.w), st);
+    NB_CUDA(cudaMemcpyAsync(dx, ctx->io.p, size_t(in_cnt) * 8, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaGetLastError());
+    NB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// The per-GPU engine: contexts, resident batches (sessions), the lowering of
+// a network to kernel plans, and the Fisher / forward pipelines.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace nb {
+
+void cuda_check(cudaError_t e, const char* what);
+#define NB_CUDA(x) ::nb::cuda_check((x), #x)
+
+// Growable device buffer (grown only between launches on the owning stream).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n);
+  ~DevBuf();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n);
+  ~PinnedBuf();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Kernel family of one output-channel range (the lowering of SURVEY 7:
+// ConvSpec range -> family).
+enum class Family { Direct = 0, TensorCore = 1 };
+
+// Lowered layer: geometry + per-range family + packed-weight offsets.
+struct LayerPlan {
+  ConvGeom geom{};
+  Family family[kMaxRanges]{};
+  int64_t wpack_floats = 0;  // floats of Wf (and of Wd) for this layer
+  int64_t w_off = 0;         // offset of this layer's Wf block in the weight arena
+  int64_t act_off = 0;       // offset (floats) of the layer's output activation
+  int64_t act_floats = 0;
+  int64_t part_off = 0;      // offset (doubles) of its Fisher partials
+  int tiles = 0;
+  double fprop_flops = 0, dgrad_flops = 0;
+};
+
+struct NetPlan {
+  std::vector<LayerPlan> layers;
+  int64_t act_total = 0, w_total = 0, part_total = 0, dpre_floats = 0;
+  int64_t ch_total = 0;  // sum_l C_l
+};
+
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec);
+
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+
+// Event-timed launch records (profiling) resolved at the end of each call.
+class Profiler {
+ public:
+  bool on = false;
+  void begin(cudaStream_t st);
+  void end(cudaStream_t st, const char* family, double flops, double bytes);
+  void resolve();  // stream must be synchronized
+  std::map<std::string, KStat> stats;
+  ~Profiler();
+
+ private:
+  struct Pending {
+    cudaEvent_t a, b;
+    std::string fam;
+    double flops, bytes;
+  };
+  std::vector<cudaEvent_t> pool_;
+  std::vector<Pending> pending_;
+  cudaEvent_t cur_ = nullptr;
+  cudaEvent_t get();
+};
+
+}  // namespace nb
+
+struct nb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::recursive_mutex mu;
+  nb::DevBuf act, wpack_f, wpack_d, part, misc, wsrc, dpre[2], gtmp, io;
+  nb::PinnedBuf host_io;
+  // device copies of z streams keyed by (seed, stream index)
+  std::map<std::pair<uint64_t, int64_t>, std::unique_ptr<nb::DevBuf>> zdev;
+  std::map<std::pair<uint64_t, int64_t>, int64_t> zlen;
+  nb::Profiler prof;
+  int64_t launches = 0;
+};
+
+struct nb_session {
+  nb_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int64_t ci = 0, h = 0, w = 0, num_classes = 0;
+  uint64_t seed = 0;
+  nb::DevBuf x;       // (N, H, W, Ci) fp32
+  nb::DevBuf labels;  // N int32
+};
+
+namespace nb {
+
+// Outputs requested from one pipeline run (host pointers, nullable).
+struct RunOut {
+  double* per_channel = nullptr;
+  double* per_layer = nullptr;
+  double* total = nullptr;
+  double* probs = nullptr;
+  double* ex_loss = nullptr;
+  double* loss = nullptr;
+  double* acts = nullptr;   // reference layout, see nb_activation_gradients
+  double* grads = nullptr;
+};
+
+// Runs forward (and, when `backward`, activation gradients + Fisher) of `net`
+// on the session's resident batch.
+void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
+                 bool backward, const RunOut& out);
+
+void ctx_activate(nb_ctx* c);
+
+}  // namespace nb

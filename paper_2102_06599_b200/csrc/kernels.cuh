@@ -1,0 +1,72 @@
+// Device-side parameter blocks and launchers shared by the nb200 kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nb {
+
+constexpr int kMaxRanges = 16;
+
+// One output-channel range of a ConvSpec (I/ir.hpp:54-57): channels
+// [b, b+len) in G groups of slice_co outputs, each reading slice_ci inputs.
+struct RangeDesc {
+  int b, len, groups, slice_co, slice_ci;
+  int64_t wf_off;  // offset (floats) of the fprop-packed weights Wf_r[tap][j][co_local]
+  int64_t wd_off;  // offset (floats) of the dgrad-packed weights Wd_r[tap][t][ci]
+};
+
+// Geometry of one conv layer over a batch, NHWC fp32 activations.
+struct ConvGeom {
+  int N, H, W, Ci, OH, OW, Co, KH, KW, S, P;
+  int nranges;
+  RangeDesc r[kMaxRanges];
+};
+
+// Pixel tile of the fused dgrad/Fisher epilogue: partial sums of A*g are
+// produced per (image, tile, channel) and combined in a fixed order.
+constexpr int kDgradTilePix = 64;
+inline int dgrad_tiles(int H, int W) { return (H * W + kDgradTilePix - 1) / kDgradTilePix; }
+
+// ---- launchers (kernels_simt.cu) -----------------------------------------
+void launch_nchw64_to_nhwc32(const double* src, float* dst, int64_t N, int C, int H, int W,
+                             cudaStream_t st);
+void launch_nhwc32_to_nchw64(const float* src, double* dst, int64_t N, int C, int H, int W,
+                             cudaStream_t st);
+void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
+                         float* wf, float* wd, cudaStream_t st);
+void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
+                         float* y, bool relu, cudaStream_t st);
+// g_in = convT(W, dpre) over all ranges; fused epilogue on the previous
+// layer's activation a_prev (nullable): partial[n][tile][ci] = sum A*g,
+// dpre_out = g * [a_prev > 0] (or g when !relu_prev), g_out = g (nullable).
+void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
+                         const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
+                         double* partial, cudaStream_t st);
+// GAP + linear head + softmax-CE (+ backward, + last-layer Fisher partial,
+// + the masked head gradient dpre of the last layer).
+struct HeadArgs {
+  const float* act;  // (N, HW, C) last layer output
+  int N, HW, C, K;
+  const double* head_src;  // K x C source (z-stream or explicit)
+  double head_scale;
+  const int32_t* labels;
+  double* probs;        // N x K
+  double* ex_loss;      // N
+  bool backward;
+  bool relu_last;
+  double* partial;      // N x C (sum_hw A*g), nullable
+  float* dpre;          // (N, HW, C) masked gradient, nullable
+  float* g_out;         // (N, HW, C) unmasked gradient, nullable
+};
+void launch_head(const HeadArgs& a, cudaStream_t st);
+// Fisher reduction: per (layer, channel) delta = sum_n (sum_tiles partial)^2 / (2N).
+struct FisherLayer {
+  const double* partial;
+  int C, tiles;
+  int64_t out_off;
+};
+void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,
+                          double* per_channel, cudaStream_t st);
+
+}  // namespace nb

@@ -1,0 +1,309 @@
+// fp32 FFMA kernels of the nb200 hot path: layout conversion, weight packing,
+// direct (grouped / depthwise / generic) conv fprop and the dgrad with the
+// fused Fisher epilogue, the fp64 head, and the deterministic Fisher
+// reduction.  Tensor-core-shaped ranges use kernels_tc.cu instead.
+//
+// Activations are NHWC fp32 in HBM (channels contiguous: coalesced across
+// output channels for fprop and across input channels for dgrad).
+#include <cfloat>
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace nb {
+
+namespace {
+
+__global__ void k_nchw64_to_nhwc32(const double* __restrict__ src, float* __restrict__ dst,
+                                   int64_t N, int C, int H, int W) {
+  const int64_t total = N * C * H * W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    // i indexes dst (n, h, w, c)
+    const int c = int(i % C);
+    int64_t p = i / C;
+    const int w = int(p % W);
+    p /= W;
+    const int h = int(p % H);
+    const int64_t n = p / H;
+    dst[i] = float(src[((n * C + c) * H + h) * W + w]);
+  }
+}
+
+__global__ void k_nhwc32_to_nchw64(const float* __restrict__ src, double* __restrict__ dst,
+                                   int64_t N, int C, int H, int W) {
+  const int64_t total = N * C * H * W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    // i indexes dst (n, c, h, w)
+    const int w = int(i % W);
+    int64_t p = i / W;
+    const int h = int(p % H);
+    p /= H;
+    const int c = int(p % C);
+    const int64_t n = p / C;
+    dst[i] = double(src[((n * H + h) * W + w) * C + c]);
+  }
+}
+
+// Weights of one range, from the dense (Co_eff, Ci, Kh, Kw) fp64 tensor of
+// the reference (I/nnet.hpp:65-67; grouped variants read only the diagonal
+// blocks, I/nnet.hpp:111-127), scaled (z * 1/sqrt(fan-in), or 1 for explicit
+// weights) in fp64 and rounded once to fp32, into two packings:
+//   Wf[tap][j][co_local]  (fprop: coalesced over output channels)
+//   Wd[tap][t][ci]        (dgrad: coalesced over input channels)
+__global__ void k_pack_weights(const double* __restrict__ src, double scale, int Ci, int taps,
+                               RangeDesc r, float* __restrict__ wf, float* __restrict__ wd) {
+  const int64_t total = int64_t(r.len) * r.slice_ci * taps;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int co_local = int(e % r.len);
+    const int64_t q = e / r.len;
+    const int j = int(q % r.slice_ci);
+    const int tap = int(q / r.slice_ci);
+    const int g = co_local / r.slice_co;
+    const int t = co_local - g * r.slice_co;
+    const int ci = g * r.slice_ci + j;
+    const int64_t co = r.b + co_local;
+    const float v = float(src[(co * Ci + ci) * taps + tap] * scale);
+    wf[r.wf_off + e] = v;
+    wd[r.wd_off + (int64_t(tap) * r.slice_co + t) * Ci + ci] = v;
+  }
+}
+
+// Direct conv fprop of one range: one thread per (output pixel, channel),
+// channel fastest.  out[n,oh,ow,b+c] = sum_{kh,kw,j} Wf[tap][j][c] *
+// x[n, s*oh-p+kh, s*ow-p+kw, g*slice_ci + j], padded taps skipped
+// (I/nnet.hpp:121-123).
+__global__ void k_fprop_direct(ConvGeom g, int ri, const float* __restrict__ x,
+                               const float* __restrict__ wbase, float* __restrict__ y,
+                               bool relu) {
+  const RangeDesc r = g.r[ri];
+  const float* __restrict__ wf = wbase + r.wf_off;
+  const int64_t total = int64_t(g.N) * g.OH * g.OW * r.len;
+  const int taps = g.KH * g.KW;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % r.len);
+    int64_t p = i / r.len;
+    const int ow = int(p % g.OW);
+    p /= g.OW;
+    const int oh = int(p % g.OH);
+    const int64_t n = p / g.OH;
+    const int grp = c / r.slice_co;
+    float acc = 0.f;
+    for (int kh = 0; kh < g.KH; ++kh) {
+      const int ih = g.S * oh - g.P + kh;
+      if (ih < 0 || ih >= g.H) continue;
+      for (int kw = 0; kw < g.KW; ++kw) {
+        const int iw = g.S * ow - g.P + kw;
+        if (iw < 0 || iw >= g.W) continue;
+        const float* __restrict__ xr =
+            x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci;
+        const float* __restrict__ wr = wf + int64_t(kh * g.KW + kw) * r.slice_ci * r.len + c;
+#pragma unroll 4
+        for (int j = 0; j < r.slice_ci; ++j) acc = fmaf(xr[j], wr[int64_t(j) * r.len], acc);
+      }
+    }
+    (void)taps;
+    if (relu) acc = acc > 0.f ? acc : 0.f;  // I/nnet.hpp:138-139
+    y[((n * g.OH + oh) * g.OW + ow) * g.Co + r.b + c] = acc;
+  }
+}
+
+// Direct dgrad (the dgrad MAC loop of I/nnet.hpp:235-243 as a gather):
+// g[n,ih,iw,ci] = sum_r sum_t sum_{kh,kw} Wd_r[tap][t][ci] *
+// dpre[n, oh, ow, b_r + (ci/slice_ci_r)*slice_co_r + t] with
+// oh = (ih+p-kh)/s when integral and inside the (cropped) output.
+// Block = 32 channels x 8 pixel lanes; grid = (ci tiles, pixel tiles, N).
+// Fused epilogue: partial[n][tile][ci] = sum over the tile of A*g in a fixed
+// order (deterministic), dpre_out = g masked by the previous layer's ReLU.
+__global__ void __launch_bounds__(256) k_dgrad_direct(
+    ConvGeom g, const float* __restrict__ dpre, const float* __restrict__ wbase,
+    const float* __restrict__ a_prev, bool relu_prev, float* __restrict__ dpre_out,
+    float* __restrict__ g_out, double* __restrict__ partial) {
+  __shared__ float red[8][33];
+  const int ci = blockIdx.x * 32 + threadIdx.x;
+  const int tile = blockIdx.y;
+  const int64_t n = blockIdx.z;
+  const int HW = g.H * g.W;
+  const int p0 = tile * kDgradTilePix;
+  const int p1 = min(HW, p0 + kDgradTilePix);
+  float contrib = 0.f;
+  if (ci < g.Ci) {
+    for (int p = p0 + threadIdx.y; p < p1; p += 8) {
+      const int ih = p / g.W, iw = p - (p / g.W) * g.W;
+      float acc = 0.f;
+      for (int ri = 0; ri < g.nranges; ++ri) {
+        const RangeDesc r = g.r[ri];
+        const float* __restrict__ wd = wbase + r.wd_off;
+        const int co0 = r.b + (ci / r.slice_ci) * r.slice_co;
+        for (int kh = 0; kh < g.KH; ++kh) {
+          const int th = ih + g.P - kh;
+          if (th < 0) break;
+          if (th % g.S) continue;
+          const int oh = th / g.S;
+          if (oh >= g.OH) continue;
+          for (int kw = 0; kw < g.KW; ++kw) {
+            const int tw = iw + g.P - kw;
+            if (tw < 0) break;
+            if (tw % g.S) continue;
+            const int ow = tw / g.S;
+            if (ow >= g.OW) continue;
+            const float* __restrict__ dr = dpre + ((n * g.OH + oh) * g.OW + ow) * g.Co + co0;
+            const float* __restrict__ wr =
+                wd + int64_t(kh * g.KW + kw) * r.slice_co * g.Ci + ci;
+#pragma unroll 4
+            for (int t = 0; t < r.slice_co; ++t) acc = fmaf(wr[int64_t(t) * g.Ci], dr[t], acc);
+          }
+        }
+      }
+      const int64_t idx = (n * HW + p) * g.Ci + ci;
+      if (g_out) g_out[idx] = acc;
+      if (a_prev) {
+        const float a = a_prev[idx];
+        contrib = fmaf(a, acc, contrib);
+        if (dpre_out) dpre_out[idx] = (relu_prev && !(a > 0.f)) ? 0.f : acc;  // I/nnet.hpp:229-233
+      } else if (dpre_out) {
+        dpre_out[idx] = acc;
+      }
+    }
+  }
+  if (!partial) return;
+  red[threadIdx.y][threadIdx.x] = contrib;
+  __syncthreads();
+  if (threadIdx.y == 0 && ci < g.Ci) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    partial[(n * gridDim.y + tile) * g.Ci + ci] = double(s);
+  }
+}
+
+// One block per example; fp64 throughout (head_logits/softmax/CE,
+// I/nnet.hpp:152-194; dz/dpool/g[L-1], I/nnet.hpp:209-224).
+__global__ void k_head(HeadArgs a) {
+  extern __shared__ double sm[];
+  double* pooled = sm;            // C
+  double* dpool = sm + a.C;       // C
+  double* z = sm + 2 * a.C;       // K
+  double* dz = z + a.K;           // K
+  const int n = blockIdx.x;
+  const float* act = a.act + int64_t(n) * a.HW * a.C;
+  for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < a.HW; ++j) s += double(act[int64_t(j) * a.C + i]);
+    pooled[i] = s / double(a.HW);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < a.C; ++i) s += (a.head_src[int64_t(k) * a.C + i] * a.head_scale) * pooled[i];
+    z[k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = z[0];
+    for (int k = 0; k < a.K; ++k) m = fmax(m, z[k]);
+    double sum = 0.0;
+    for (int k = 0; k < a.K; ++k) sum += (dz[k] = exp(z[k] - m));
+    for (int k = 0; k < a.K; ++k) dz[k] /= sum;
+    const int y = a.labels[n];
+    a.ex_loss[n] = -log(fmax(dz[y], 1e-300));
+    for (int k = 0; k < a.K; ++k) a.probs[int64_t(n) * a.K + k] = dz[k];
+    dz[y] -= 1.0;
+    for (int k = 0; k < a.K; ++k) dz[k] /= double(a.N);
+  }
+  __syncthreads();
+  if (!a.backward) return;
+  for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < a.K; ++k) s += (a.head_src[int64_t(k) * a.C + i] * a.head_scale) * dz[k];
+    dpool[i] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+    const double gv = dpool[i] / double(a.HW);
+    const float gf = float(gv);
+    double s = 0.0;
+    for (int j = 0; j < a.HW; ++j) {
+      const int64_t idx = (int64_t(n) * a.HW + j) * a.C + i;
+      const float av = a.act[idx];
+      s += double(av) * gv;
+      if (a.dpre) a.dpre[idx] = (a.relu_last && !(av > 0.f)) ? 0.f : gf;
+      if (a.g_out) a.g_out[idx] = gf;
+    }
+    if (a.partial) a.partial[int64_t(n) * a.C + i] = s;
+  }
+}
+
+// delta[l][c] = (sum_n s_nc^2) / (2N), s_nc = -sum_tiles partial (fixed
+// order), I/nnet.hpp:330-345.
+__global__ void k_fisher_reduce(const FisherLayer* __restrict__ layers, int N,
+                                double* __restrict__ per_channel) {
+  const FisherLayer L = layers[blockIdx.y];
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.C; c += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int n = 0; n < N; ++n) {
+      double s = 0.0;
+      for (int t = 0; t < L.tiles; ++t) s -= L.partial[(int64_t(n) * L.tiles + t) * L.C + c];
+      acc += s * s;
+    }
+    per_channel[L.out_off + c] = acc / (2.0 * double(N));
+  }
+}
+
+int grid_for(int64_t total, int block) {
+  int64_t g = (total + block - 1) / block;
+  const int64_t cap = 148 * 32;
+  return int(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+void launch_nchw64_to_nhwc32(const double* src, float* dst, int64_t N, int C, int H, int W,
+                             cudaStream_t st) {
+  const int64_t total = N * C * H * W;
+  k_nchw64_to_nhwc32<<<grid_for(total, 256), 256, 0, st>>>(src, dst, N, C, H, W);
+}
+
+void launch_nhwc32_to_nchw64(const float* src, double* dst, int64_t N, int C, int H, int W,
+                             cudaStream_t st) {
+  const int64_t total = N * C * H * W;
+  k_nhwc32_to_nchw64<<<grid_for(total, 256), 256, 0, st>>>(src, dst, N, C, H, W);
+}
+
+void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
+                         float* wf, float* wd, cudaStream_t st) {
+  const RangeDesc& r = g.r[range];
+  const int taps = g.KH * g.KW;
+  const int64_t total = int64_t(r.len) * r.slice_ci * taps;
+  k_pack_weights<<<grid_for(total, 256), 256, 0, st>>>(src, scale, g.Ci, taps, r, wf, wd);
+}
+
+void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
+                         float* y, bool relu, cudaStream_t st) {
+  const int64_t total = int64_t(g.N) * g.OH * g.OW * g.r[range].len;
+  k_fprop_direct<<<grid_for(total, 256), 256, 0, st>>>(g, range, x, wbase, y, relu);
+}
+
+void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
+                         const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
+                         double* partial, cudaStream_t st) {
+  dim3 grid((g.Ci + 31) / 32, dgrad_tiles(g.H, g.W), g.N);
+  k_dgrad_direct<<<grid, dim3(32, 8), 0, st>>>(g, dpre, wbase, a_prev, relu_prev, dpre_out,
+                                               g_out, partial);
+}
+
+void launch_head(const HeadArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * size_t(a.C) + 2 * size_t(a.K));
+  k_head<<<a.N, 256, smem, st>>>(a);
+}
+
+void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,
+                          double* per_channel, cudaStream_t st) {
+  dim3 grid((max_c + 127) / 128, L);
+  k_fisher_reduce<<<grid, 128, 0, st>>>(layers_dev, N, per_channel);
+}
+
+}  // namespace nb
