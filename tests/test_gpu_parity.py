@@ -1,0 +1,222 @@
+"""GPU parity tests: the sm_100a kernels (through the C ABI) against the
+reference's golden fixtures and the fp64 oracle restatement.
+
+Tolerances (fp32-accurate mode, NB_PREC_FP32 / NB_PREC_SIMT):
+  * conv outputs on small integers: bit-exact (every partial sum < 2^24);
+  * conv outputs on real data: |gpu - ref| <= 2e-6 * (sum |w||x| per output);
+  * Fisher totals: 1e-5 relative; per layer 1e-4 relative; per channel
+    1e-4 of the layer total; loss 1e-6 relative; probs 1e-6 absolute.
+The TF32 throughput mode is checked against 5e-3 on totals.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+import paper_2102_06599_b200 as nb
+from paper_2102_06599_b200 import ChannelSplit, ConvSpec, Layer, Network, Precision
+
+pytestmark = pytest.mark.gpu
+
+GOLD_CONV = golden("conv_cases.json")["cases"]
+GOLD_FISHER = golden("fisher_nets.json")["nets"]
+EXACT_PRECS = [Precision.FP32, Precision.SIMT]
+
+
+def _inputs(seed, spec):
+    rng = np.random.default_rng(seed)
+    x = rng.integers(-3, 4, size=(spec.ci, spec.h, spec.w)).astype(np.int64)
+    w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(np.int64)
+    return x, w
+
+
+@pytest.mark.parametrize("prec", EXACT_PRECS)
+@pytest.mark.parametrize("case", GOLD_CONV, ids=lambda c: str(c["seed"]))
+def test_conv_matches_reference_conv(ctx, case, prec):
+    spec = ConvSpec.from_json(case["spec"])
+    x, w = _inputs(case["seed"], spec)
+    y = nb.reference_conv(spec, x.astype(np.float64), w.astype(np.float64), precision=prec,
+                          ctx=ctx)
+    assert np.array_equal(y.ravel(), np.asarray(case["out_int"], np.float64))
+    xf, wf = x * 0.37, w * 1.3
+    yf = nb.reference_conv(spec, xf, wf, precision=prec, ctx=ctx)
+    scale = nb.reference_conv(spec, np.abs(xf), np.abs(wf), precision=Precision.SIMT, ctx=ctx)
+    assert np.all(np.abs(yf.ravel() - case["out_f64"]) <= 2e-6 * scale.ravel() + 1e-30)
+
+
+def test_conv_kats_and_batching(ctx):
+    """T/test_interp.cpp KATs, batched with distinct images per example."""
+    s = ConvSpec(4, 4, 1, 1, groups=2)
+    x = np.stack([np.array([1, 10, 100, 1000.]).reshape(4, 1, 1) * k for k in (1, 2, 3)])
+    y = nb.reference_conv(s, x, np.ones((4, 4, 1, 1)), ctx=ctx)
+    assert y[:, :, 0, 0].tolist() == [[11, 11, 1100, 1100], [22, 22, 2200, 2200],
+                                      [33, 33, 3300, 3300]]
+    s = ConvSpec(1, 1, 2, 2, 3, 3, 1, 1)
+    y = nb.reference_conv(s, np.arange(1, 5.).reshape(1, 2, 2), np.ones((1, 1, 3, 3)), ctx=ctx)
+    assert y.ravel().tolist() == [10, 10, 10, 10]
+
+
+@pytest.mark.parametrize("prec", EXACT_PRECS)
+def test_dgrad_matches_oracle(ctx, oracle, prec):
+    rng = np.random.default_rng(3)
+    for case in GOLD_CONV:
+        spec = ConvSpec.from_json(case["spec"])
+        dy = rng.integers(-3, 4, size=spec.output_shape()).astype(np.float64)
+        w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(
+            np.float64)
+        got = nb.conv_dgrad(spec, dy, w, precision=prec, ctx=ctx)
+        want = oracle.conv_dgrad(spec, dy, w)
+        assert np.array_equal(got, want), case["spec"]
+
+
+@pytest.mark.parametrize("prec", EXACT_PRECS)
+@pytest.mark.parametrize("case", GOLD_FISHER, ids=lambda c: c["name"])
+def test_fisher_matches_reference_golden(ctx, case, prec):
+    net = Network.from_json(case["network"])
+    batch = nb.make_batch(net, case["n"], case["batch_seed"])
+    rep = nb.fisher_potential(net, batch, precision=prec, ctx=ctx)
+    assert math.isclose(rep.total, case["total"], rel_tol=1e-5), (rep.total, case["total"])
+    np.testing.assert_allclose(rep.per_layer, case["per_layer"], rtol=1e-4)
+    scale = max(case["per_layer"])
+    np.testing.assert_allclose(np.concatenate(rep.per_channel), case["per_channel"], rtol=0,
+                               atol=1e-4 * scale)
+    assert math.isclose(rep.loss, case["loss"], rel_tol=1e-6)
+    np.testing.assert_allclose(rep.probs.ravel(), case["probs"], atol=1e-6)
+    assert rep.seed == case["batch_seed"]
+
+
+def test_tf32_mode_within_stated_tolerance(ctx):
+    for case in GOLD_FISHER:
+        net = Network.from_json(case["network"])
+        batch = nb.make_batch(net, case["n"], case["batch_seed"])
+        rep = nb.fisher_potential(net, batch, precision=Precision.TF32, ctx=ctx)
+        assert math.isclose(rep.total, case["total"], rel_tol=5e-3), case["name"]
+
+
+def _feature_net(seed=11):
+    return Network([
+        Layer(ConvSpec(3, 8, 9, 9, 3, 3, 2, 1)),
+        Layer(ConvSpec(8, 8, 5, 5, 3, 3, 1, 1, groups=2, spatial_div_h=5), relu=False),
+        Layer(ConvSpec(8, 6, 1, 5, 1, 3, 1, 0,
+                       channel_splits=[ChannelSplit(0, 2, 2), ChannelSplit(2, 6, 1)])),
+        Layer(ConvSpec(6, 6, 1, 3, 3, 3, 1, 1, groups=6)),
+    ], num_classes=5, seed=seed)
+
+
+@pytest.mark.parametrize("prec", EXACT_PRECS)
+def test_activation_gradients_match_oracle(ctx, oracle, prec):
+    net = _feature_net()
+    batch = nb.make_batch(net, 3, 4)
+    acts, grads = nb.activation_gradients(net, batch, precision=prec, ctx=ctx)
+    o = oracle.fisher(net, 3, batch=batch, grads=True)
+    off = 0
+    for a, g in zip(acts, grads):
+        k = a.size
+        ra, rg = o["acts"][off:off + k], o["grads"][off:off + k]
+        np.testing.assert_allclose(a.ravel(), ra, rtol=1e-5, atol=1e-6 * np.abs(ra).max())
+        np.testing.assert_allclose(g.ravel(), rg, rtol=1e-4, atol=1e-5 * np.abs(rg).max())
+        off += k
+
+
+def test_gradients_agree_with_finite_differences(ctx, oracle):
+    """acceptance criterion 5 (T/acceptance.cpp:333-369): the GPU's analytic
+    activation gradients against central differences of the fp64 loss."""
+    net = Network([Layer(ConvSpec(2, 4, 5, 5, 3, 3, 1, 1)), Layer(ConvSpec(4, 4, 5, 5, 3, 3, 1, 1)),
+                   Layer(ConvSpec(4, 3, 5, 5))], num_classes=4, seed=42)
+    batch = nb.make_batch(net, 3, 11)
+    acts, grads = nb.activation_gradients(net, batch, ctx=ctx)
+    net.init_weights()
+    eps = 1e-5
+    probes = 0
+    for l in range(len(net.layers)):
+        n = l % 3
+        sub = Network(net.layers[l + 1:], num_classes=4, seed=42) if l + 1 < len(net.layers) else None
+        for p in range(6):
+            i = (p * 17 + l * 5) % acts[l][n].size
+            loss = []
+            for sgn in (1, -1):
+                a = acts[l][n].ravel().copy()
+                a[i] += sgn * eps
+                a = a.reshape(acts[l][n].shape)
+                if sub is None:
+                    z = net.head @ a.reshape(a.shape[0], -1).mean(axis=1)
+                else:
+                    sub.weights = net.weights[l + 1:]
+                    sub.head = net.head
+                    from paper_2102_06599_b200.api import Batch
+                    fwd = oracle.fisher(sub, 1, batch=Batch(a[None], batch.labels[n:n + 1], 0))
+                    z = None
+                    loss.append(fwd["loss"])
+                    continue
+                pz = np.exp(z - z.max())
+                pz /= pz.sum()
+                loss.append(-math.log(max(pz[batch.labels[n]], 1e-300)))
+            fd = (loss[0] - loss[1]) / (2 * eps) / 3.0  # other examples' terms cancel
+            g = grads[l][n].ravel()[i]
+            assert abs(g - fd) <= 1e-4 * max(abs(fd), 1e-3), (l, i, g, fd)
+            probes += 1
+    assert probes == 18
+
+
+def test_zero_weights_and_relu_killed(ctx):
+    """T/test_nnet.cpp:35-44, :145-157, :180-186."""
+    net = Network([Layer(ConvSpec(2, 4, 5, 5, 3, 3, 1, 1)), Layer(ConvSpec(4, 4, 5, 5, 3, 3, 1, 1)),
+                   Layer(ConvSpec(4, 3, 5, 5))], num_classes=4, seed=42)
+    net.init_weights()
+    zero = net.copy()
+    zero.weights = [np.zeros_like(w) for w in net.weights]
+    zero.head = np.zeros_like(net.head)
+    batch = nb.make_batch(net, 8, 1)
+    rep = nb.fisher_potential(zero, batch, ctx=ctx)
+    assert math.isclose(rep.loss, math.log(4.0), rel_tol=1e-12)
+    assert rep.total == 0.0
+    killed = net.copy()
+    killed.weights[1] = np.full_like(net.weights[1], -10.0)
+    acts, grads = nb.activation_gradients(killed, nb.make_batch(net, 2, 3), ctx=ctx)
+    assert np.all(acts[1] == 0.0)
+    assert np.all(grads[0] == 0.0)
+
+
+def test_determinism_and_exact_ties(ctx):
+    """Identical networks score bit-identically, so fisher_accepts(origin,
+    origin) holds exactly (T/test_nnet.cpp:188-200)."""
+    case = GOLD_FISHER[0]
+    net = Network.from_json(case["network"])
+    batch = nb.make_batch(net, 8, 1)
+    a = nb.fisher_potential(net, batch, ctx=ctx)
+    b = nb.fisher_potential(net, batch, ctx=ctx)
+    assert a.total == b.total
+    assert all(np.array_equal(x, y) for x, y in zip(a.per_channel, b.per_channel))
+    assert nb.fisher_accepts(a, b) and nb.legality_fisher(net, net, batch, ctx=ctx)
+
+
+def test_session_and_scheduler_match_single_calls(ctx):
+    """evaluate (the evaluate_all replacement) == per-network calls, with
+    duplicates answered by dedupe (T/test_search.cpp:83-94 analogue)."""
+    base = Network.from_json(GOLD_FISHER[1]["network"])
+    batch = nb.make_batch(base, 4, 1)
+    variants = []
+    for b, g in [(1, 1), (2, 1), (1, 2), (1, 1), (2, 1)]:
+        n = base.copy()
+        n.layers[1].spec.bottleneck_out = b
+        n.layers[2].spec.groups = g
+        nb.repair_network(n)
+        variants.append(n)
+    sess = nb.Session(base, batch, ctx=ctx)
+    reps, stats = nb.evaluate([sess], variants)
+    assert stats.evaluated == 3 and stats.deduplicated == 2
+    for n, r in zip(variants, reps):
+        single = nb.fisher_potential(n, batch, ctx=ctx)
+        assert single.total == r.total
+        assert sess.fisher(n).total == r.total
+
+
+def test_larger_chain_matches_oracle(ctx, oracle):
+    """A 10-layer 16->32 channel chain at N=4 (the mid10 shape, larger batch)."""
+    net = Network.from_json([c for c in GOLD_FISHER if c["name"] == "mid10"][0]["network"])
+    batch = nb.make_batch(net, 4, 2)
+    rep = nb.fisher_potential(net, batch, ctx=ctx)
+    o = oracle.fisher(net, 4, batch=batch)
+    assert math.isclose(rep.total, o["total"], rel_tol=1e-5)
+    np.testing.assert_allclose(rep.per_layer, o["per_layer"], rtol=1e-4)
