@@ -103,15 +103,34 @@ Profiler::~Profiler() {
 
 namespace {
 int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
+
+// Largest N tile that divides the per-group width and still yields >= 2
+// waves of tiles on 148 SMs (else the smallest legal one).
+int pick_bn(int n_per_group, int groups, int m_tiles, bool split3) {
+  static const int o3[] = {128, 64, 32};
+  static const int o1[] = {256, 128, 64, 32};
+  const int* o = split3 ? o3 : o1;
+  const int no = split3 ? 3 : 4;
+  int smallest = 0;
+  for (int i = 0; i < no; ++i) {
+    if (n_per_group % o[i]) continue;
+    smallest = o[i];
+    if (int64_t(m_tiles) * groups * (n_per_group / o[i]) >= 2 * 148) return o[i];
+  }
+  return smallest;
+}
 }  // namespace
 
-// Lowering of a (derived, repaired) network to kernel plans: per layer the
-// ConvSpec ranges (I/ir.hpp:54-57) become RangeDescs with packed-weight
-// offsets, each range gets a kernel family, and activations / Fisher
-// partials get arena offsets.
+// Lowering of a (derived, repaired) network to kernel plans (SURVEY 7
+// "Lowering design"): per layer the ConvSpec ranges (I/ir.hpp:54-57) become
+// RangeDescs; each range's fprop and the layer's dgrad get a kernel family --
+// tcgen05 implicit GEMM when the range is tensor-core shaped (32-channel K
+// chunks, 16-aligned N), the direct FFMA kernels otherwise -- plus packed-
+// weight, activation and Fisher-partial arena offsets.
 NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
-  (void)prec;
   NetPlan P;
+  const bool tc_on = prec != NB_PREC_SIMT;
+  P.split3 = prec == NB_PREC_FP32;
   const int64_t L = net.L();
   for (int64_t l = 0; l < L; ++l) {
     const Spec& s = net.specs[l];
@@ -133,7 +152,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
       fail(NB_ERR_UNSUPPORTED, "more than 16 channel ranges in one layer");
     g.nranges = int(rs.size());
     int64_t off = 0;
-    const int64_t taps = s.kh * s.kw;
+    const int taps = int(s.kh * s.kw);
     for (int i = 0; i < g.nranges; ++i) {
       RangeDesc& r = g.r[i];
       r.b = int(rs[i].begin);
@@ -141,10 +160,83 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
       r.groups = int(rs[i].groups);
       r.slice_co = r.len / r.groups;
       r.slice_ci = int(s.ci / rs[i].groups);
+      const int64_t used = int64_t(r.len) * r.slice_ci * taps;
       r.wf_off = off;
+      off += align64(used);
       r.wd_off = off;
-      off += align64(int64_t(r.len) * r.slice_ci * taps);
+      off += align64(used);
       lp.family[i] = Family::Direct;
+      if (tc_on && (g.S == 1 || g.S == 2) && r.slice_ci % 32 == 0 && r.b % 16 == 0 &&
+          g.Co % 4 == 0) {
+        tc::TcArgs t{};
+        if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
+          const int bn = pick_bn(r.slice_co, r.groups, t.m_tiles, P.split3);
+          if (bn) {
+            t.mode = 0;
+            t.n_tiles_per_group = r.slice_co / bn;
+            t.n_tiles = r.groups * t.n_tiles_per_group;
+            t.taps_h = g.KH;
+            t.taps_w = g.KW;
+            t.S = g.S;
+            t.P = g.P;
+            t.a_cblocks = r.slice_ci / 32;
+            t.a_c_base = 0;
+            t.a_c_per_group = r.slice_ci;
+            t.b_k_per_tap = r.slice_ci;
+            t.b_row_base = 0;
+            t.b_row_per_group = r.slice_co;
+            t.out_ld = g.Co;
+            t.out_c_base = r.b;
+            t.out_c_per_group = r.slice_co;
+            TcPlan& tp = lp.tcf[i];
+            tp.bn = bn;
+            tp.tile = t;
+            tp.w_n = align64(used);
+            tp.w_off = off;
+            tp.b_rows = r.len;
+            tp.b_k = taps * r.slice_ci;
+            off += 2 * tp.w_n;
+            lp.family[i] = Family::TensorCore;
+          }
+        }
+      }
+    }
+    if (l >= 1 && tc_on && g.nranges == 1 && g.S == 1 && g.r[0].slice_co % 32 == 0 &&
+        g.Ci % 4 == 0) {
+      const RangeDesc& r = g.r[0];
+      tc::TcArgs t{};
+      if (tc::plan_tiles(g.H, g.W, g.N, 1, t)) {
+        const int bn = pick_bn(r.slice_ci, r.groups, t.m_tiles, P.split3);
+        if (bn) {
+          t.mode = 1;
+          t.n_tiles_per_group = r.slice_ci / bn;
+          t.n_tiles = r.groups * t.n_tiles_per_group;
+          t.taps_h = g.KH;
+          t.taps_w = g.KW;
+          t.S = 1;
+          t.P = g.P;
+          t.a_cblocks = r.slice_co / 32;
+          t.a_c_base = r.b;
+          t.a_c_per_group = r.slice_co;
+          t.b_k_per_tap = r.slice_co;
+          t.b_row_base = 0;
+          t.b_row_per_group = r.slice_ci;
+          t.out_ld = g.Ci;
+          t.out_c_base = 0;
+          t.out_c_per_group = r.slice_ci;
+          t.part_ld = g.Ci;
+          t.part_tiles_per_img = t.BNI == 1 ? t.tiles_h * t.tiles_w : 1;
+          TcPlan& tp = lp.tcd;
+          tp.bn = bn;
+          tp.tile = t;
+          tp.w_n = align64(int64_t(g.Ci) * taps * r.slice_co);
+          tp.w_off = off;
+          tp.b_rows = g.Ci;
+          tp.b_k = taps * r.slice_co;
+          off += 2 * tp.w_n;
+          lp.dgrad_family = Family::TensorCore;
+        }
+      }
     }
     lp.wpack_floats = off;
     lp.w_off = P.w_total;
@@ -152,14 +244,25 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
     lp.act_floats = n * s.co_eff() * s.oh() * s.ow();
     lp.act_off = P.act_total;
     P.act_total += align64(lp.act_floats);
-    lp.tiles = (l == L - 1) ? 1 : dgrad_tiles(int(s.oh()), int(s.ow()));
-    lp.part_off = P.part_total;
-    P.part_total += align64(n * lp.tiles * s.co_eff());
     P.dpre_floats = std::max(P.dpre_floats, lp.act_floats);
     P.ch_total += s.co_eff();
     lp.fprop_flops = 2.0 * double(n) * double(s.macs());
     lp.dgrad_flops = l > 0 ? 2.0 * double(n) * double(s.macs()) : 0.0;
     P.layers.push_back(lp);
+  }
+  // Fisher partials of layer l are produced by the dgrad of layer l+1 (or the
+  // head for the last layer); their tiling follows that kernel.
+  for (int64_t l = 0; l < L; ++l) {
+    LayerPlan& lp = P.layers[l];
+    if (l == L - 1) {
+      lp.tiles = 1;
+    } else {
+      const LayerPlan& nx = P.layers[l + 1];
+      lp.tiles = nx.dgrad_family == Family::TensorCore ? nx.tcd.tile.part_tiles_per_img
+                                                       : dgrad_tiles(lp.geom.OH, lp.geom.OW);
+    }
+    lp.part_off = P.part_total;
+    P.part_total += align64(n * lp.tiles * lp.geom.Co);
   }
   return P;
 }
@@ -182,6 +285,94 @@ const double* ensure_z(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) 
   return buf->as<double>();
 }
 
+void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
+                cudaStream_t st) {
+  float* base = c->wpack.as<float>() + lp.w_off;
+  for (int r = 0; r < lp.geom.nranges; ++r) {
+    PackDst d{base, base, nullptr, nullptr, nullptr, nullptr};
+    if (lp.family[r] == Family::TensorCore) {
+      d.tcf_hi = base + lp.tcf[r].w_off;
+      d.tcf_lo = d.tcf_hi + lp.tcf[r].w_n;
+    }
+    if (r == 0 && lp.dgrad_family == Family::TensorCore) {
+      d.tcd_hi = base + lp.tcd.w_off;
+      d.tcd_lo = d.tcd_hi + lp.tcd.w_n;
+    }
+    launch_pack_weights(src, scale, lp.geom, r, d, st);
+    c->launches++;
+  }
+}
+
+void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
+               const float* A, int AC, int AW, int AH, int AN, const float* whi,
+               cudaStream_t st) {
+  tc::TcLaunch L;
+  L.args = args;
+  L.bn = tp.bn;
+  L.split3 = split3;
+  L.num_sms = c->num_sms;
+  if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
+    fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  NB_CUDA(tc::launch(L, st));
+  c->launches++;
+}
+
+// One layer's fprop (all ranges): y = relu?(conv(x)).
+void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* x, float* y,
+                 bool relu, cudaStream_t st) {
+  const ConvGeom& g = lp.geom;
+  float* base = c->wpack.as<float>() + lp.w_off;
+  for (int r = 0; r < g.nranges; ++r) {
+    const RangeDesc& rd = g.r[r];
+    const double fl =
+        2.0 * double(g.N) * rd.len * g.OH * g.OW * rd.slice_ci * g.KH * g.KW;
+    const double by = 4.0 * (double(g.N) * g.H * g.W * g.Ci +
+                             double(rd.len) * rd.slice_ci * g.KH * g.KW +
+                             double(g.N) * g.OH * g.OW * rd.len);
+    c->prof.begin(st);
+    if (lp.family[r] == Family::TensorCore) {
+      tc::TcArgs a = lp.tcf[r].tile;
+      a.out = y;
+      a.relu = relu ? 1 : 0;
+      launch_tc(c, lp.tcf[r], a, P.split3, x, g.Ci, g.W, g.H, g.N, base + lp.tcf[r].w_off, st);
+      c->prof.end(st, P.split3 ? "conv_fprop_tc_3xtf32" : "conv_fprop_tc_tf32", fl, by);
+    } else {
+      launch_fprop_direct(g, r, x, base, y, relu, st);
+      c->launches++;
+      c->prof.end(st, "conv_fprop_direct", fl, by);
+    }
+  }
+}
+
+// One layer's dgrad with the fused epilogue on the previous layer's output.
+void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* dpre,
+                 const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
+                 double* partial, cudaStream_t st) {
+  const ConvGeom& g = lp.geom;
+  float* base = c->wpack.as<float>() + lp.w_off;
+  const double prev_floats = double(g.N) * g.H * g.W * g.Ci;
+  const double by = 4.0 * (double(g.N) * g.OH * g.OW * g.Co + double(lp.wpack_floats) / 6.0 +
+                           (a_prev ? prev_floats : 0.0) + (dpre_out ? prev_floats : 0.0) +
+                           (g_out ? prev_floats : 0.0));
+  c->prof.begin(st);
+  if (lp.dgrad_family == Family::TensorCore) {
+    tc::TcArgs a = lp.tcd.tile;
+    a.out = g_out;
+    a.g_out = g_out;
+    a.a_prev = a_prev;
+    a.dpre_out = dpre_out;
+    a.partial = partial;
+    a.relu_prev = relu_prev ? 1 : 0;
+    launch_tc(c, lp.tcd, a, P.split3, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
+    c->prof.end(st, P.split3 ? "conv_dgrad_tc_3xtf32_fisher" : "conv_dgrad_tc_tf32_fisher",
+                lp.dgrad_flops, by);
+  } else {
+    launch_dgrad_direct(g, dpre, base, a_prev, relu_prev, dpre_out, g_out, partial, st);
+    c->launches++;
+    c->prof.end(st, "conv_dgrad_direct_fisher", lp.dgrad_flops, by);
+  }
+}
+
 }  // namespace
 
 void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
@@ -200,8 +391,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   const bool want_grads = out.grads != nullptr;
 
   c->act.ensure(size_t(P.act_total) * 4);
-  c->wpack_f.ensure(size_t(P.w_total) * 4);
-  c->wpack_d.ensure(size_t(P.w_total) * 4);
+  c->wpack.ensure(size_t(P.w_total) * 4);
   c->part.ensure(size_t(P.part_total) * 8);
   c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
   c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
@@ -215,8 +405,6 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   double* d_perch = d_exloss + align64(N);
   FisherLayer* d_ftab = reinterpret_cast<FisherLayer*>(d_perch + align64(P.ch_total));
   float* act = c->act.as<float>();
-  float* wf = c->wpack_f.as<float>();
-  float* wd = c->wpack_d.as<float>();
   double* part = c->part.as<double>();
 
   // ---- weights: z-stream prefix (init_weights) or explicit, packed on device
@@ -241,11 +429,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       src = ensure_z(c, net.seed, l, sp.weight_count());
       scale = 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw));  // I/nnet.hpp:65
     }
-    const LayerPlan& lp = P.layers[l];
-    for (int r = 0; r < lp.geom.nranges; ++r) {
-      launch_pack_weights(src, scale, lp.geom, r, wf + lp.w_off, wd + lp.w_off, st);
-      c->launches++;
-    }
+    pack_layer(c, P.layers[l], src, scale, st);
   }
   const double* head_src;
   double head_scale;
@@ -263,20 +447,8 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   // ---- forward (I/nnet.hpp:180-197)
   const float* x = s->x.as<float>();
   for (int64_t l = 0; l < L; ++l) {
-    const LayerPlan& lp = P.layers[l];
-    float* y = act + lp.act_off;
-    for (int r = 0; r < lp.geom.nranges; ++r) {
-      const RangeDesc& rd = lp.geom.r[r];
-      const double fl = 2.0 * double(N) * rd.len * lp.geom.OH * lp.geom.OW * rd.slice_ci *
-                        lp.geom.KH * lp.geom.KW;
-      const double by = 4.0 * (double(N) * lp.geom.H * lp.geom.W * lp.geom.Ci +
-                               double(rd.len) * rd.slice_ci * lp.geom.KH * lp.geom.KW +
-                               double(N) * lp.geom.OH * lp.geom.OW * rd.len);
-      c->prof.begin(st);
-      launch_fprop_direct(lp.geom, r, x, wf + lp.w_off, y, net.relu[l], st);
-      c->prof.end(st, "conv_fprop_direct", fl, by);
-      c->launches++;
-    }
+    float* y = act + P.layers[l].act_off;
+    fprop_layer(c, P, P.layers[l], x, y, net.relu[l], st);
     x = y;
   }
 
@@ -311,15 +483,8 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       const LayerPlan& prev = P.layers[l - 1];
       float* dpre_out = (l - 1 >= 1) ? c->dpre[cur ^ 1].as<float>() : nullptr;
       float* g_out = want_grads ? c->gtmp.as<float>() + prev.act_off : nullptr;
-      const double by = 4.0 * (double(N) * lp.geom.OH * lp.geom.OW * lp.geom.Co +
-                               double(lp.wpack_floats) + 2.0 * double(prev.act_floats) +
-                               (dpre_out ? double(prev.act_floats) : 0.0));
-      c->prof.begin(st);
-      launch_dgrad_direct(lp.geom, c->dpre[cur].as<float>(), wd + lp.w_off,
-                          act + prev.act_off, net.relu[l - 1], dpre_out, g_out,
-                          part + prev.part_off, st);
-      c->prof.end(st, "conv_dgrad_direct_fisher", lp.dgrad_flops, by);
-      c->launches++;
+      dgrad_layer(c, P, lp, c->dpre[cur].as<float>(), act + prev.act_off, net.relu[l - 1],
+                  dpre_out, g_out, part + prev.part_off, st);
       cur ^= 1;
     }
     // ---- Fisher reduction (I/nnet.hpp:330-350)
@@ -358,8 +523,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       for (int which = 0; which < 2; ++which) {
         double* dst = which == 0 ? out.acts : out.grads;
         if (!dst) continue;
-        const float* src =
-            (which == 0 ? act : c->gtmp.as<float>()) + lp.act_off;
+        const float* src = (which == 0 ? act : c->gtmp.as<float>()) + lp.act_off;
         launch_nhwc32_to_nchw64(src, c->io.as<double>(), N, g.Co, g.OH, g.OW, st);
         c->launches++;
         NB_CUDA(cudaMemcpyAsync(dst + o, c->io.p, size_t(lp.act_floats) * 8,
@@ -391,6 +555,59 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     if (out.per_channel) std::memcpy(out.per_channel, perch.data(), perch.size() * 8);
     if (out.total) *out.total = tot;
   }
+}
+
+// Single-layer entry points (reference_conv / the dgrad step) through the
+// same per-layer executors as the network pipeline.
+void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* in,
+                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad) {
+  nb_layer layer{*spec, relu, 0};
+  nb_network one{1, &layer, 2, 0};
+  NetDesc d = NetDesc::from(&one);
+  if (dgrad) {
+    // plan the layer as the second of a pair so the dgrad family is chosen
+    NetDesc two = d;
+    two.specs.insert(two.specs.begin(), d.specs[0]);
+    two.relu.insert(two.relu.begin(), false);
+    d = two;
+  }
+  const Spec& s = d.specs.back();
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+  ctx_activate(ctx);
+  cudaStream_t st = ctx->stream;
+  NetPlan P = lower(d, n, prec);
+  const LayerPlan& lp = P.layers.back();
+  const int64_t x_cnt = n * s.ci * s.h * s.w, y_cnt = lp.act_floats;
+  ctx->io.ensure(size_t(std::max(x_cnt, y_cnt)) * 8);
+  ctx->gtmp.ensure(size_t(align64(x_cnt) + align64(y_cnt)) * 4);
+  ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
+  ctx->wpack.ensure(size_t(P.w_total) * 4);
+  float* xb = ctx->gtmp.as<float>();
+  float* yb = xb + align64(x_cnt);
+  NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8, cudaMemcpyHostToDevice,
+                          st));
+  pack_layer(ctx, lp, ctx->wsrc.as<double>(), 1.0, st);
+  if (!dgrad) {
+    NB_CUDA(cudaMemcpyAsync(ctx->io.p, in, size_t(x_cnt) * 8, cudaMemcpyHostToDevice, st));
+    launch_nchw64_to_nhwc32(ctx->io.as<double>(), xb, n, int(s.ci), int(s.h), int(s.w), st);
+    fprop_layer(ctx, P, lp, xb, yb, relu != 0, st);
+    launch_nhwc32_to_nchw64(yb, ctx->io.as<double>(), n, lp.geom.Co, lp.geom.OH, lp.geom.OW, st);
+    NB_CUDA(cudaMemcpyAsync(out, ctx->io.p, size_t(y_cnt) * 8, cudaMemcpyDeviceToHost, st));
+  } else {
+    NB_CUDA(cudaMemcpyAsync(ctx->io.p, in, size_t(y_cnt) * 8, cudaMemcpyHostToDevice, st));
+    launch_nchw64_to_nhwc32(ctx->io.as<double>(), yb, n, lp.geom.Co, lp.geom.OH, lp.geom.OW, st);
+    dgrad_layer(ctx, P, lp, yb, nullptr, false, nullptr, xb, nullptr, st);
+    launch_nhwc32_to_nchw64(xb, ctx->io.as<double>(), n, int(s.ci), int(s.h), int(s.w), st);
+    NB_CUDA(cudaMemcpyAsync(out, ctx->io.p, size_t(x_cnt) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  NB_CUDA(cudaGetLastError());
+  NB_CUDA(cudaStreamSynchronize(st));
+  ctx->prof.resolve();
+}
+
+void warm_z(nb_ctx* c, const NetDesc& net) {
+  for (int64_t l = 0; l < net.L(); ++l) ensure_z(c, net.seed, l, net.specs[l].weight_count());
+  ensure_z(c, net.seed, net.L(), net.num_classes * net.c_last());
 }
 
 }  // namespace nb
@@ -484,6 +701,7 @@ nb_status nb_ctx_create(int device, nb_ctx** out) {
                                  prop.name);
     auto c = std::make_unique<nb_ctx>();
     c->device = device;
+    c->num_sms = prop.multiProcessorCount;
     NB_CUDA(cudaSetDevice(device));
     NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     *out = c.release();
@@ -549,6 +767,9 @@ nb_status nb_session_create(nb_ctx* ctx, const nb_network* shape_net, const nb_b
     need(out, "output pointer");
     NetDesc d = NetDesc::from(shape_net);
     *out = make_session(ctx, d, batch);
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx_activate(ctx);
+    warm_z(ctx, d);  // candidates draw prefixes of the origin's z-streams
   });
 }
 
@@ -649,38 +870,7 @@ nb_status nb_conv_forward(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, cons
     need(x, "input");
     need(w, "weights");
     need(y, "output");
-    OneLayer one(spec, relu);
-    NetDesc d = NetDesc::from(&one.net);
-    const Spec& s = d.specs[0];
-    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-    ctx_activate(ctx);
-    cudaStream_t st = ctx->stream;
-    NetPlan P = lower(d, n, prec);
-    const LayerPlan& lp = P.layers[0];
-    const int64_t in_cnt = n * s.ci * s.h * s.w, out_cnt = lp.act_floats;
-    ctx->io.ensure(size_t(std::max(in_cnt, out_cnt)) * 8);
-    ctx->gtmp.ensure(size_t(align64(in_cnt) + align64(out_cnt)) * 4);
-    ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
-    ctx->wpack_f.ensure(size_t(P.w_total) * 4);
-    ctx->wpack_d.ensure(size_t(P.w_total) * 4);
-    float* xin = ctx->gtmp.as<float>();
-    float* yout = xin + align64(in_cnt);
-    NB_CUDA(cudaMemcpyAsync(ctx->io.p, x, size_t(in_cnt) * 8, cudaMemcpyHostToDevice, st));
-    launch_nchw64_to_nhwc32(ctx->io.as<double>(), xin, n, int(s.ci), int(s.h), int(s.w), st);
-    NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8,
-                            cudaMemcpyHostToDevice, st));
-    for (int r = 0; r < lp.geom.nranges; ++r)
-      launch_pack_weights(ctx->wsrc.as<double>(), 1.0, lp.geom, r, ctx->wpack_f.as<float>(),
-                          ctx->wpack_d.as<float>(), st);
-    for (int r = 0; r < lp.geom.nranges; ++r) {
-      launch_fprop_direct(lp.geom, r, xin, ctx->wpack_f.as<float>(), yout, relu != 0, st);
-      ctx->launches++;
-    }
-    launch_nhwc32_to_nchw64(yout, ctx->io.as<double>(), n, lp.geom.Co, lp.geom.OH, lp.geom.OW,
-                            st);
-    NB_CUDA(cudaMemcpyAsync(y, ctx->io.p, size_t(out_cnt) * 8, cudaMemcpyDeviceToHost, st));
-    NB_CUDA(cudaGetLastError());
-    NB_CUDA(cudaStreamSynchronize(st));
+    conv_single(ctx, spec, n, x, w, y, relu, prec, false);
   });
 }
 
@@ -692,37 +882,7 @@ nb_status nb_conv_dgrad(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const 
     need(dy, "dy");
     need(w, "weights");
     need(dx, "dx");
-    OneLayer one(spec, 0);
-    NetDesc d = NetDesc::from(&one.net);
-    const Spec& s = d.specs[0];
-    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-    ctx_activate(ctx);
-    cudaStream_t st = ctx->stream;
-    NetPlan P = lower(d, n, prec);
-    const LayerPlan& lp = P.layers[0];
-    const int64_t in_cnt = n * s.ci * s.h * s.w, out_cnt = lp.act_floats;
-    ctx->io.ensure(size_t(std::max(in_cnt, out_cnt)) * 8);
-    ctx->gtmp.ensure(size_t(align64(in_cnt) + align64(out_cnt)) * 4);
-    ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
-    ctx->wpack_f.ensure(size_t(P.w_total) * 4);
-    ctx->wpack_d.ensure(size_t(P.w_total) * 4);
-    float* dxo = ctx->gtmp.as<float>();
-    float* dyi = dxo + align64(in_cnt);
-    NB_CUDA(cudaMemcpyAsync(ctx->io.p, dy, size_t(out_cnt) * 8, cudaMemcpyHostToDevice, st));
-    launch_nchw64_to_nhwc32(ctx->io.as<double>(), dyi, n, lp.geom.Co, lp.geom.OH, lp.geom.OW,
-                            st);
-    NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8,
-                            cudaMemcpyHostToDevice, st));
-    for (int r = 0; r < lp.geom.nranges; ++r)
-      launch_pack_weights(ctx->wsrc.as<double>(), 1.0, lp.geom, r, ctx->wpack_f.as<float>(),
-                          ctx->wpack_d.as<float>(), st);
-    launch_dgrad_direct(lp.geom, dyi, ctx->wpack_d.as<float>(), nullptr, false, nullptr, dxo,
-                        nullptr, st);
-    ctx->launches++;
-    launch_nhwc32_to_nchw64(dxo, ctx->io.as<double>(), n, int(s.ci), int(s.h), int(s.w), st);
-    NB_CUDA(cudaMemcpyAsync(dx, ctx->io.p, size_t(in_cnt) * 8, cudaMemcpyDeviceToHost, st));
-    NB_CUDA(cudaGetLastError());
-    NB_CUDA(cudaStreamSynchronize(st));
+    conv_single(ctx, spec, n, dy, w, dx, 0, prec, true);
   });
 }
 

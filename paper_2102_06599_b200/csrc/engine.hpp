@@ -12,6 +12,7 @@
 
 #include "common.hpp"
 #include "kernels.cuh"
+#include "kernels_tc.cuh"
 
 namespace nb {
 
@@ -41,12 +42,24 @@ struct PinnedBuf {
 // ConvSpec range -> family).
 enum class Family { Direct = 0, TensorCore = 1 };
 
+// Tensor-core lowering of one GEMM (a range's fprop or a layer's dgrad).
+struct TcPlan {
+  int bn = 0;
+  tc::TcArgs tile{};   // M/N tiling and operand bases (pointers filled at launch)
+  int64_t w_off = 0;   // hi at w_off, lo at w_off + w_n (floats, layer-relative)
+  int64_t w_n = 0;
+  int b_rows = 0, b_k = 0;
+};
+
 // Lowered layer: geometry + per-range family + packed-weight offsets.
 struct LayerPlan {
   ConvGeom geom{};
   Family family[kMaxRanges]{};
-  int64_t wpack_floats = 0;  // floats of Wf (and of Wd) for this layer
-  int64_t w_off = 0;         // offset of this layer's Wf block in the weight arena
+  TcPlan tcf[kMaxRanges];    // fprop tensor-core plans (family == TensorCore)
+  Family dgrad_family = Family::Direct;
+  TcPlan tcd;                // dgrad tensor-core plan
+  int64_t wpack_floats = 0;  // floats of all packings of this layer
+  int64_t w_off = 0;         // offset of this layer's block in the weight arena
   int64_t act_off = 0;       // offset (floats) of the layer's output activation
   int64_t act_floats = 0;
   int64_t part_off = 0;      // offset (doubles) of its Fisher partials
@@ -58,6 +71,7 @@ struct NetPlan {
   std::vector<LayerPlan> layers;
   int64_t act_total = 0, w_total = 0, part_total = 0, dpre_floats = 0;
   int64_t ch_total = 0;  // sum_l C_l
+  bool split3 = false;    // 3xTF32 tensor-core numerics (NB_PREC_FP32)
 };
 
 NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec);
@@ -95,7 +109,8 @@ struct nb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::recursive_mutex mu;
-  nb::DevBuf act, wpack_f, wpack_d, part, misc, wsrc, dpre[2], gtmp, io;
+  nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io;
+  int num_sms = 148;
   nb::PinnedBuf host_io;
   // device copies of z streams keyed by (seed, stream index)
   std::map<std::pair<uint64_t, int64_t>, std::unique_ptr<nb::DevBuf>> zdev;
@@ -133,5 +148,8 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
                  bool backward, const RunOut& out);
 
 void ctx_activate(nb_ctx* c);
+void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* in,
+                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad);
+void warm_z(nb_ctx* c, const NetDesc& net);
 
 }  // namespace nb

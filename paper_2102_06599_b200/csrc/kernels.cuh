@@ -33,8 +33,20 @@ void launch_nchw64_to_nhwc32(const double* src, float* dst, int64_t N, int C, in
                              cudaStream_t st);
 void launch_nhwc32_to_nchw64(const float* src, double* dst, int64_t N, int C, int H, int W,
                              cudaStream_t st);
+// Packs one range's weights; null destinations are skipped.  TC packings
+// are K-major hi/lo pairs (hi = tf32-truncated value, lo = value - hi):
+//   tcf: [co_local][tap][j]      (fprop B operand, rows = output channels)
+//   tcd: [ci][tap][t]            (dgrad B operand, rows = input channels)
+struct PackDst {
+  float* wf;
+  float* wd;
+  float* tcf_hi;
+  float* tcf_lo;
+  float* tcd_hi;
+  float* tcd_lo;
+};
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
-                         float* wf, float* wd, cudaStream_t st);
+                         const PackDst& d, cudaStream_t st);
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
                          float* y, bool relu, cudaStream_t st);
 // g_in = convT(W, dpre) over all ranges; fused epilogue on the previous

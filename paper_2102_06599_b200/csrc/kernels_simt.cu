@@ -53,7 +53,7 @@ __global__ void k_nhwc32_to_nchw64(const float* __restrict__ src, double* __rest
 //   Wf[tap][j][co_local]  (fprop: coalesced over output channels)
 //   Wd[tap][t][ci]        (dgrad: coalesced over input channels)
 __global__ void k_pack_weights(const double* __restrict__ src, double scale, int Ci, int taps,
-                               RangeDesc r, float* __restrict__ wf, float* __restrict__ wd) {
+                               RangeDesc r, PackDst d) {
   const int64_t total = int64_t(r.len) * r.slice_ci * taps;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -66,8 +66,20 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     const int ci = g * r.slice_ci + j;
     const int64_t co = r.b + co_local;
     const float v = float(src[(co * Ci + ci) * taps + tap] * scale);
-    wf[r.wf_off + e] = v;
-    wd[r.wd_off + (int64_t(tap) * r.slice_co + t) * Ci + ci] = v;
+    if (d.wf) d.wf[r.wf_off + e] = v;
+    if (d.wd) d.wd[r.wd_off + (int64_t(tap) * r.slice_co + t) * Ci + ci] = v;
+    const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    const float lo = v - hi;
+    if (d.tcf_hi) {
+      const int64_t i = (int64_t(co_local) * taps + tap) * r.slice_ci + j;
+      d.tcf_hi[i] = hi;
+      d.tcf_lo[i] = lo;
+    }
+    if (d.tcd_hi) {
+      const int64_t i = (int64_t(ci) * taps + tap) * r.slice_co + t;
+      d.tcd_hi[i] = hi;
+      d.tcd_lo[i] = lo;
+    }
   }
 }
 
@@ -274,11 +286,11 @@ void launch_nhwc32_to_nchw64(const float* src, double* dst, int64_t N, int C, in
 }
 
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
-                         float* wf, float* wd, cudaStream_t st) {
+                         const PackDst& d, cudaStream_t st) {
   const RangeDesc& r = g.r[range];
   const int taps = g.KH * g.KW;
   const int64_t total = int64_t(r.len) * r.slice_ci * taps;
-  k_pack_weights<<<grid_for(total, 256), 256, 0, st>>>(src, scale, g.Ci, taps, r, wf, wd);
+  k_pack_weights<<<grid_for(total, 256), 256, 0, st>>>(src, scale, g.Ci, taps, r, d);
 }
 
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,

@@ -1,0 +1,535 @@
+// tcgen05 implicit-GEMM convolution (fprop and dgrad) for sm_100a.
+//
+// GEMM view of one output-channel range/group of a ConvSpec:
+//   fprop: D[pixel(n,oh,ow)][co] = sum_{tap,ci} X[n, s*oh-p+kh, s*ow-p+kw, ci] * W[co][tap][ci]
+//   dgrad: D[pixel(n,ih,iw)][ci] = sum_{tap,co} dY[n, ih+p-kh, iw+p-kw, co] * W[ci][tap][co]
+// (stride-1 dgrad; padded / cropped taps are TMA out-of-bounds zero fill).
+//
+// Warp-specialised persistent kernel, one CTA per SM:
+//   warp 0      TMA producer: per K-block (tap, 32-channel chunk) one 4-D box
+//               of the NHWC activation (128 output pixels x 128 B, SWIZZLE_128B)
+//               and one 2-D box of the K-major weights (BN rows x 128 B)
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN,
+//               K=8 per instruction, accumulator in TMEM (double-buffered)
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
+//   warps 8-11  (3xTF32 only) split converter: A_hi = trunc_tf32(A) in place,
+//               A_lo = A - A_hi, so the MMA warp can issue
+//               A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (fp32-accurate mode)
+// Epilogues: fprop -> ReLU + store; dgrad -> store g, mask with the previous
+// layer's ReLU (dpre for the next dgrad) and per-(image, tile, channel)
+// partial sums of A*g for the Fisher Potential (fixed order, deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "kernels_tc.cuh"
+
+namespace nb {
+namespace tc {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
+// apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                         uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int kABytes = 128 * 128;  // 128 pixels x 32 fp32 channels
+
+template <int BN, bool SPLIT3>
+struct Cfg {
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStageBytes = kABytes * (SPLIT3 ? 2 : 1) + kBBytes * (SPLIT3 ? 2 : 1);
+  static constexpr int kStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
+  static constexpr int kThreads = SPLIT3 ? 384 : 256;
+  static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
+                                 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int kRedBytes = 128 * 17 * 4;
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
+};
+
+template <int BN, bool SPLIT3>
+__global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
+    k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
+              const __grid_constant__ CUtensorMap mapBl, const TcArgs a) {
+  using C = Cfg<BN, SPLIT3>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // stage layout: [A_hi | A_lo? | B_hi | B_lo?]
+  auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
+  auto a_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
+  auto b_hi = [&](int s) { return smem + s * C::kStageBytes + kABytes * (SPLIT3 ? 2 : 1); };
+  auto b_lo = [&](int s) {
+    return smem + s * C::kStageBytes + kABytes * (SPLIT3 ? 2 : 1) + C::kBBytes;
+  };
+  float* red = reinterpret_cast<float*>(smem + S * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kRedBytes);
+  uint64_t* full = bars;            // S
+  uint64_t* conv = bars + S;        // S (3xTF32 converter done)
+  uint64_t* empty = bars + 2 * S;   // S
+  uint64_t* tfull = bars + 3 * S;   // 2
+  uint64_t* tempty = bars + 3 * S + 2;  // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    prefetch_map(&mapA);
+    prefetch_map(&mapBh);
+    if (SPLIT3) prefetch_map(&mapBl);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = a.m_tiles * a.n_tiles;
+  const int kblocks = a.taps_h * a.taps_w * a.a_cblocks;
+  const uint32_t a_box_bytes = uint32_t(a.BW) * a.BH * a.BNI * 128;
+  const int sgn = a.mode == 0 ? 1 : -1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m = t / a.n_tiles, nt = t % a.n_tiles;
+        const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
+        const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
+        const int c_base = a.a_c_base + g * a.a_c_per_group;
+        const int row = a.b_row_base + g * a.b_row_per_group + nn * BN;
+        const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
+        int kb = 0;
+        for (int kh = 0; kh < a.taps_h; ++kh)
+          for (int kw = 0; kw < a.taps_w; ++kw)
+            for (int cb = 0; cb < a.a_cblocks; ++cb, ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_expect_tx(&full[stage],
+                             a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
+              tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32,
+                          w0 + sgn * (kw - a.P), h0 + sgn * (kh - a.P), n0);
+              const int kcoord = (kh * a.taps_w + kw) * a.b_k_per_tap + cb * 32;
+              tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
+              if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
+              if (++stage == S) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
+                                 (uint32_t(128 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(SPLIT3 ? &conv[stage] : &full[stage], phase);
+          tc_fence_after();
+          const uint64_t dah = sw128_desc(smem_u32(a_hi(stage)));
+          const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t koff = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 B along K
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
+            if (SPLIT3) {
+              const uint64_t dal = sw128_desc(smem_u32(a_lo(stage)));
+              const uint64_t dbl = sw128_desc(smem_u32(b_lo(stage)));
+              mma_tf32(d_tmem, dah + koff, dbl + koff, idesc, 1u);
+              mma_tf32(d_tmem, dal + koff, dbh + koff, idesc, 1u);
+            }
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- epilogue (TMEM lanes 32*(warp-4) .. +31)
+    const int q = warp - 4;
+    const int r = threadIdx.x - 128;  // accumulator row == TMEM lane
+    const int rows_per_img = a.BW * a.BH;
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      const int m = t / a.n_tiles, nt = t % a.n_tiles;
+      const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
+      const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
+      const int wi = r % a.BW, hi = (r / a.BW) % a.BH, ni = r / rows_per_img;
+      const int n = nb * a.BNI + ni, oh = hb * a.BH + hi, ow = wb * a.BW + wi;
+      const bool valid = ni < a.BNI && n < a.nimg && oh < a.OH && ow < a.OW;
+      const int64_t pix = (int64_t(n) * a.OH + oh) * a.OW + ow;
+      const int col0 = a.out_c_base + g * a.out_c_per_group + nn * BN;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(trow + uint32_t(c), v);
+        if (a.mode == 0) {
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              if (a.relu) {
+                x.x = x.x > 0.f ? x.x : 0.f;
+                x.y = x.y > 0.f ? x.y : 0.f;
+                x.z = x.z > 0.f ? x.z : 0.f;
+                x.w = x.w > 0.f ? x.w : 0.f;
+              }
+              o[i] = x;
+            }
+          }
+        } else {
+          float contrib[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) contrib[i] = 0.f;
+          if (valid) {
+            const int64_t base = pix * a.out_ld + col0 + c;
+            if (a.g_out) {
+              float4* go = reinterpret_cast<float4*>(a.g_out + base);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                go[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            if (a.a_prev) {
+              const float4* ap = reinterpret_cast<const float4*>(a.a_prev + base);
+              float av[16];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                float4 x = ap[i];
+                av[4 * i] = x.x;
+                av[4 * i + 1] = x.y;
+                av[4 * i + 2] = x.z;
+                av[4 * i + 3] = x.w;
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) contrib[i] = av[i] * v[i];
+              if (a.dpre_out) {
+                float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float4 x;
+                  x.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
+                  x.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
+                  x.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
+                  x.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+                  dp[i] = x;
+                }
+              }
+            } else if (a.dpre_out) {
+              float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          }
+          if (a.partial) {
+            // deterministic per-(image, channel) sums over this tile's rows
+#pragma unroll
+            for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
+            named_bar(1, 128);
+            for (int wi2 = r; wi2 < a.BNI * 16; wi2 += 128) {
+              const int img = wi2 / 16, j = wi2 % 16;
+              const int nimg = nb * a.BNI + img;
+              if (nimg < a.nimg) {
+                float s = 0.f;
+                for (int rr = img * rows_per_img; rr < (img + 1) * rows_per_img; ++rr)
+                  s += red[rr * 17 + j];
+                const int tile_in_img = hb * a.tiles_w + wb;
+                a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
+                          col0 + c + j] = double(s);
+              }
+            }
+            named_bar(1, 128);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  } else if (SPLIT3 && warp >= 8) {
+    // ---------------- 3xTF32 split converter: A_hi = trunc(A), A_lo = A - A_hi
+    const int ct = threadIdx.x - 256;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        uint4* hi = reinterpret_cast<uint4*>(a_hi(stage));
+        uint4* lo = reinterpret_cast<uint4*>(a_lo(stage));
+#pragma unroll
+        for (int i = 0; i < kABytes / 16 / 128; ++i) {
+          const int idx = ct + i * 128;
+          uint4 x = hi[idx];
+          uint4 h;
+          h.x = x.x & 0xFFFFE000u;
+          h.y = x.y & 0xFFFFE000u;
+          h.z = x.z & 0xFFFFE000u;
+          h.w = x.w & 0xFFFFE000u;
+          float4 l;
+          l.x = __uint_as_float(x.x) - __uint_as_float(h.x);
+          l.y = __uint_as_float(x.y) - __uint_as_float(h.y);
+          l.z = __uint_as_float(x.z) - __uint_as_float(h.z);
+          l.w = __uint_as_float(x.w) - __uint_as_float(h.w);
+          hi[idx] = h;
+          lo[idx] = *reinterpret_cast<uint4*>(&l);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::kTmemCols));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map_4d(CUtensorMap* m, const float* base, int C, int W, int H, int N, int boxW,
+                 int boxH, int boxN, int stride) {
+  cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
+  cuuint64_t strides[3] = {cuuint64_t(C) * 4, cuuint64_t(C) * W * 4, cuuint64_t(C) * W * H * 4};
+  cuuint32_t box[4] = {32, cuuint32_t(boxW * stride), cuuint32_t(boxH * stride),
+                       cuuint32_t(boxN)};
+  cuuint32_t es[4] = {1, cuuint32_t(stride), cuuint32_t(stride), 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_map_2d(CUtensorMap* m, const float* base, int K, int rows, int box_rows) {
+  cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(K) * 4};
+  cuuint32_t box[2] = {32, cuuint32_t(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool SPLIT3>
+cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
+  using C = Cfg<BN, SPLIT3>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = L.args.m_tiles * L.args.n_tiles;
+  const int grid = tiles < L.num_sms ? tiles : L.num_sms;
+  k_conv_tc<BN, SPLIT3><<<grid, C::kThreads, C::kSmem, st>>>(L.mapA, L.mapBh, L.mapBl, L.args);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a) {
+  a.OH = OH;
+  a.OW = OW;
+  a.nimg = nimg;
+  a.BW = OW < 128 ? OW : 128;
+  int bh = 128 / a.BW;
+  a.BH = OH < bh ? OH : bh;
+  int bn = 128 / (a.BW * a.BH);
+  a.BNI = nimg < bn ? nimg : bn;
+  if (a.BW * S > 256 || a.BH * S > 256) return false;
+  a.tiles_w = (OW + a.BW - 1) / a.BW;
+  a.tiles_h = (OH + a.BH - 1) / a.BH;
+  a.tiles_n = (nimg + a.BNI - 1) / a.BNI;
+  a.m_tiles = a.tiles_w * a.tiles_h * a.tiles_n;
+  return true;
+}
+
+bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const float* Bhi,
+               const float* Blo, int BK, int Brows) {
+  const TcArgs& a = L.args;
+  if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
+  if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, L.bn)) return false;
+  if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, L.bn)) return false;
+  return true;
+}
+
+cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
+  if (L.split3) {
+    switch (L.bn) {
+      case 32: return launch_t<32, true>(L, st);
+      case 64: return launch_t<64, true>(L, st);
+      case 128: return launch_t<128, true>(L, st);
+    }
+  } else {
+    switch (L.bn) {
+      case 32: return launch_t<32, false>(L, st);
+      case 64: return launch_t<64, false>(L, st);
+      case 128: return launch_t<128, false>(L, st);
+      case 256: return launch_t<256, false>(L, st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tc
+}  // namespace nb

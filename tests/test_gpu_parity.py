@@ -220,3 +220,100 @@ def test_larger_chain_matches_oracle(ctx, oracle):
     o = oracle.fisher(net, 4, batch=batch)
     assert math.isclose(rep.total, o["total"], rel_tol=1e-5)
     np.testing.assert_allclose(rep.per_layer, o["per_layer"], rtol=1e-4)
+
+
+# ---------------------------------------------------------------------------
+# tensor-core (tcgen05) shaped cases: 32-channel K chunks, 16-aligned N
+
+TC_SPECS = [
+    ConvSpec(32, 32, 8, 8, 3, 3, 1, 1),
+    ConvSpec(64, 64, 16, 16, 3, 3, 1, 1),
+    ConvSpec(64, 128, 16, 16, 3, 3, 2, 1),                     # stride 2 (TMA element strides)
+    ConvSpec(64, 64, 8, 8, 3, 3, 1, 1, groups=2),              # grouped, slice_ci = 32
+    ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, bottleneck_out=2),    # Co_eff = 32
+    ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, spatial_div_h=4, spatial_div_w=2),  # crop
+    ConvSpec(64, 64, 4, 4, 3, 3, 1, 1),                        # 8 images per M tile
+    ConvSpec(32, 64, 7, 7, 3, 3, 1, 1),                        # 49-pixel images (partial tiles)
+    ConvSpec(64, 64, 8, 8, 1, 1, 1, 0),                        # 1x1
+    ConvSpec(64, 96, 8, 8, 3, 3, 1, 1,
+             channel_splits=[ChannelSplit(0, 32, 1), ChannelSplit(32, 96, 2)]),
+    ConvSpec(128, 128, 2, 2, 3, 3, 1, 1),                      # 32 images per M tile
+]
+
+
+@pytest.mark.parametrize("prec", [Precision.FP32, Precision.TF32])
+@pytest.mark.parametrize("spec", TC_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}g{s.groups}")
+def test_tc_conv_integer_exact(ctx, oracle, spec, prec):
+    """Small integers are exact in tf32 and their sums exact in fp32, so the
+    tensor-core path must reproduce reference_conv<int64> bit for bit."""
+    rng = np.random.default_rng(spec.ci * 7 + spec.co)
+    n = 3
+    x = rng.integers(-3, 4, size=(n, spec.ci, spec.h, spec.w)).astype(np.float64)
+    w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(np.float64)
+    y = nb.reference_conv(spec, x, w, precision=prec, ctx=ctx)
+    for i in range(n):
+        want = oracle.conv(spec, x[i].astype(np.int64), w.astype(np.int64))
+        assert np.array_equal(y[i], want.astype(np.float64)), i
+
+
+@pytest.mark.parametrize("spec", TC_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}g{s.groups}")
+def test_tc_conv_fp32_accuracy(ctx, oracle, spec):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, spec.ci, spec.h, spec.w))
+    w = rng.standard_normal((spec.co_eff(), spec.ci, spec.kh, spec.kw)) / np.sqrt(spec.ci * 9)
+    y3 = nb.reference_conv(spec, x, w, precision=Precision.FP32, ctx=ctx)
+    y1 = nb.reference_conv(spec, x, w, precision=Precision.TF32, ctx=ctx)
+    scale = np.stack([oracle.conv(spec, np.abs(x[i]), np.abs(w)) for i in range(2)])
+    want = np.stack([oracle.conv(spec, x[i], w) for i in range(2)])
+    assert np.all(np.abs(y3 - want) <= 2e-6 * scale + 1e-30)   # fp32-accurate (3xTF32)
+    assert np.all(np.abs(y1 - want) <= 2e-3 * scale + 1e-30)   # TF32 throughput mode
+
+
+@pytest.mark.parametrize("prec", [Precision.FP32, Precision.TF32])
+@pytest.mark.parametrize("spec", [s for s in TC_SPECS if s.stride == 1 and not s.channel_splits],
+                         ids=lambda s: f"{s.ci}x{s.co}x{s.h}g{s.groups}")
+def test_tc_dgrad_integer_exact(ctx, oracle, spec, prec):
+    rng = np.random.default_rng(11)
+    dy = rng.integers(-3, 4, size=(2,) + spec.output_shape()).astype(np.float64)
+    w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(np.float64)
+    got = nb.conv_dgrad(spec, dy, w, precision=prec, ctx=ctx)
+    for i in range(2):
+        assert np.array_equal(got[i], oracle.conv_dgrad(spec, dy[i], w)), i
+
+
+def _tc_chain():
+    return Network([
+        Layer(ConvSpec(3, 32, 16, 16, 3, 3, 1, 1)),
+        Layer(ConvSpec(32, 64, 16, 16, 3, 3, 1, 1)),
+        Layer(ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, groups=2)),
+        Layer(ConvSpec(64, 128, 16, 16, 3, 3, 2, 1)),
+        Layer(ConvSpec(128, 128, 8, 8, 3, 3, 1, 1, bottleneck_out=2)),
+        Layer(ConvSpec(64, 64, 8, 8, 3, 3, 1, 1, spatial_div_h=2, spatial_div_w=2)),
+        Layer(ConvSpec(64, 64, 4, 4, 3, 3, 1, 1, groups=64)),
+        Layer(ConvSpec(64, 64, 4, 4, 3, 3, 1, 1)),
+    ], num_classes=10, seed=42)
+
+
+@pytest.mark.parametrize("prec,tol", [(Precision.FP32, 1e-5), (Precision.TF32, 5e-3)])
+def test_tc_chain_fisher_matches_oracle(ctx, oracle, prec, tol):
+    net = _tc_chain()
+    batch = nb.make_batch(net, 4, 1)
+    rep = nb.fisher_potential(net, batch, precision=prec, ctx=ctx)
+    o = oracle.fisher(net, 4, batch=batch)
+    assert math.isclose(rep.total, o["total"], rel_tol=tol), (rep.total, o["total"])
+    np.testing.assert_allclose(rep.per_layer, o["per_layer"], rtol=20 * tol)
+    assert math.isclose(rep.loss, o["loss"], rel_tol=tol)
+
+
+def test_tc_chain_gradients_match_oracle(ctx, oracle):
+    net = _tc_chain()
+    batch = nb.make_batch(net, 2, 3)
+    acts, grads = nb.activation_gradients(net, batch, precision=Precision.FP32, ctx=ctx)
+    o = oracle.fisher(net, 2, batch=batch, grads=True)
+    off = 0
+    for a, g in zip(acts, grads):
+        k = a.size
+        ra, rg = o["acts"][off:off + k], o["grads"][off:off + k]
+        np.testing.assert_allclose(a.ravel(), ra, rtol=0, atol=1e-5 * np.abs(ra).max())
+        np.testing.assert_allclose(g.ravel(), rg, rtol=0, atol=1e-4 * np.abs(rg).max())
+        off += k
