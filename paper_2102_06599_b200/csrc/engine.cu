@@ -119,6 +119,55 @@ int pick_bn(int n_per_group, int groups, int m_tiles, bool split3) {
   }
   return smallest;
 }
+// fprop: one phase over the OH x OW output, every tap, A box at
+// (S*oy - P + kh, S*ox - P + kw) (the element stride S is in the tensor map).
+void fprop_phase(const ConvGeom& g, tc::TcArgs& t) {
+  t.nphase = 1;
+  t.PS = 1;
+  t.OHp[0] = g.OH;
+  t.OWp[0] = g.OW;
+  t.py[0] = t.px[0] = 0;
+  t.OutH = g.OH;
+  t.OutW = g.OW;
+  int n = 0;
+  for (int kh = 0; kh < g.KH; ++kh)
+    for (int kw = 0; kw < g.KW; ++kw) t.taps[0][n++] = tc::pack_tap(kh * g.KW + kw, kh - g.P, kw - g.P);
+  t.ntaps[0] = n;
+}
+
+// dgrad (I/nnet.hpp:235-243 as a gather): g[ih,iw] = sum over taps with
+// (ih + P - kh) % S == 0 of W * dY[(ih + P - kh)/S, ...].  With ih = S*oy + py
+// the dY row is oy + (py + P - kh)/S, so each phase (py, px) is a stride-1
+// correlation over the taps of matching parity; out-of-range dY rows (the
+// border and the output crop, I/ir.hpp:47-50) are TMA zero fill.
+void dgrad_phases(const ConvGeom& g, tc::TcArgs& t) {
+  const int S = g.S;
+  t.nphase = S * S;
+  t.PS = S;
+  t.OutH = g.H;
+  t.OutW = g.W;
+  for (int py = 0; py < S; ++py)
+    for (int px = 0; px < S; ++px) {
+      const int ph = py * S + px;
+      t.py[ph] = py;
+      t.px[ph] = px;
+      t.OHp[ph] = (g.H - py + S - 1) / S;
+      t.OWp[ph] = (g.W - px + S - 1) / S;
+      int n = 0;
+      for (int kh = 0; kh < g.KH; ++kh) {
+        const int th = py + g.P - kh;
+        if (((th % S) + S) % S) continue;
+        for (int kw = 0; kw < g.KW; ++kw) {
+          const int tw = px + g.P - kw;
+          if (((tw % S) + S) % S) continue;
+          // floor division of the (exact) multiples of S
+          t.taps[ph][n++] = tc::pack_tap(kh * g.KW + kw, (th - ((th % S) + S) % S) / S,
+                                         (tw - ((tw % S) + S) % S) / S);
+        }
+      }
+      t.ntaps[ph] = n;
+    }
+}
 }  // namespace
 
 // Lowering of a (derived, repaired) network to kernel plans (SURVEY 7
@@ -167,7 +216,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
       off += align64(used);
       lp.family[i] = Family::Direct;
       if (tc_on && (g.S == 1 || g.S == 2) && r.slice_ci % 32 == 0 && r.b % 16 == 0 &&
-          g.Co % 4 == 0) {
+          g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
           const int bn = pick_bn(r.slice_co, r.groups, t.m_tiles, P.split3);
@@ -175,10 +224,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
             t.mode = 0;
             t.n_tiles_per_group = r.slice_co / bn;
             t.n_tiles = r.groups * t.n_tiles_per_group;
-            t.taps_h = g.KH;
-            t.taps_w = g.KW;
             t.S = g.S;
-            t.P = g.P;
+            fprop_phase(g, t);
             t.a_cblocks = r.slice_ci / 32;
             t.a_c_base = 0;
             t.a_c_per_group = r.slice_ci;
@@ -201,20 +248,21 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
         }
       }
     }
-    if (l >= 1 && tc_on && g.nranges == 1 && g.S == 1 && g.r[0].slice_co % 32 == 0 &&
-        g.Ci % 4 == 0) {
+    // dgrad on the tensor cores: stride 1 as one phase, stride 2 as the four
+    // sub-pixel phases (a phase grid of ceil(H/2) x ceil(W/2)).
+    if (l >= 1 && tc_on && g.nranges == 1 && (g.S == 1 || g.S == 2) &&
+        g.r[0].slice_co % 32 == 0 && g.Ci % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
       const RangeDesc& r = g.r[0];
       tc::TcArgs t{};
-      if (tc::plan_tiles(g.H, g.W, g.N, 1, t)) {
-        const int bn = pick_bn(r.slice_ci, r.groups, t.m_tiles, P.split3);
+      const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
+      if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
+        const int bn = pick_bn(r.slice_ci, r.groups, t.m_tiles * g.S * g.S, P.split3);
         if (bn) {
           t.mode = 1;
           t.n_tiles_per_group = r.slice_ci / bn;
           t.n_tiles = r.groups * t.n_tiles_per_group;
-          t.taps_h = g.KH;
-          t.taps_w = g.KW;
           t.S = 1;
-          t.P = g.P;
+          dgrad_phases(g, t);
           t.a_cblocks = r.slice_co / 32;
           t.a_c_base = r.b;
           t.a_c_per_group = r.slice_co;
@@ -225,7 +273,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          t.part_tiles_per_img = t.BNI == 1 ? t.tiles_h * t.tiles_w : 1;
+          t.part_tiles_per_img = t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
           TcPlan& tp = lp.tcd;
           tp.bn = bn;
           tp.tile = t;
@@ -277,9 +325,14 @@ const double* ensure_z(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) 
   if (!buf) buf = std::make_unique<DevBuf>();
   int64_t& have = c->zlen[key];
   if (have < count) {
+    // The host stream is cached for the process lifetime, so the copy can be
+    // stream-ordered with the pack kernels that read it (a plain cudaMemcpy
+    // from pageable memory may return before its DMA lands, and the context
+    // stream does not synchronise with the legacy stream).
     const std::vector<double>& z = z_stream(seed, stream, count);
     buf->ensure(size_t(count) * 8);
-    NB_CUDA(cudaMemcpy(buf->p, z.data(), size_t(count) * 8, cudaMemcpyHostToDevice));
+    NB_CUDA(cudaMemcpyAsync(buf->p, z.data(), size_t(count) * 8, cudaMemcpyHostToDevice,
+                            c->stream));
     have = count;
   }
   return buf->as<double>();

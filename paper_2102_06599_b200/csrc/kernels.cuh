@@ -8,6 +8,18 @@ namespace nb {
 
 constexpr int kMaxRanges = 16;
 
+#ifdef __CUDACC__
+// 3xTF32 operand split: hi = round-to-nearest tf32(x), lo = tf32(x - hi), so
+// hi + lo carries 22 significant bits and hi*hi + hi*lo + lo*hi reproduces an
+// fp32 product to ~2^-22 (the tensor core reads only the top 19 bits of each
+// operand, so both halves are pre-rounded rather than left to truncation).
+__device__ __forceinline__ void split_tf32(uint32_t x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(__uint_as_float(x)));
+  const float r = __uint_as_float(x) - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+#endif
+
 // One output-channel range of a ConvSpec (I/ir.hpp:54-57): channels
 // [b, b+len) in G groups of slice_co outputs, each reading slice_ci inputs.
 struct RangeDesc {

@@ -68,8 +68,9 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     const float v = float(src[(co * Ci + ci) * taps + tap] * scale);
     if (d.wf) d.wf[r.wf_off + e] = v;
     if (d.wd) d.wd[r.wd_off + (int64_t(tap) * r.slice_co + t) * Ci + ci] = v;
-    const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    const float lo = v - hi;
+    uint32_t hb, lb;
+    split_tf32(__float_as_uint(v), hb, lb);
+    const float hi = __uint_as_float(hb), lo = __uint_as_float(lb);
     if (d.tcf_hi) {
       const int64_t i = (int64_t(co_local) * taps + tap) * r.slice_ci + j;
       d.tcf_hi[i] = hi;
@@ -250,18 +251,30 @@ __global__ void k_head(HeadArgs a) {
 }
 
 // delta[l][c] = (sum_n s_nc^2) / (2N), s_nc = -sum_tiles partial (fixed
-// order), I/nnet.hpp:330-345.
-__global__ void k_fisher_reduce(const FisherLayer* __restrict__ layers, int N,
-                                double* __restrict__ per_channel) {
+// order), I/nnet.hpp:330-345.  Block = 32 channels x 16 example lanes; the
+// 16 lane sums are combined in a fixed order (deterministic, fp64).
+__global__ void __launch_bounds__(512) k_fisher_reduce(const FisherLayer* __restrict__ layers,
+                                                       int N, double* __restrict__ per_channel) {
+  __shared__ double red[16][33];
   const FisherLayer L = layers[blockIdx.y];
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.C; c += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int n = 0; n < N; ++n) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  if (blockIdx.x * 32 >= L.C) return;
+  double acc = 0.0;
+  if (c < L.C) {
+    for (int n = threadIdx.y; n < N; n += 16) {
+      const double* p = L.partial + int64_t(n) * L.tiles * L.C + c;
       double s = 0.0;
-      for (int t = 0; t < L.tiles; ++t) s -= L.partial[(int64_t(n) * L.tiles + t) * L.C + c];
+      for (int t = 0; t < L.tiles; ++t) s -= p[int64_t(t) * L.C];
       acc += s * s;
     }
-    per_channel[L.out_off + c] = acc / (2.0 * double(N));
+  }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < L.C) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tot += red[k][threadIdx.x];
+    per_channel[L.out_off + c] = tot / (2.0 * double(N));
   }
 }
 
@@ -314,8 +327,8 @@ void launch_head(const HeadArgs& a, cudaStream_t st) {
 
 void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,
                           double* per_channel, cudaStream_t st) {
-  dim3 grid((max_c + 127) / 128, L);
-  k_fisher_reduce<<<grid, 128, 0, st>>>(layers_dev, N, per_channel);
+  dim3 grid((max_c + 31) / 32, L);
+  k_fisher_reduce<<<grid, dim3(32, 16), 0, st>>>(layers_dev, N, per_channel);
 }
 
 }  // namespace nb

@@ -2,8 +2,11 @@
 //
 // GEMM view of one output-channel range/group of a ConvSpec:
 //   fprop: D[pixel(n,oh,ow)][co] = sum_{tap,ci} X[n, s*oh-p+kh, s*ow-p+kw, ci] * W[co][tap][ci]
-//   dgrad: D[pixel(n,ih,iw)][ci] = sum_{tap,co} dY[n, ih+p-kh, iw+p-kw, co] * W[ci][tap][co]
-// (stride-1 dgrad; padded / cropped taps are TMA out-of-bounds zero fill).
+//   dgrad: D[pixel(n,ih,iw)][ci] = sum_{tap,co} dY[n, (ih+p-kh)/s, (iw+p-kw)/s, co] * W[ci][tap][co]
+// Padded / cropped taps are TMA out-of-bounds zero fill.  A stride-2 dgrad
+// runs as four sub-pixel phases (ih = 2*oy + py): each is a stride-1
+// correlation of dY with the taps kh = py + p (mod 2), all four in one
+// persistent launch (tiles are phase-major).
 //
 // Warp-specialised persistent kernel, one CTA per SM:
 //   warp 0      TMA producer: per K-block (tap, 32-channel chunk) one 4-D box
@@ -13,8 +16,8 @@
 //               K=8 per instruction, accumulator in TMEM (double-buffered)
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
-//   warps 8-11  (3xTF32 only) split converter: A_hi = trunc_tf32(A) in place,
-//               A_lo = A - A_hi, so the MMA warp can issue
+//   warps 8-11  (3xTF32 only) split converter: A_hi = rn_tf32(A) in place,
+//               A_lo = rn_tf32(A - A_hi), so the MMA warp can issue
 //               A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (fp32-accurate mode)
 // Epilogues: fprop -> ReLU + store; dgrad -> store g, mask with the previous
 // layer's ReLU (dpre for the next dgrad) and per-(image, tile, channel)
@@ -25,6 +28,7 @@
 #include <cstdint>
 #include <cstdio>
 
+#include "kernels.cuh"
 #include "kernels_tc.cuh"
 
 namespace nb {
@@ -204,10 +208,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = a.m_tiles * a.n_tiles;
-  const int kblocks = a.taps_h * a.taps_w * a.a_cblocks;
+  const int tiles_per_phase = a.m_tiles * a.n_tiles;
+  const int num_tiles = a.nphase * tiles_per_phase;
   const uint32_t a_box_bytes = uint32_t(a.BW) * a.BH * a.BNI * 128;
-  const int sgn = a.mode == 0 ? 1 : -1;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -215,29 +218,31 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m = t / a.n_tiles, nt = t % a.n_tiles;
+        const int ph = t / tiles_per_phase, tt = t % tiles_per_phase;
+        const int m = tt / a.n_tiles, nt = tt % a.n_tiles;
         const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
         const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
         const int c_base = a.a_c_base + g * a.a_c_per_group;
         const int row = a.b_row_base + g * a.b_row_per_group + nn * BN;
         const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
-        int kb = 0;
-        for (int kh = 0; kh < a.taps_h; ++kh)
-          for (int kw = 0; kw < a.taps_w; ++kw)
-            for (int cb = 0; cb < a.a_cblocks; ++cb, ++kb) {
-              mbar_wait(&empty[stage], phase ^ 1);
-              mbar_expect_tx(&full[stage],
-                             a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
-              tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32,
-                          w0 + sgn * (kw - a.P), h0 + sgn * (kh - a.P), n0);
-              const int kcoord = (kh * a.taps_w + kw) * a.b_k_per_tap + cb * 32;
-              tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
-              if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
-              if (++stage == S) {
-                stage = 0;
-                phase ^= 1;
-              }
+        const int nt_ph = a.ntaps[ph];
+        for (int ti = 0; ti < nt_ph; ++ti) {
+          const int32_t tp = a.taps[ph][ti];
+          const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
+          const int kbase = tap_kidx(tp) * a.b_k_per_tap;
+          for (int cb = 0; cb < a.a_cblocks; ++cb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
+            tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+            const int kcoord = kbase + cb * 32;
+            tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
+            if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
             }
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -249,6 +254,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int kblocks = a.ntaps[t / tiles_per_phase] * a.a_cblocks;
         const int acc = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit(&tfull[acc]);  // with no taps (empty phase) this arrives at once
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -285,18 +291,23 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     const int q = warp - 4;
     const int r = threadIdx.x - 128;  // accumulator row == TMEM lane
     const int rows_per_img = a.BW * a.BH;
+    const int part_per_phase = a.BNI == 1 ? a.tiles_h * a.tiles_w : 1;
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m = t / a.n_tiles, nt = t % a.n_tiles;
+      const int ph = t / tiles_per_phase, tt = t % tiles_per_phase;
+      const int m = tt / a.n_tiles, nt = tt % a.n_tiles;
       const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
       const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
       const int wi = r % a.BW, hi = (r / a.BW) % a.BH, ni = r / rows_per_img;
       const int n = nb * a.BNI + ni, oh = hb * a.BH + hi, ow = wb * a.BW + wi;
-      const bool valid = ni < a.BNI && n < a.nimg && oh < a.OH && ow < a.OW;
-      const int64_t pix = (int64_t(n) * a.OH + oh) * a.OW + ow;
+      const bool valid = ni < a.BNI && n < a.nimg && oh < a.OHp[ph] && ow < a.OWp[ph];
+      const int64_t pix =
+          (int64_t(n) * a.OutH + oh * a.PS + a.py[ph]) * a.OutW + ow * a.PS + a.px[ph];
       const int col0 = a.out_c_base + g * a.out_c_per_group + nn * BN;
+      const bool empty_phase = a.ntaps[ph] == 0;
+      const int tile_in_img = ph * part_per_phase + (a.BNI == 1 ? hb * a.tiles_w + wb : 0);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
@@ -304,6 +315,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(trow + uint32_t(c), v);
+        if (empty_phase) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
         if (a.mode == 0) {
           if (valid) {
             float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
@@ -375,7 +390,6 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
                 float s = 0.f;
                 for (int rr = img * rows_per_img; rr < (img + 1) * rows_per_img; ++rr)
                   s += red[rr * 17 + j];
-                const int tile_in_img = hb * a.tiles_w + wb;
                 a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
                           col0 + c + j] = double(s);
               }
@@ -388,11 +402,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       mbar_arrive(&tempty[acc]);
     }
   } else if (SPLIT3 && warp >= 8) {
-    // ---------------- 3xTF32 split converter: A_hi = trunc(A), A_lo = A - A_hi
+    // ---------------- 3xTF32 split converter: A_hi = rn_tf32(A), A_lo = rn_tf32(A - A_hi)
     const int ct = threadIdx.x - 256;  // 0..127
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int kblocks = a.ntaps[t / tiles_per_phase] * a.a_cblocks;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&full[stage], phase);
         uint4* hi = reinterpret_cast<uint4*>(a_hi(stage));
@@ -400,19 +415,14 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
 #pragma unroll
         for (int i = 0; i < kABytes / 16 / 128; ++i) {
           const int idx = ct + i * 128;
-          uint4 x = hi[idx];
-          uint4 h;
-          h.x = x.x & 0xFFFFE000u;
-          h.y = x.y & 0xFFFFE000u;
-          h.z = x.z & 0xFFFFE000u;
-          h.w = x.w & 0xFFFFE000u;
-          float4 l;
-          l.x = __uint_as_float(x.x) - __uint_as_float(h.x);
-          l.y = __uint_as_float(x.y) - __uint_as_float(h.y);
-          l.z = __uint_as_float(x.z) - __uint_as_float(h.z);
-          l.w = __uint_as_float(x.w) - __uint_as_float(h.w);
+          const uint4 x = hi[idx];
+          uint4 h, l;
+          split_tf32(x.x, h.x, l.x);
+          split_tf32(x.y, h.y, l.y);
+          split_tf32(x.z, h.z, l.z);
+          split_tf32(x.w, h.w, l.w);
           hi[idx] = h;
-          lo[idx] = *reinterpret_cast<uint4*>(&l);
+          lo[idx] = l;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[stage]);
@@ -479,7 +489,7 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = L.args.m_tiles * L.args.n_tiles;
+  const int tiles = L.args.nphase * L.args.m_tiles * L.args.n_tiles;
   const int grid = tiles < L.num_sms ? tiles : L.num_sms;
   k_conv_tc<BN, SPLIT3><<<grid, C::kThreads, C::kSmem, st>>>(L.mapA, L.mapBh, L.mapBl, L.args);
   return cudaGetLastError();

@@ -9,22 +9,49 @@
 namespace nb {
 namespace tc {
 
+constexpr int kMaxPhases = 4;      // sub-pixel phases of a stride-2 dgrad
+constexpr int kMaxPhaseTaps = 32;  // taps per phase (kernels up to 5x5 in one phase)
+
+// One tap of a phase, packed: bits 0-11 = tap index kh*KW+kw into the B
+// operand's K dimension, bits 12-21 / 22-31 = signed 10-bit offsets (h, w) of
+// the A box relative to the tile origin (in A-tensor elements, before the
+// element stride).
+__host__ __device__ inline int32_t pack_tap(int kidx, int dh, int dw) {
+  return int32_t(uint32_t(kidx & 0xFFF) | (uint32_t(dh & 0x3FF) << 12) |
+                 (uint32_t(dw & 0x3FF) << 22));
+}
+__host__ __device__ inline int tap_kidx(int32_t t) { return int(uint32_t(t) & 0xFFF); }
+__host__ __device__ inline int tap_dh(int32_t t) { return (int(uint32_t(t) << 10) >> 22); }
+__host__ __device__ inline int tap_dw(int32_t t) { return int(t) >> 22; }
+
 // One GEMM launch: an output-channel range (all its groups) of a conv layer,
-// fprop (mode 0) or stride-1 dgrad (mode 1).  See kernels_tc.cu.
+// fprop (mode 0) or dgrad (mode 1).  See kernels_tc.cu.
+//
+// The GEMM's M dimension is a set of `nphase` pixel grids.  Phase p covers
+// the output pixels (n, oy*PS + py[p], ox*PS + px[p]) for oy < OHp[p],
+// ox < OWp[p]; fprop and stride-1 dgrad have one phase with PS = 1, a
+// stride-2 dgrad has the four sub-pixel phases (PS = 2), each a stride-1
+// correlation of dY with the taps whose parity matches the phase.
 struct TcArgs {
   int mode;
-  // GEMM output pixel space (fprop: OH x OW; dgrad: the layer input H x W)
-  int nimg, OH, OW;
-  // M tile = BNI images x BH rows x BW columns (<= 128 pixels)
+  int nimg;
+  // tile geometry shared by all phases (planned on the largest phase grid)
+  int OH, OW;  // largest phase grid
   int BW, BH, BNI, tiles_w, tiles_h, tiles_n, m_tiles;
   int n_tiles, n_tiles_per_group;
-  int taps_h, taps_w, S, P;
+  int S;  // element stride of the A box (fprop stride; 1 for dgrad)
+  // phases
+  int nphase, PS;
+  int OHp[kMaxPhases], OWp[kMaxPhases], py[kMaxPhases], px[kMaxPhases];
+  int ntaps[kMaxPhases];
+  int32_t taps[kMaxPhases][kMaxPhaseTaps];
   // A operand (4-D NHWC activation): 32-channel K chunks per tap, channel base
   int a_cblocks, a_c_base, a_c_per_group;
   // B operand (2-D K-major weights [rows][taps*K]): K per tap, row bases
   int b_k_per_tap, b_row_base, b_row_per_group;
-  // epilogue output (NHWC, ld channels)
+  // epilogue output (NHWC over OutH x OutW pixels, ld channels)
   float* out;
+  int OutH, OutW;
   int out_ld, out_c_base, out_c_per_group;
   int relu;
   // dgrad fused epilogue
@@ -43,8 +70,8 @@ struct TcLaunch {
   int num_sms;
 };
 
-// Fills the M-tile geometry of `a` for an OH x OW output over nimg images;
-// false if the TMA box would be illegal.
+// Fills the M-tile geometry of `a` for an OH x OW (largest phase) grid over
+// nimg images; false if the TMA box would be illegal.
 bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a);
 // Encodes the tensor maps (A: C x W x H x N activation, B: rows x K weights).
 bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const float* Bhi,
