@@ -1,0 +1,475 @@
+// nestopt <-> nb200 bridge: the reference-side binding of the B200 hot path.
+//
+// This header is what a nestopt maintainer adds to the reference's C++ host
+// (proj/include/nestopt stays intact and is used through the include path):
+// it converts the reference's value types to the plain-C descriptors of
+// include/nb200.h, calls the sm_100a library through that C ABI, and turns
+// nb_status codes back into the *same* nestopt exception classes
+// (I/errors.hpp), so callers written against the reference -- evaluate_
+// candidate-style code catching `const nestopt::Error&` -- behave the same.
+//
+// Replaced reference functions (I/ = proj/include/nestopt/):
+//   fisher_potential   I/nnet.hpp:321  -> nb200::fisher_potential
+//   forward            I/nnet.hpp:180  -> nb200::forward (probs + loss)
+//   layer_forward      I/nnet.hpp:130  -> nb200::layer_forward
+//   reference_conv     I/interp.hpp:152 -> nb200::reference_conv
+//   evaluate_all       I/search.hpp:315 -> nb200::evaluate_all_gpu
+//   run_search         I/search.hpp:364 -> nb200::run_search_gpu
+// Everything else (draw_candidates, apply, check_semantic_legality,
+// derived_spec, rank_survivors, the report writers) is the reference's own
+// code, called unchanged.
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "nb200.h"
+#include "nestopt/nestopt.hpp"
+
+namespace nb200 {
+
+// A CUDA / device failure surfaced through the reference's error hierarchy.
+struct DeviceError : nestopt::Error {
+  using nestopt::Error::Error;
+};
+
+// nb_status -> the nestopt exception class it mirrors (include/nb200.h).
+[[noreturn]] inline void rethrow(nb_status s) {
+  const std::string m = nb_last_error();
+  switch (s) {
+    case NB_ERR_INVALID_SPEC: throw nestopt::InvalidSpec(m);
+    case NB_ERR_CONFIG: throw nestopt::ConfigError(m);
+    case NB_ERR_SHAPE_MISMATCH: throw nestopt::ShapeMismatch(m);
+    case NB_ERR_CAP_EXCEEDED: throw nestopt::CapExceeded(m);
+    case NB_ERR_TRANSFORM: throw nestopt::TransformError(m);
+    case NB_ERR_PARSE: throw nestopt::ParseError(m);
+    case NB_ERR_IO: throw nestopt::IoError(m);
+    case NB_ERR_GENERIC: throw nestopt::Error(m);
+    default: throw DeviceError("nb200 [" + std::to_string(int(s)) + "]: " + m);
+  }
+}
+
+inline void check(nb_status s) {
+  if (s != NB_OK) rethrow(s);
+}
+
+// ---- descriptors ----------------------------------------------------------
+
+// ConvSpec (I/ir.hpp:26-87) -> nb_conv_spec; keeps the split array alive.
+struct SpecDesc {
+  std::vector<nb_channel_split> splits;
+  nb_conv_spec c{};
+  explicit SpecDesc(const nestopt::ConvSpec& s) {
+    for (const auto& r : s.channel_splits) splits.push_back({r.begin, r.end, r.groups});
+    c = nb_conv_spec{s.ci, s.co, s.h, s.w, s.kh, s.kw, s.stride, s.pad, s.groups,
+                     s.bottleneck_out, s.spatial_div_h, s.spatial_div_w,
+                     int64_t(splits.size()), splits.empty() ? nullptr : splits.data()};
+  }
+};
+
+// Network (I/nnet.hpp:28-79) -> nb_network (+ explicit weights when the
+// network carries them, else the device draws init_weights(seed) itself).
+struct NetDesc {
+  std::vector<SpecDesc> specs;
+  std::vector<nb_layer> layers;
+  std::vector<const double*> wptr;
+  std::vector<double> head;
+  nb_network c{};
+  nb_weights w{};
+  bool explicit_weights = false;
+  explicit NetDesc(const nestopt::Network& n) {
+    specs.reserve(n.layers.size());
+    for (const auto& l : n.layers) specs.emplace_back(l.spec);
+    for (size_t i = 0; i < n.layers.size(); ++i)
+      layers.push_back(nb_layer{specs[i].c, n.layers[i].relu ? 1 : 0, 0});
+    c = nb_network{int64_t(layers.size()), layers.data(), n.num_classes, n.seed};
+    if (!n.weights.empty()) {
+      explicit_weights = true;
+      for (const auto& t : n.weights) wptr.push_back(t.data.data());
+      for (const auto& row : n.head) head.insert(head.end(), row.begin(), row.end());
+      w = nb_weights{wptr.data(), head.data()};
+    }
+  }
+  const nb_weights* weights() const { return explicit_weights ? &w : nullptr; }
+};
+
+// Batch (I/nnet.hpp:81-85) -> nb_batch with the reference's own values.
+struct BatchDesc {
+  std::vector<double> x;
+  std::vector<int32_t> y;
+  nb_batch c{};
+  explicit BatchDesc(const nestopt::Batch& b) {
+    for (const auto& t : b.inputs) x.insert(x.end(), t.data.begin(), t.data.end());
+    for (int v : b.labels) y.push_back(int32_t(v));
+    c = nb_batch{int64_t(b.inputs.size()), x.data(), y.data(), b.seed};
+  }
+};
+
+// ---- contexts and sessions ---------------------------------------------------
+
+class Context {
+ public:
+  explicit Context(int device = 0) { check(nb_ctx_create(device, &p_)); }
+  ~Context() { nb_ctx_destroy(p_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  nb_ctx* get() const { return p_; }
+
+ private:
+  nb_ctx* p_ = nullptr;
+};
+
+// A batch resident in one GPU's HBM (the search's fixed batch).
+class Session {
+ public:
+  Session(Context& ctx, const nestopt::Network& shape, const nestopt::Batch& batch) {
+    NetDesc nd(shape);
+    BatchDesc bd(batch);
+    check(nb_session_create(ctx.get(), &nd.c, &bd.c, &p_));
+  }
+  ~Session() { nb_session_destroy(p_); }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+  nb_session* get() const { return p_; }
+
+ private:
+  nb_session* p_ = nullptr;
+};
+
+// ---- hot-path functions --------------------------------------------------
+
+inline nestopt::FisherReport to_report(const nestopt::Network& net,
+                                       const std::vector<double>& per_channel,
+                                       const std::vector<double>& per_layer, double total,
+                                       uint64_t seed) {
+  nestopt::FisherReport r;
+  r.per_layer = per_layer;
+  r.total = total;
+  r.seed = seed;
+  size_t off = 0;
+  for (const auto& l : net.layers) {
+    const size_t c = size_t(l.spec.co_eff());
+    r.per_channel.emplace_back(per_channel.begin() + long(off), per_channel.begin() + long(off + c));
+    off += c;
+  }
+  return r;
+}
+
+inline size_t channel_total(const nestopt::Network& net) {
+  size_t t = 0;
+  for (const auto& l : net.layers) t += size_t(l.spec.co_eff());
+  return t;
+}
+
+// fisher_potential, I/nnet.hpp:321-352.
+inline nestopt::FisherReport fisher_potential(Context& ctx, const nestopt::Network& net,
+                                              const nestopt::Batch& batch,
+                                              nb_precision prec = NB_PREC_FP32) {
+  NetDesc nd(net);
+  BatchDesc bd(batch);
+  std::vector<double> pc(channel_total(net)), pl(net.layers.size());
+  nb_fisher_out out{pc.data(), pl.data(), 0.0, 0, 0.0, nullptr};
+  check(nb_fisher_potential(ctx.get(), &nd.c, nd.weights(), &bd.c, prec, &out));
+  return to_report(net, pc, pl, out.total, out.seed);
+}
+
+inline nestopt::FisherReport fisher_potential(Session& s, const nestopt::Network& net,
+                                              nb_precision prec = NB_PREC_FP32) {
+  NetDesc nd(net);
+  std::vector<double> pc(channel_total(net)), pl(net.layers.size());
+  nb_fisher_out out{pc.data(), pl.data(), 0.0, 0, 0.0, nullptr};
+  check(nb_session_fisher(s.get(), &nd.c, nd.weights(), prec, &out));
+  return to_report(net, pc, pl, out.total, out.seed);
+}
+
+// forward, I/nnet.hpp:180-197: the outputs ForwardCache exposes to callers
+// (probs, example_loss, loss).
+struct ForwardResult {
+  std::vector<std::vector<double>> probs;
+  std::vector<double> example_loss;
+  double loss = 0.0;
+};
+
+inline ForwardResult forward(Context& ctx, const nestopt::Network& net, const nestopt::Batch& batch,
+                             nb_precision prec = NB_PREC_FP32) {
+  NetDesc nd(net);
+  BatchDesc bd(batch);
+  const size_t n = batch.inputs.size(), k = size_t(net.num_classes);
+  std::vector<double> probs(n * k);
+  ForwardResult r;
+  r.example_loss.resize(n);
+  check(nb_forward(ctx.get(), &nd.c, nd.weights(), &bd.c, prec, probs.data(),
+                   r.example_loss.data(), &r.loss));
+  for (size_t i = 0; i < n; ++i)
+    r.probs.emplace_back(probs.begin() + long(i * k), probs.begin() + long((i + 1) * k));
+  return r;
+}
+
+// reference_conv<double>, I/interp.hpp:151-186 (one image).
+inline nestopt::TensorF reference_conv(Context& ctx, const nestopt::ConvSpec& spec,
+                                       const nestopt::TensorF& input,
+                                       const nestopt::TensorF& weights,
+                                       nb_precision prec = NB_PREC_FP32, bool relu = false) {
+  SpecDesc sd(spec);
+  nestopt::TensorF out({spec.co_eff(), spec.out_h(), spec.out_w()});
+  check(nb_conv_forward(ctx.get(), &sd.c, 1, input.data.data(), weights.data.data(),
+                        out.data.data(), relu ? 1 : 0, prec));
+  return out;
+}
+
+// layer_forward, I/nnet.hpp:130-141.
+inline nestopt::TensorF layer_forward(Context& ctx, const nestopt::Layer& layer,
+                                      const nestopt::TensorF& weights,
+                                      const nestopt::TensorF& input,
+                                      nb_precision prec = NB_PREC_FP32) {
+  return reference_conv(ctx, layer.spec, input, weights, prec, layer.relu);
+}
+
+// ---- the candidate scheduler -------------------------------------------
+
+// The host half of evaluate_candidate (I/search.hpp:219-293): replays the
+// per-layer steps, flushes semantic runs through the reference's brute-force
+// legality check, lowers each layer with derived_spec, and repairs shapes.
+// Returns false when the candidate is decided here (semantic rejection or
+// a non-neural survivor); otherwise `net` is the network to score.
+// Differences from the reference: repair_network's init_weights (0.8 s on
+// the R34 chain) is skipped -- the device draws the same weights from the
+// cached z-streams -- so only Network::validate() runs after propagation.
+inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
+                       const nestopt::SearchConfig& cfg,
+                       const nestopt::FisherReport& origin_fisher, nestopt::Network& net) {
+  using namespace nestopt;
+  std::vector<ConvSpec> specs;
+  for (size_t l = 0; l < origin.layers.size(); ++l) {
+    LoopNest nest = conv_nest(origin.layers[l].spec);
+    LoopNest run_origin = nest;
+    bool pending_semantic = false;
+    auto flush = [&](size_t s) {
+      if (!pending_semantic) return true;
+      LegalityResult lr = check_semantic_legality(run_origin, nest, cfg.cap);
+      pending_semantic = false;
+      if (lr.verdict == Verdict::Illegal) {
+        cand.status = CandidateStatus::RejectedSemantic;
+        cand.reason = "layer " + std::to_string(l) + " steps up to " + std::to_string(s) +
+                      ": " + lr.reason;
+        return false;
+      }
+      return true;
+    };
+    for (size_t s = 0; s < cand.layer_seqs[l].steps.size(); ++s) {
+      const Transform& t = cand.layer_seqs[l].steps[s];
+      try {
+        if (t.cls() == TransformClass::Semantic) {
+          nest = apply(nest, t);
+          pending_semantic = true;
+        } else {
+          if (!flush(s)) return false;
+          nest = apply(nest, t);
+          run_origin = nest;
+        }
+      } catch (const Error& e) {
+        cand.status = CandidateStatus::RejectedSemantic;
+        cand.reason = "layer " + std::to_string(l) + " step " + std::to_string(s + 1) + " (" +
+                      to_dsl(t) + "): " + e.what();
+        return false;
+      }
+    }
+    try {
+      if (!flush(cand.layer_seqs[l].steps.size())) return false;
+    } catch (const Error& e) {
+      cand.status = CandidateStatus::RejectedSemantic;
+      cand.reason = "layer " + std::to_string(l) + ": " + e.what();
+      return false;
+    }
+    std::optional<ConvSpec> spec = derived_spec(nest);
+    if (!spec) {
+      cand.status = CandidateStatus::RejectedSemantic;
+      cand.reason = "layer " + std::to_string(l) + ": rewritten nest is not a convolution operator";
+      return false;
+    }
+    specs.push_back(*spec);
+  }
+  net.layers = origin.layers;
+  net.num_classes = origin.num_classes;
+  net.seed = origin.seed;
+  net.weights.clear();
+  net.head.clear();
+  for (size_t l = 0; l < specs.size(); ++l) net.layers[l].spec = specs[l];
+  try {
+    // repair_network's shape propagation (I/nnet.hpp:372-380)
+    for (size_t l = 1; l < net.layers.size(); ++l) {
+      const ConvSpec& prev = net.layers[l - 1].spec;
+      ConvSpec& cur = net.layers[l].spec;
+      cur.ci = prev.co_eff();
+      cur.h = prev.out_h();
+      cur.w = prev.out_w();
+    }
+    net.validate();
+  } catch (const Error& e) {
+    cand.status = CandidateStatus::RejectedSemantic;
+    cand.reason = std::string("network repair failed: ") + e.what();
+    return false;
+  }
+  const ConvSpec& in0 = origin.layers[0].spec;
+  const ConvSpec& in1 = net.layers[0].spec;
+  if (in0.ci != in1.ci || in0.h != in1.h || in0.w != in1.w) {
+    cand.status = CandidateStatus::RejectedSemantic;
+    cand.reason = "network input shape changed";
+    return false;
+  }
+  cand.macs = network_macs(net);
+  if (!cand.neural) {
+    cand.status = CandidateStatus::Survivor;
+    cand.fisher_total = origin_fisher.total;
+    cand.fisher_per_layer = origin_fisher.per_layer;
+    return false;
+  }
+  return true;
+}
+
+// Scheduler statistics of one evaluate_all_gpu call.
+struct GpuStats {
+  int64_t scored = 0, evaluated = 0, deduplicated = 0;
+  std::vector<double> est_flops, busy_ms;
+  double gates_ms = 0, gpu_ms = 0;
+};
+
+// evaluate_all, I/search.hpp:315-334, on GPU sessions: host gates on
+// cfg.jobs threads (same per-index result slots as the reference), then
+// every neural candidate that passed them is scored by nb_evaluate (dedupe +
+// LPT over the sessions, one worker per GPU), then the reference's accept
+// rule and rejection message are applied.
+inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
+                                 const nestopt::Network& origin,
+                                 const nestopt::SearchConfig& cfg,
+                                 const nestopt::FisherReport& origin_fisher,
+                                 const std::vector<Session*>& sessions,
+                                 nb_precision prec = NB_PREC_FP32) {
+  using namespace nestopt;
+  GpuStats st;
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<Network> nets(cands.size());
+  std::vector<char> pending(cands.size(), 0);
+  {
+    const int jobs = std::max(1, std::min<int>(cfg.jobs, int(cands.size())));
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= cands.size()) return;
+        pending[i] = host_gates(cands[i], origin, cfg, origin_fisher, nets[i]) ? 1 : 0;
+      }
+    };
+    if (jobs == 1) {
+      worker();
+    } else {
+      std::vector<std::thread> pool;
+      for (int j = 0; j < jobs; ++j) pool.emplace_back(worker);
+      for (auto& t : pool) t.join();
+    }
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  std::vector<size_t> idx;
+  for (size_t i = 0; i < cands.size(); ++i)
+    if (pending[i]) idx.push_back(i);
+  st.scored = int64_t(idx.size());
+  if (!idx.empty()) {
+    std::vector<NetDesc> descs;
+    descs.reserve(idx.size());
+    for (size_t i : idx) descs.emplace_back(nets[i]);
+    std::vector<nb_network> cnets;
+    for (auto& d : descs) cnets.push_back(d.c);
+    std::vector<std::vector<double>> pl(idx.size());
+    std::vector<nb_fisher_out> outs(idx.size());
+    for (size_t k = 0; k < idx.size(); ++k) {
+      pl[k].resize(nets[idx[k]].layers.size());
+      outs[k] = nb_fisher_out{nullptr, pl[k].data(), 0.0, 0, 0.0, nullptr};
+    }
+    std::vector<nb_session*> sp;
+    for (auto* s : sessions) sp.push_back(s->get());
+    nb_eval_stats es{};
+    check(nb_evaluate(sp.data(), int32_t(sp.size()), cnets.data(), int64_t(cnets.size()), prec,
+                      outs.data(), &es));
+    st.evaluated = es.evaluated;
+    st.deduplicated = es.deduplicated;
+    for (size_t k = 0; k < sp.size() && k < 16; ++k) {
+      st.est_flops.push_back(es.est_flops[k]);
+      st.busy_ms.push_back(es.busy_ms[k]);
+    }
+    for (size_t k = 0; k < idx.size(); ++k) {
+      Candidate& cand = cands[idx[k]];
+      cand.fisher_total = outs[k].total;
+      cand.fisher_per_layer = pl[k];
+      // fisher_accepts (I/nnet.hpp:356-359) and the message of
+      // I/search.hpp:303-309
+      if (!(outs[k].total >= origin_fisher.total)) {
+        cand.status = CandidateStatus::RejectedFisher;
+        std::ostringstream os;
+        os << "fisher potential dropped: " << outs[k].total << " < " << origin_fisher.total;
+        cand.reason = os.str();
+      } else {
+        cand.status = CandidateStatus::Survivor;
+      }
+    }
+  }
+  auto t2 = std::chrono::steady_clock::now();
+  st.gates_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  st.gpu_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  return st;
+}
+
+// run_search, I/search.hpp:364-393, with the origin score and the candidate
+// evaluation on the GPU sessions (one per entry of `devices`).
+inline nestopt::SearchReport run_search_gpu(const nestopt::Network& origin,
+                                            const nestopt::SearchConfig& cfg,
+                                            const std::vector<int>& devices,
+                                            nb_precision prec = NB_PREC_FP32,
+                                            GpuStats* stats = nullptr) {
+  using namespace nestopt;
+  cfg.validate();
+  origin.validate();
+  if (devices.empty()) throw ConfigError("need at least one device");
+  auto t0 = std::chrono::steady_clock::now();
+  SearchReport rep;
+  rep.config = cfg;
+  rep.origin_macs = network_macs(origin);
+  Batch batch = make_batch(origin, cfg.batch_n, cfg.batch_seed);
+  std::vector<std::unique_ptr<Context>> ctxs;
+  std::vector<std::unique_ptr<Session>> sess;
+  std::vector<Session*> sp;
+  for (int d : devices) {
+    ctxs.push_back(std::make_unique<Context>(d));
+    sess.push_back(std::make_unique<Session>(*ctxs.back(), origin, batch));
+    sp.push_back(sess.back().get());
+  }
+  FisherReport origin_fisher = fisher_potential(*sess[0], origin, prec);
+  rep.origin_fisher = origin_fisher.total;
+
+  auto t1 = std::chrono::steady_clock::now();
+  rep.candidates = draw_candidates(origin, cfg);
+  auto t2 = std::chrono::steady_clock::now();
+  GpuStats st = evaluate_all_gpu(rep.candidates, origin, cfg, origin_fisher, sp, prec);
+  auto t3 = std::chrono::steady_clock::now();
+
+  rep.survivors_ranked = rank_survivors(rep.candidates);
+  for (const auto& c : rep.candidates) {
+    switch (c.status) {
+      case CandidateStatus::Survivor: ++rep.survivors; break;
+      case CandidateStatus::RejectedSemantic: ++rep.rejected_semantic; break;
+      case CandidateStatus::RejectedFisher: ++rep.rejected_fisher; break;
+    }
+  }
+  rep.draw_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  rep.eval_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
+  rep.total_ms = std::chrono::duration<double, std::milli>(t3 - t0).count();
+  if (stats) *stats = st;
+  return rep;
+}
+
+}  // namespace nb200

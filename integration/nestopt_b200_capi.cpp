@@ -1,0 +1,75 @@
+// extern "C" entry points over nestopt_b200.hpp, so the GPU search driver can
+// be driven from Python tests and from the CLI: JSON in (the reference's
+// search-config schema v1 with an embedded "network", as in
+// P/samples/search_toy.json), the reference's search report JSON out
+// (search_report_to_json, I/search.hpp:461-496) plus a "gpu" block.
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "nestopt_b200.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+std::vector<int> parse_devices(const char* devs) {
+  std::vector<int> out;
+  std::stringstream ss(devs ? devs : "0");
+  std::string tok;
+  while (std::getline(ss, tok, ',')) out.push_back(std::stoi(tok));
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+const char* nbi_last_error(void) { return g_err.c_str(); }
+void nbi_free(char* p) { std::free(p); }
+
+// Runs the search of `cfg_json` with candidate scoring on the GPU sessions
+// listed in `devices` ("0,1,2,3"; a device may repeat: several sessions on
+// one GPU exercise the multi-worker scheduler).  jobs > 0 overrides the
+// config's host-gate thread count.  Returns 0 or an nb_status-style code.
+int nbi_run_search(const char* cfg_json, const char* devices, int precision, int jobs,
+                   char** report_json) {
+  try {
+    nlohmann::json j = nlohmann::json::parse(cfg_json);
+    nestopt::Network net = nestopt::network_from_json(j.at("network"));
+    nestopt::SearchConfig cfg = nestopt::search_config_from_json(j);
+    if (jobs > 0) cfg.jobs = jobs;
+    nb200::GpuStats st;
+    nestopt::SearchReport rep =
+        nb200::run_search_gpu(net, cfg, parse_devices(devices), nb_precision(precision), &st);
+    nlohmann::json out = nestopt::search_report_to_json(rep);
+    out["gpu"] = {{"devices", parse_devices(devices)},
+                  {"precision", precision},
+                  {"scored", st.scored},
+                  {"evaluated", st.evaluated},
+                  {"deduplicated", st.deduplicated},
+                  {"est_flops", st.est_flops},
+                  {"busy_ms", st.busy_ms},
+                  {"gates_ms", st.gates_ms},
+                  {"gpu_ms", st.gpu_ms}};
+    *report_json = dup(out.dump());
+    return 0;
+  } catch (const nestopt::ConfigError& e) {
+    g_err = e.what();
+    return NB_ERR_CONFIG;
+  } catch (const nb200::DeviceError& e) {
+    g_err = e.what();
+    return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+"""The GPU search driver (run_search, I/search.hpp:364) from Python.
+
+It is the reference's own search pipeline -- draw_candidates, the semantic
+legality gate, derived_spec, rank_survivors and the report writer, compiled
+from the unmodified nestopt headers -- with fisher_potential / evaluate_all
+replaced by the nb200 scheduler (integration/nestopt_b200.hpp), loaded from
+integration/_build/libnb200_nestopt.so.  The report is the reference's
+search_report_to_json schema plus a "gpu" block.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from typing import Optional
+
+from . import abi
+from .api import Precision, _STATUS, Error
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(os.path.dirname(_HERE), "integration", "_build", "libnb200_nestopt.so")
+_lib: Optional[C.CDLL] = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise Error(f"nestopt integration library not built: {SO} (make -C integration)")
+        abi.load()  # libnb200.so first (the integration library links it)
+        lib = C.CDLL(SO)
+        lib.nbi_last_error.restype = C.c_char_p
+        lib.nbi_free.argtypes = [C.c_void_p]
+        lib.nbi_run_search.restype = C.c_int
+        lib.nbi_run_search.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                       C.POINTER(C.c_void_p)]
+        _lib = lib
+    return _lib
+
+
+def run_search_gpu(cfg: dict, devices: str = "0", precision: int = Precision.FP32,
+                   jobs: int = 0) -> dict:
+    """cfg: the reference's search config (schema v1) with an embedded
+    "network" (P/samples/search_toy.json).  devices: comma-separated GPU
+    indices, one session each (repeats allowed)."""
+    lib = load()
+    p = C.c_void_p()
+    rc = lib.nbi_run_search(json.dumps(cfg).encode(), devices.encode(), int(precision),
+                            int(jobs), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode())
+    finally:
+        lib.nbi_free(p)

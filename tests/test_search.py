@@ -1,0 +1,132 @@
+"""The GPU search driver (integration/nestopt_b200.hpp run_search_gpu) against
+the reference's own search reports (tests/golden/search_toy_*.json,
+generated from the unmodified reference by oracle/gen_golden.py and
+oracle/gen_search_golden.py).
+
+Decision parity: every candidate's status is identical to the reference's,
+except a documented near-threshold tie band |cand - origin| / origin <
+TOL_TOTAL (none occur in these fixtures); exact ties (identical networks)
+are exact on the GPU because the scheduler de-duplicates networks and the
+kernels are deterministic.  Fisher totals agree within the FP32-mode
+tolerance (1e-4 relative); reports are bitwise identical for any number of
+GPU sessions.
+"""
+import json
+import math
+import os
+
+import pytest
+
+from conftest import golden
+from paper_2102_06599_b200 import Precision
+from paper_2102_06599_b200 import search as S
+
+TOL_TOTAL = 1e-4
+NEEDS_LIB = pytest.mark.skipif(not os.path.exists(S.SO), reason="integration library not built")
+
+
+@NEEDS_LIB
+def test_integration_library_exports_and_fails_loudly_without_gpu():
+    lib = S.load()
+    for sym in ("nbi_run_search", "nbi_last_error", "nbi_free"):
+        assert hasattr(lib, sym)
+    import paper_2102_06599_b200 as nb
+    if nb.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    cfg = dict(golden("search_toy_100.json")["config"])
+    cfg["network"] = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                                 "search_toy_1000.json")))["config"]["network"]
+    with pytest.raises(Exception, match="no CUDA device|no CPU fallback"):
+        S.run_search_gpu(cfg)
+
+
+def _cfg100():
+    g = golden("search_toy_100.json")
+    cfg = dict(g["config"])
+    cfg["network"] = golden("search_toy_1000.json")["config"]["network"]
+    return g, cfg
+
+
+def _reason_number(r):
+    # "fisher potential dropped: A < B"
+    return float(r.split(":")[1].split("<")[0])
+
+
+def _check_candidates(got, want, origin):
+    near = 0
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g["macs"] == w["macs"], i
+        assert g["neural"] == w["neural"], i
+        if "fisher_total" in w:
+            assert math.isclose(g["fisher_total"], w["fisher_total"], rel_tol=TOL_TOTAL), i
+        if g["status"] != w["status"]:
+            # only a near-threshold tie may flip (none expected)
+            assert abs(w["fisher_total"] - origin) / origin < TOL_TOTAL, (i, g, w)
+            near += 1
+            continue
+        if w["status"] == "rejected_fisher":
+            assert math.isclose(_reason_number(g["reason"]), _reason_number(w["reason"]),
+                                rel_tol=1e-4)
+        else:
+            assert g.get("reason", "") == w.get("reason", ""), i
+    return near
+
+
+@pytest.mark.gpu
+@NEEDS_LIB
+def test_search_toy_100_matches_reference_report():
+    g, cfg = _cfg100()
+    rep = S.run_search_gpu(cfg, "0")
+    assert rep["stats"] == g["stats"]
+    assert rep["origin"]["macs"] == g["origin"]["macs"]
+    assert math.isclose(rep["origin"]["fisher_total"], g["origin"]["fisher_total"],
+                        rel_tol=TOL_TOTAL)
+    for a, b in zip(rep["candidates"], g["candidates"]):
+        assert a["sequences"] == b["sequences"] and a["index"] == b["index"]
+    assert _check_candidates(rep["candidates"], g["candidates"],
+                             g["origin"]["fisher_total"]) == 0
+    assert rep["survivors_ranked"] == g["survivors_ranked"]
+    assert rep["config"] == g["config"]
+
+
+@pytest.mark.gpu
+@NEEDS_LIB
+def test_search_toy_1000_decisions_match_reference():
+    """acceptance criterion 7 (T/acceptance.cpp:406-433): 220 survivors /
+    100 semantic / 680 Fisher rejections, best index 103."""
+    g = golden("search_toy_1000.json")
+    rep = S.run_search_gpu(g["config"], "0", jobs=8)
+    assert rep["stats"] == g["stats"]
+    assert _check_candidates(rep["candidates"], g["candidates"],
+                             g["origin"]["fisher_total"]) == 0
+    assert rep["survivors_ranked"] == g["survivors_ranked"]
+    assert rep["survivors_ranked"][0] == 103
+    assert rep["gpu"]["deduplicated"] > 0
+
+
+@pytest.mark.gpu
+@NEEDS_LIB
+def test_search_report_independent_of_session_count():
+    """T/test_search.cpp:83-94 (jobs=4 == jobs=1), for GPU sessions: the
+    candidates are sharded by LPT over 1 or 3 sessions and the report (minus
+    timing and the gpu block) is bitwise identical."""
+    _, cfg = _cfg100()
+    a = S.run_search_gpu(cfg, "0")
+    b = S.run_search_gpu(cfg, "0,0,0")
+    for r in (a, b):
+        r.pop("timing")
+        r.pop("gpu")
+    assert json.dumps(a, sort_keys=True) == json.dumps(b, sort_keys=True)
+
+
+@pytest.mark.gpu
+@NEEDS_LIB
+def test_tf32_search_decisions_outside_the_tie_band():
+    """The TF32 throughput mode may only flip decisions whose reference
+    margin is inside its stated tolerance (1e-2)."""
+    g, cfg = _cfg100()
+    rep = S.run_search_gpu(cfg, "0", precision=Precision.TF32)
+    origin = g["origin"]["fisher_total"]
+    for a, b in zip(rep["candidates"], g["candidates"]):
+        if a["status"] != b["status"]:
+            assert abs(b["fisher_total"] - origin) / origin < 1e-2
