@@ -3,12 +3,14 @@
 transformed-net inference ms; Fisher candidates/sec").
 
 Workload (configs[1]): the 33-conv ResNet-34 CIFAR chain at batch 128,
-synthetic data (make_batch, seed 1) and init_weights (seed 42); a step is one
-Fisher Potential evaluation (forward + activation gradients + per-channel
-A*g reduction, I/nnet.hpp:321) of one candidate network from a per-layer
-neural search.  Candidates are sharded across ranks by LPT on estimated
-FLOPs (weak scaling: a fixed candidate count per GPU), with no collective on
-the data path.
+synthetic data (make_batch, seed 1) and init_weights (seed 42).  The
+candidate pool is the reference's own per-layer neural search
+(tests/golden/r34_candidates.json: draw_candidates + evaluate_candidate's host
+gates over 12 masked layers, 726 distinct networks).  A step is one Fisher
+Potential evaluation (forward + activation gradients + per-channel A*g
+reduction, I/nnet.hpp:321) of one candidate; every rank scores its LPT share
+of the pool through the product's scheduler (nb_evaluate: --streams
+concurrent sessions per GPU), weak scaling, no collective on the data path.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nb200|reference]
 
@@ -37,11 +39,11 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=64)
+    p.add_argument("--warmup", type=int, default=8)
     p.add_argument("--impl", default="nb200", choices=["nb200", "reference"])
     p.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "simt"])
-    p.add_argument("--candidates-per-gpu", type=int, default=16)
+    p.add_argument("--streams", type=int, default=4, help="concurrent sessions per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=2)
     return p.parse_args()
@@ -50,8 +52,7 @@ def parse():
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
-            d = json.load(f)
-        return d, "measured"
+            return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
             "fallback"
@@ -82,7 +83,7 @@ class Clocks:
                     self.samples.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -112,11 +113,11 @@ class Clocks:
 def reference_sample(layers: int, threads: int):
     """Times the reference's fisher_potential on a bounded slice of the R34
     chain (its first `layers` convs, one image) on `threads` host threads at
-    once (one candidate per thread, like evaluate_all's jobs), and scales it
+    once (one evaluation per thread, like evaluate_all's jobs), and scales it
     to candidates/s of the full chain at N=128 by the Fisher-MAC ratio (the
     reference's cost is linear in MACs and examples, I/nnet.hpp:184,206)."""
     from oracle.oracle import Reference
-    from paper_2102_06599_b200.api import Network
+    from paper_2102_06599_b200.api import Network, count_macs
     from paper_2102_06599_b200.workloads import resnet34_chain
 
     full = resnet34_chain()
@@ -124,7 +125,6 @@ def reference_sample(layers: int, threads: int):
     R = Reference()
 
     def fisher_macs(net, n):
-        from paper_2102_06599_b200.api import count_macs
         m = [count_macs(l.spec) for l in net.layers]
         return n * (sum(m) + sum(m[1:]))
 
@@ -149,7 +149,7 @@ def reference_sample(layers: int, threads: int):
     cand_per_s = threads / (dt * scale)
     return cand_per_s, dt, (f"reference fisher_potential (oracle/_ref) on R34 layers 0-{layers - 1}"
                             f" at N=1, {threads} concurrent on {threads} host threads, "
-                            f"{dt:.2f} s wall, scaled x{scale:.0f} by Fisher MACs to the full "
+                            f"{dt:.2f} s wall, scaled x{scale:.0f} by Fisher MACs to the origin "
                             f"chain at N={N_BATCH} (extrapolated)")
 
 
@@ -158,12 +158,11 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    # CPU code has no warm-up effects beyond the first call; keep the whole
-    # arm within a few minutes (each step is a ~10 s sample).
+    # each step is a ~6-10 s sample; keep the whole arm within a few minutes
     warm, steps = min(args.warmup, 1), min(args.steps, 8)
     for _ in range(warm):
         reference_sample(args.cpu_sample_layers, threads)
-    vals, walls = [], []
+    vals, walls, sample = [], [], ""
     for _ in range(steps):
         v, dt, sample = reference_sample(args.cpu_sample_layers, threads)
         vals.append(v)
@@ -171,9 +170,9 @@ def run_reference(args):
     v = statistics.mean(vals)
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-            "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
+            "ms_per_step": 1e3 / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "resnet34_chain_fisher", "global_batch": N_BATCH,
+            "config": {"workload": "resnet34_chain_fisher_search", "global_batch": N_BATCH,
                        "network": "ResNet-34 CIFAR 33-conv chain (SURVEY App. B)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
@@ -195,8 +194,7 @@ def main():
 
     import paper_2102_06599_b200 as nb
     from paper_2102_06599_b200 import Precision
-    from paper_2102_06599_b200.workloads import (fixture_path, load_candidates,
-                                                 per_layer_candidates, resnet34_chain)
+    from paper_2102_06599_b200.workloads import fixture_path, load_candidates, resnet34_chain
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -207,36 +205,44 @@ def main():
     prec = {"fp32": Precision.FP32, "tf32": Precision.TF32, "simt": Precision.SIMT}[args.precision]
 
     origin = resnet34_chain()
-    fx = fixture_path("r34_candidates.json")
-    pool_n = args.candidates_per_gpu * world
-    if os.path.exists(fx):
-        pool = load_candidates(fx, origin)
-        pool = [pool[i % len(pool)] for i in range(pool_n)]
-        cand_src = "tests/golden/r34_candidates.json (reference draw_candidates + host gates)"
-    else:
-        pool = per_layer_candidates(origin, pool_n)
-        cand_src = "workloads.per_layer_candidates (programmatic per-layer neural rewrites)"
-    costs = [nb.fisher_flops(n, N_BATCH) for n in pool]
-    assign = nb.schedule_lpt(costs, world)
-    mine = [n for n, a in zip(pool, assign) if a == rank]
+    pool = load_candidates(fixture_path("r34_candidates.json"), origin)
+    order = np.random.default_rng(0).permutation(len(pool))
+    pool = [pool[i] for i in order]
+    # warm-up networks and the timed pool are disjoint; the timed pool is
+    # K per rank, LPT-sharded over the ranks by estimated FLOPs
+    warm_pool = pool[:max(1, args.warmup)]
+    timed = pool[len(warm_pool):]
+    need = args.steps * world
+    if need > len(timed):
+        raise SystemExit(f"--steps x gpus = {need} exceeds the {len(timed)} distinct candidates")
+    timed = timed[:need]
+    costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
+    # LPT with exactly K per rank: greedy by cost onto the least-loaded rank
+    # that still has room
+    loads, counts, assign = [0.0] * world, [0] * world, [0] * len(timed)
+    for i in sorted(range(len(timed)), key=lambda i: -costs[i]):
+        r = min((r for r in range(world) if counts[r] < args.steps), key=lambda r: loads[r])
+        assign[i] = r
+        loads[r] += costs[i]
+        counts[r] += 1
+    mine = [n for n, a in zip(timed, assign) if a == rank]
     my_flops = sum(c for c, a in zip(costs, assign) if a == rank)
 
-    ctx = nb.Context(local)
     batch = nb.make_batch(origin, N_BATCH, 1)
-    sess = nb.Session(origin, batch, ctx=ctx)
-    stream = torch.cuda.ExternalStream(ctx.stream())
+    ctxs = [nb.Context(local) for _ in range(args.streams)]
+    sessions = [nb.Session(origin, batch, ctx=c) for c in ctxs]
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def timed(fn, k):
+    def timed_region(fn):
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for i in range(k):
-            fn(i)
+        out = fn()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -245,44 +251,64 @@ def main():
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms
+        return ms, out
 
-    step = lambda i: sess.fisher(mine[i % len(mine)], prec)
-    for i in range(args.warmup):
-        step(i)
-    ctx.reset_stats()
-    ctx.set_profiling(True)
-    l0 = ctx.launch_count()
+    # warm-up (W steps on networks outside the timed pool): packed weights of
+    # the origin's layers, z-streams and arenas on every context
+    nb.evaluate(sessions, warm_pool, prec)
+    for s in sessions:
+        s.fisher(origin, prec)
+    origin_rep = sessions[0].fisher(origin, prec)
+
+    for c in ctxs:
+        c.reset_stats()
+        c.set_profiling(True)
+    l0 = sum(c.launch_count() for c in ctxs)
     with Clocks(local) as clk:
-        ms = timed(step, args.steps)
-    launches = ctx.launch_count() - l0
-    ctx.set_profiling(False)
-    kstats = ctx.kernel_stats()
+        ms, (reps, st) = timed_region(lambda: nb.evaluate(sessions, mine, prec))
+    launches = sum(c.launch_count() for c in ctxs) - l0
+    kstats = {}
+    for c in ctxs:
+        c.set_profiling(False)
+        for k, v in c.kernel_stats().items():
+            a = kstats.setdefault(k, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+            for f in a:
+                a[f] += v[f]
     total_units = args.steps * world
     value = total_units / (ms / 1e3)
 
-    # steps per rank cover (steps/len(mine)) of its queue; FLOP-weighted per step
-    step_flops = sum(nb.fisher_flops(mine[i % len(mine)], N_BATCH) for i in range(args.steps))
-
-    # ---- e2e: public API with host (pinned) batch each step
+    # ---- e2e: the reference-facing call with HOST buffers: sessions built
+    # from the pinned host batch (H2D), evaluate_all over the K candidates,
+    # reports back on the host (D2H), all inside the timed region
     xin = torch.from_numpy(batch.inputs).pin_memory()
     lab = torch.from_numpy(batch.labels).pin_memory()
     hbatch = nb.Batch(xin.numpy(), lab.numpy(), batch.seed)
-    e2e_step = lambda i: nb.fisher_potential(mine[i % len(mine)], hbatch, prec, ctx=ctx)
-    for i in range(min(2, args.warmup)):
-        e2e_step(i)
-    e2e_ms = timed(e2e_step, args.steps)
+
+    def e2e():
+        ss = [nb.Session(origin, hbatch, ctx=c) for c in ctxs]
+        r = nb.evaluate(ss, mine, prec)
+        for s in ss:
+            s.close()
+        return r
+
+    e2e_ms, _ = timed_region(e2e)
     e2e_val = total_units / (e2e_ms / 1e3)
-    h2d = batch.inputs.nbytes + batch.labels.nbytes
-    d2h = 8 * (sum(l.spec.co_eff() for l in origin.layers) + len(origin.layers) +
-               N_BATCH * origin.num_classes)
+    h2d = (batch.inputs.nbytes + batch.labels.nbytes) * len(ctxs) / args.steps
+    d2h = sum(8 * (sum(l.spec.co_eff() for l in n.layers) + len(n.layers) + 2 +
+                   N_BATCH * n.num_classes) for n in mine) / args.steps
 
-    # ---- transformed-net inference (forward of the best-ranked candidate shape)
-    best = min(mine, key=lambda n: nb.network_macs(n))
-    inf_ms = timed(lambda i: sess.forward(best, prec), args.steps) / args.steps
-    inf_origin_ms = timed(lambda i: sess.forward(origin, prec), args.steps) / args.steps
+    # ---- transformed-net inference: forward of the best-ranked survivor
+    # (rank_survivors: macs ascending, fisher descending, I/search.hpp:338)
+    surv = [(nb.network_macs(n), -r.total, i) for i, (n, r) in enumerate(zip(mine, reps))
+            if r.total >= origin_rep.total]
+    best = mine[min(surv)[2]] if surv else origin
+    for _ in range(3):
+        sessions[0].forward(best, prec)
+    inf_ms, _ = timed_region(lambda: [sessions[0].forward(best, prec) for _ in range(10)])
+    inf_o_ms, _ = timed_region(lambda: [sessions[0].forward(origin, prec) for _ in range(10)])
 
-    # ---- roofline of the dominant kernel family
+    # ---- roofline of the dominant kernel family (CUDA events per launch on
+    # the launching stream, inside the timed region)
     pk, pk_kind = peaks()
     dom_name, dom = max(kstats.items(), key=lambda kv: kv[1]["ms"]) if kstats else ("", None)
     roof = None
@@ -293,15 +319,17 @@ def main():
             peak = pk["bf16_tflops"]
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": None, "kernel": dom_name,
-                    "peak_source": f"{pk_kind} bf16 dense (MEASURED_PEAKS.json)",
-                    "launch_ms": avg_ms, "share_of_step": dom["ms"] / ms if ms else None}
+                    "peak_source": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json); the "
+                                   "kernel runs 3xTF32 = 3 tf32 MMAs (tf32 = bf16/2) per fp32 "
+                                   "product, so its own ceiling is peak/6",
+                    "launch_ms": avg_ms, "share_of_step": dom["ms"] / (ms * len(ctxs))}
         else:
             ach = dom["bytes"] / dom["launches"] / (avg_ms / 1e3) / 1e9
             peak = pk["hbm_gbs"]
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": ach / peak, "traffic": None, "kernel": dom_name,
                     "peak_source": f"{pk_kind} HBM copy (MEASURED_PEAKS.json)",
-                    "launch_ms": avg_ms, "share_of_step": dom["ms"] / ms if ms else None}
+                    "launch_ms": avg_ms, "share_of_step": dom["ms"] / (ms * len(ctxs))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -318,14 +346,20 @@ def main():
             "dtype": "f32" if args.precision != "tf32" else "tf32", "data": "synthetic",
             "config": {"workload": "resnet34_chain_fisher_search", "global_batch": N_BATCH,
                        "network": "ResNet-34 CIFAR 33-conv chain (SURVEY App. B)",
-                       "candidates": cand_src, "candidates_per_gpu": args.candidates_per_gpu,
-                       "precision": args.precision, "parallelism": f"candidate-sharded x{world}",
-                       "l2": "inputs larger than L2 (~0.5 GB activations per evaluation)"},
-            "inference_ms": inf_ms, "inference_origin_ms": inf_origin_ms,
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                       "candidates": "tests/golden/r34_candidates.json (reference "
+                                     "draw_candidates + host gates, 12 masked layers)",
+                       "candidates_per_gpu": args.steps, "streams_per_gpu": args.streams,
+                       "precision": args.precision,
+                       "parallelism": f"candidate-sharded x{world} (LPT, no collective)",
+                       "l2": "inputs larger than L2 (~0.5 GB of activations per evaluation)"},
+            "inference_ms": inf_ms / 10, "inference_origin_ms": inf_o_ms / 10,
+            "inference_net_macs": nb.network_macs(best),
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
-            "achieved_tflops_step": step_flops / (ms / 1e3) / 1e12 * 1,
+            "achieved_tflops_step": my_flops / (ms / 1e3) / 1e12,
+            "scheduler": {"evaluated": st.evaluated, "deduplicated": st.deduplicated,
+                          "busy_ms": [round(b, 2) for b in st.busy_ms]},
             "roofline": roof,
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3)}
                         for k, v in kstats.items()},

@@ -4,6 +4,7 @@
 // P/samples/search_toy.json), the reference's search report JSON out
 // (search_report_to_json, I/search.hpp:461-496) plus a "gpu" block.
 #include <cstdlib>
+#include <limits>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -66,6 +67,57 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
   } catch (const nb200::DeviceError& e) {
     g_err = e.what();
     return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+// Host half of a search without a GPU: the reference's draw_candidates and
+// the gates of evaluate_candidate (nb200::host_gates).  Per candidate the
+// output holds its status after the gates ("fisher" = a neural candidate the
+// GPU must score), reason, macs, and for "fisher" candidates the repaired
+// network (network_to_json, I/nnet.hpp:444-454).
+int nbi_gate_candidates(const char* cfg_json, char** out_json) {
+  try {
+    nlohmann::json j = nlohmann::json::parse(cfg_json);
+    nestopt::Network origin = nestopt::network_from_json(j.at("network"));
+    nestopt::SearchConfig cfg = nestopt::search_config_from_json(j);
+    cfg.validate();
+    origin.validate();
+    std::vector<nestopt::Candidate> cands = nestopt::draw_candidates(origin, cfg);
+    nestopt::FisherReport dummy;
+    dummy.total = std::numeric_limits<double>::quiet_NaN();
+    std::vector<nestopt::Network> nets(cands.size());
+    std::vector<char> pend(cands.size(), 0);
+    {
+      std::atomic<size_t> next{0};
+      auto worker = [&]() {
+        for (size_t i; (i = next.fetch_add(1)) < cands.size();)
+          pend[i] = nb200::host_gates(cands[i], origin, cfg, dummy, nets[i]) ? 1 : 0;
+      };
+      std::vector<std::thread> pool;
+      const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+      for (unsigned t = 0; t < nt; ++t) pool.emplace_back(worker);
+      for (auto& t : pool) t.join();
+    }
+    nlohmann::json arr = nlohmann::json::array();
+    for (size_t i = 0; i < cands.size(); ++i) {
+      const nestopt::Candidate& c = cands[i];
+      const nestopt::Network& net = nets[i];
+      const bool pending = pend[i] != 0;
+      nlohmann::json cj{{"status", pending ? "fisher" : nestopt::status_name(c.status)},
+                        {"neural", c.neural},
+                        {"macs", c.macs}};
+      if (!c.reason.empty()) cj["reason"] = c.reason;
+      if (pending) cj["network"] = nestopt::network_to_json(net);
+      arr.push_back(std::move(cj));
+    }
+    *out_json = dup(nlohmann::json{{"candidates", arr}}.dump());
+    return 0;
+  } catch (const nestopt::ConfigError& e) {
+    g_err = e.what();
+    return NB_ERR_CONFIG;
   } catch (const std::exception& e) {
     g_err = e.what();
     return NB_ERR_GENERIC;

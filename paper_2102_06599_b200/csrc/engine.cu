@@ -104,21 +104,21 @@ Profiler::~Profiler() {
 namespace {
 int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
 
-// Largest N tile that divides the per-group width and still yields >= 2
-// waves of tiles on 148 SMs (else the smallest legal one).
-int pick_bn(int n_per_group, int groups, int m_tiles, bool split3) {
+// N tile of a range: the largest that divides the per-group width.  A wider
+// tile re-reads each A (activation) stage for more output channels, which
+// is what bounds the kernel (shared-memory operand traffic, profiles/);
+// SMs left idle by a small tile count are filled by the other candidates
+// the scheduler runs concurrently on the same GPU.
+int pick_bn(int n_per_group, bool split3) {
   static const int o3[] = {128, 64, 32};
   static const int o1[] = {256, 128, 64, 32};
   const int* o = split3 ? o3 : o1;
   const int no = split3 ? 3 : 4;
-  int smallest = 0;
-  for (int i = 0; i < no; ++i) {
-    if (n_per_group % o[i]) continue;
-    smallest = o[i];
-    if (int64_t(m_tiles) * groups * (n_per_group / o[i]) >= 2 * 148) return o[i];
-  }
-  return smallest;
+  for (int i = 0; i < no; ++i)
+    if (n_per_group % o[i] == 0) return o[i];
+  return 0;
 }
+
 // fprop: one phase over the OH x OW output, every tap, A box at
 // (S*oy - P + kh, S*ox - P + kw) (the element stride S is in the tensor map).
 void fprop_phase(const ConvGeom& g, tc::TcArgs& t) {
@@ -219,7 +219,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
           g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
-          const int bn = pick_bn(r.slice_co, r.groups, t.m_tiles, P.split3);
+          const int bn = pick_bn(r.slice_co, P.split3);
           if (bn) {
             t.mode = 0;
             t.n_tiles_per_group = r.slice_co / bn;
@@ -256,7 +256,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
-        const int bn = pick_bn(r.slice_ci, r.groups, t.m_tiles * g.S * g.S, P.split3);
+        const int bn = pick_bn(r.slice_ci, P.split3);
         if (bn) {
           t.mode = 1;
           t.n_tiles_per_group = r.slice_ci / bn;
@@ -338,9 +338,31 @@ const double* ensure_z(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) 
   return buf->as<double>();
 }
 
+// Identity of a layer's packed init_weights weights: the z-stream (seed,
+// layer), the fan-in scale and every offset/family the lowering chose.
+std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) {
+  std::string k = std::to_string(seed) + "/" + std::to_string(l) + "/" + std::to_string(sp.ci) +
+                  "x" + std::to_string(sp.kh) + "x" + std::to_string(sp.kw) + "/" +
+                  std::to_string(lp.wpack_floats);
+  const ConvGeom& g = lp.geom;
+  for (int r = 0; r < g.nranges; ++r) {
+    const RangeDesc& d = g.r[r];
+    k += "|" + std::to_string(d.b) + "," + std::to_string(d.len) + "," + std::to_string(d.groups) +
+         "," + std::to_string(d.wf_off) + "," + std::to_string(d.wd_off) + "," +
+         std::to_string(int(lp.family[r]));
+    if (lp.family[r] == Family::TensorCore)
+      k += "," + std::to_string(lp.tcf[r].w_off) + "," + std::to_string(lp.tcf[r].w_n);
+  }
+  if (lp.dgrad_family == Family::TensorCore)
+    k += "|d" + std::to_string(lp.tcd.w_off) + "," + std::to_string(lp.tcd.w_n);
+  return k;
+}
+
+constexpr size_t kWCacheCap = size_t(8) << 30;  // packed-weight cache bytes per context
+
 void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
                 cudaStream_t st) {
-  float* base = c->wpack.as<float>() + lp.w_off;
+  float* base = lp.wbase;
   for (int r = 0; r < lp.geom.nranges; ++r) {
     PackDst d{base, base, nullptr, nullptr, nullptr, nullptr};
     if (lp.family[r] == Family::TensorCore) {
@@ -374,7 +396,7 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
 void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* x, float* y,
                  bool relu, cudaStream_t st) {
   const ConvGeom& g = lp.geom;
-  float* base = c->wpack.as<float>() + lp.w_off;
+  float* base = lp.wbase;
   for (int r = 0; r < g.nranges; ++r) {
     const RangeDesc& rd = g.r[r];
     const double fl =
@@ -402,7 +424,7 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
                  const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                  double* partial, cudaStream_t st) {
   const ConvGeom& g = lp.geom;
-  float* base = c->wpack.as<float>() + lp.w_off;
+  float* base = lp.wbase;
   const double prev_floats = double(g.N) * g.H * g.W * g.Ci;
   const double by = 4.0 * (double(g.N) * g.OH * g.OW * g.Co + double(lp.wpack_floats) / 6.0 +
                            (a_prev ? prev_floats : 0.0) + (dpre_out ? prev_floats : 0.0) +
@@ -444,7 +466,8 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   const bool want_grads = out.grads != nullptr;
 
   c->act.ensure(size_t(P.act_total) * 4);
-  c->wpack.ensure(size_t(P.w_total) * 4);
+  const bool explicit_w = w && w->layer;
+  if (explicit_w) c->wpack.ensure(size_t(P.w_total) * 4);
   c->part.ensure(size_t(P.part_total) * 8);
   c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
   c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
@@ -469,20 +492,37 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   int64_t wsrc_off = 0;
   for (int64_t l = 0; l < L; ++l) {
     const Spec& sp = net.specs[l];
-    const double* src;
-    double scale;
-    if (w && w->layer) {
+    LayerPlan& lp = P.layers[l];
+    if (explicit_w) {
       double* dst = c->wsrc.as<double>() + wsrc_off;
       NB_CUDA(cudaMemcpyAsync(dst, w->layer[l], size_t(sp.weight_count()) * 8,
                               cudaMemcpyHostToDevice, st));
       wsrc_off += align64(sp.weight_count());
-      src = dst;
-      scale = 1.0;
-    } else {
-      src = ensure_z(c, net.seed, l, sp.weight_count());
-      scale = 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw));  // I/nnet.hpp:65
+      lp.wbase = c->wpack.as<float>() + lp.w_off;
+      pack_layer(c, lp, dst, 1.0, st);
+      continue;
     }
-    pack_layer(c, P.layers[l], src, scale, st);
+    // init_weights draws: W_l = z_l * 1/sqrt(Ci*Kh*Kw) (I/nnet.hpp:64-68),
+    // packed once per distinct (seed, layer, lowering) and cached
+    const std::string key = wkey(net.seed, l, sp, lp);
+    auto it = c->wcache.find(key);
+    if (it == c->wcache.end()) {
+      const size_t bytes = size_t(lp.wpack_floats) * 4;
+      if (c->wcache_bytes + bytes > kWCacheCap) {
+        NB_CUDA(cudaStreamSynchronize(st));
+        c->wcache.clear();
+        c->wcache_bytes = 0;
+      }
+      auto buf = std::make_unique<DevBuf>();
+      buf->ensure(bytes);
+      c->wcache_bytes += buf->bytes;
+      lp.wbase = buf->as<float>();
+      const double* src = ensure_z(c, net.seed, l, sp.weight_count());
+      pack_layer(c, lp, src, 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw)), st);
+      c->wcache.emplace(key, std::move(buf));
+    } else {
+      lp.wbase = it->second->as<float>();
+    }
   }
   const double* head_src;
   double head_scale;
@@ -629,12 +669,13 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
   ctx_activate(ctx);
   cudaStream_t st = ctx->stream;
   NetPlan P = lower(d, n, prec);
-  const LayerPlan& lp = P.layers.back();
+  LayerPlan& lp = P.layers.back();
   const int64_t x_cnt = n * s.ci * s.h * s.w, y_cnt = lp.act_floats;
   ctx->io.ensure(size_t(std::max(x_cnt, y_cnt)) * 8);
   ctx->gtmp.ensure(size_t(align64(x_cnt) + align64(y_cnt)) * 4);
   ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
   ctx->wpack.ensure(size_t(P.w_total) * 4);
+  P.layers.back().wbase = ctx->wpack.as<float>() + P.layers.back().w_off;
   float* xb = ctx->gtmp.as<float>();
   float* yb = xb + align64(x_cnt);
   NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8, cudaMemcpyHostToDevice,

@@ -60,6 +60,7 @@ struct LayerPlan {
   TcPlan tcd;                // dgrad tensor-core plan
   int64_t wpack_floats = 0;  // floats of all packings of this layer
   int64_t w_off = 0;         // offset of this layer's block in the weight arena
+  float* wbase = nullptr;    // the layer's packed weights at run time (arena or cache)
   int64_t act_off = 0;       // offset (floats) of the layer's output activation
   int64_t act_floats = 0;
   int64_t part_off = 0;      // offset (doubles) of its Fisher partials
@@ -115,6 +116,11 @@ struct nb_ctx {
   // device copies of z streams keyed by (seed, stream index)
   std::map<std::pair<uint64_t, int64_t>, std::unique_ptr<nb::DevBuf>> zdev;
   std::map<std::pair<uint64_t, int64_t>, int64_t> zlen;
+  // packed init_weights weights per (seed, layer, lowering) -- candidates of
+  // one search share most layers with the origin, so each distinct layer is
+  // packed once per context
+  std::map<std::string, std::unique_ptr<nb::DevBuf>> wcache;
+  size_t wcache_bytes = 0;
   nb::Profiler prof;
   int64_t launches = 0;
 };

@@ -34,6 +34,8 @@ def load() -> C.CDLL:
         lib.nbi_run_search.restype = C.c_int
         lib.nbi_run_search.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p)]
+        lib.nbi_gate_candidates.restype = C.c_int
+        lib.nbi_gate_candidates.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         _lib = lib
     return _lib
 
@@ -51,5 +53,22 @@ def run_search_gpu(cfg: dict, devices: str = "0", precision: int = Precision.FP3
         raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
     try:
         return json.loads(C.cast(p, C.c_char_p).value.decode())
+    finally:
+        lib.nbi_free(p)
+
+
+def gate_candidates(cfg: dict) -> list:
+    """The host half of a search, no GPU needed: the reference's
+    draw_candidates and evaluate_candidate's gates (I/search.hpp:187-293).
+    Returns one dict per candidate: status ("fisher" = a neural candidate
+    that needs a Fisher score, else the reference's final status), reason,
+    macs, and the repaired network JSON of "fisher" candidates."""
+    lib = load()
+    p = C.c_void_p()
+    rc = lib.nbi_gate_candidates(json.dumps(cfg).encode(), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode())["candidates"]
     finally:
         lib.nbi_free(p)

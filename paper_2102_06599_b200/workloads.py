@@ -118,14 +118,18 @@ def per_layer_candidates(origin: Network, count: int, seed: int = 7) -> List[Net
 
 
 def load_candidates(path: str, origin: Network) -> List[Network]:
-    """Candidate networks from a fixture written by the integration glue
-    (integration/gen_candidates.py): a list of per-layer spec lists."""
+    """Candidate networks of tests/golden/r34_candidates.json (written by
+    oracle/gen_r34_candidates.py from the reference's draw_candidates and
+    evaluate_candidate's host gates): each is the origin with one layer's
+    spec replaced, shapes repaired downstream (repair_network)."""
     with open(path) as f:
         data = json.load(f)
     nets = []
     for c in data["candidates"]:
-        n = Network([Layer(ConvSpec.from_json(sj), sj.get("relu", True)) for sj in c["layers"]],
-                    num_classes=origin.num_classes, seed=origin.seed)
+        l, sj = c["diff"]
+        n = origin.copy()
+        n.layers[l] = Layer(ConvSpec.from_json(dict(sj, ci=sj["ci"])), sj.get("relu", True))
+        repair_network(n)
         nets.append(n)
     return nets
 

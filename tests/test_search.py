@@ -40,6 +40,28 @@ def test_integration_library_exports_and_fails_loudly_without_gpu():
         S.run_search_gpu(cfg)
 
 
+@NEEDS_LIB
+def test_host_gates_match_reference_on_cpu():
+    """nb200::host_gates (evaluate_candidate up to the Fisher call, re-composed
+    from the reference's apply / check_semantic_legality / derived_spec) give
+    the reference's semantic rejections (same reasons), non-neural survivors
+    and MAC counts on the 1000-candidate toy search; every candidate they send
+    to the GPU is one the reference scored."""
+    g = golden("search_toy_1000.json")
+    gated = S.gate_candidates(g["config"])
+    assert len(gated) == len(g["candidates"])
+    for i, (a, b) in enumerate(zip(gated, g["candidates"])):
+        assert a["macs"] == b["macs"], i
+        if a["status"] == "fisher":
+            assert b["neural"] and b["status"] in ("survivor", "rejected_fisher"), i
+            assert "network" in a
+        else:
+            assert a["status"] == b["status"], i
+            assert a.get("reason", "") == b.get("reason", ""), i
+            if a["status"] == "survivor":
+                assert not b["neural"]
+
+
 def _cfg100():
     g = golden("search_toy_100.json")
     cfg = dict(g["config"])
