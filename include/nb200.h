@@ -179,6 +179,8 @@ nb_status nb_ctx_set_profiling(nb_ctx* ctx, int enable);
 nb_status nb_ctx_kernel_stats(nb_ctx* ctx, nb_kernel_stat* stats, int32_t cap,
                               int32_t* count);
 nb_status nb_ctx_reset_stats(nb_ctx* ctx);
+/* Drops the context's packed-weight and z-stream caches (device memory). */
+nb_status nb_ctx_clear_caches(nb_ctx* ctx);
 /* Number of nb200 kernel launches issued by this context so far. */
 int64_t nb_ctx_launch_count(nb_ctx* ctx);
 

@@ -94,6 +94,7 @@ SIGNATURES = {
     "nb_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
     "nb_ctx_kernel_stats": (C.c_int, [vp, P(KernelStatC), C.c_int32, P(C.c_int32)]),
     "nb_ctx_reset_stats": (C.c_int, [vp]),
+    "nb_ctx_clear_caches": (C.c_int, [vp]),
     "nb_ctx_launch_count": (C.c_int64, [vp]),
     "nb_conv_forward": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int32, C.c_int]),
     "nb_conv_dgrad": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int]),

@@ -340,6 +340,10 @@ class Context:
     def reset_stats(self) -> None:
         _check(abi.load().nb_ctx_reset_stats(self.ptr))
 
+    def clear_caches(self) -> None:
+        """Drops the packed-weight and z-stream caches of this context."""
+        _check(abi.load().nb_ctx_clear_caches(self.ptr))
+
     def kernel_stats(self) -> dict:
         arr = (abi.KernelStatC * 64)()
         n = C.c_int32()

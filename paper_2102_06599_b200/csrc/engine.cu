@@ -1,6 +1,7 @@
 // nb200 engine: contexts, sessions, lowering and the Fisher / forward
 // pipelines behind the C ABI (include/nb200.h).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 
@@ -119,6 +120,18 @@ int pick_bn(int n_per_group, bool split3) {
   return 0;
 }
 
+// Split-K factor of a tensor-core launch: when its output tiles cannot fill
+// one wave of SMs, divide the K blocks (taps x 32-channel chunks, at least 4
+// per split) so that tiles x splits still fits in one wave.
+int choose_ksplit(const tc::TcArgs& t, int num_sms) {
+  const int tiles = t.nphase * t.m_tiles * t.n_tiles;
+  int mink = 1 << 30;
+  for (int p = 0; p < t.nphase; ++p) mink = std::min(mink, t.ntaps[p] * t.a_cblocks);
+  if (tiles * 2 > num_sms || mink < 8) return 1;
+  int ks = std::min({num_sms / tiles, mink / 4, 8});
+  return ks >= 2 ? ks : 1;
+}
+
 // fprop: one phase over the OH x OW output, every tap, A box at
 // (S*oy - P + kh, S*ox - P + kw) (the element stride S is in the tensor map).
 void fprop_phase(const ConvGeom& g, tc::TcArgs& t) {
@@ -176,7 +189,7 @@ void dgrad_phases(const ConvGeom& g, tc::TcArgs& t) {
 // tcgen05 implicit GEMM when the range is tensor-core shaped (32-channel K
 // chunks, 16-aligned N), the direct FFMA kernels otherwise -- plus packed-
 // weight, activation and Fisher-partial arena offsets.
-NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
   NetPlan P;
   const bool tc_on = prec != NB_PREC_SIMT;
   P.split3 = prec == NB_PREC_FP32;
@@ -235,6 +248,9 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = r.slice_co;
+            t.ksplit = choose_ksplit(t, num_sms);
+            if (t.ksplit > 1)
+              P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
             tp.bn = bn;
             tp.tile = t;
@@ -273,7 +289,12 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          t.part_tiles_per_img = t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
+          t.ksplit = choose_ksplit(t, num_sms);
+          // split-K dgrad: k_splitk_epilogue writes one partial per image
+          t.part_tiles_per_img =
+              t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
+          if (t.ksplit > 1)
+            P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
           tp.bn = bn;
           tp.tile = t;
@@ -409,7 +430,25 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       tc::TcArgs a = lp.tcf[r].tile;
       a.out = y;
       a.relu = relu ? 1 : 0;
+      a.ws = c->ws.as<float>();
+      a.ws_stride = int64_t(g.N) * g.OH * g.OW * g.Co;
       launch_tc(c, lp.tcf[r], a, P.split3, x, g.Ci, g.W, g.H, g.N, base + lp.tcf[r].w_off, st);
+      if (a.ksplit > 1) {
+        SplitEpi e{};
+        e.ws = a.ws;
+        e.ws_stride = a.ws_stride;
+        e.ksplit = a.ksplit;
+        e.mode = 0;
+        e.N = g.N;
+        e.HW = g.OH * g.OW;
+        e.ld = g.Co;
+        e.c0 = rd.b;
+        e.C = rd.len;
+        e.out = y;
+        e.relu = relu ? 1 : 0;
+        launch_splitk_epilogue(e, st);
+        c->launches++;
+      }
       c->prof.end(st, P.split3 ? "conv_fprop_tc_3xtf32" : "conv_fprop_tc_tf32", fl, by);
     } else {
       launch_fprop_direct(g, r, x, base, y, relu, st);
@@ -438,7 +477,28 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
     a.dpre_out = dpre_out;
     a.partial = partial;
     a.relu_prev = relu_prev ? 1 : 0;
+    a.ws = c->ws.as<float>();
+    a.ws_stride = int64_t(g.N) * g.H * g.W * g.Ci;
     launch_tc(c, lp.tcd, a, P.split3, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
+    if (a.ksplit > 1) {
+      SplitEpi e{};
+      e.ws = a.ws;
+      e.ws_stride = a.ws_stride;
+      e.ksplit = a.ksplit;
+      e.mode = 1;
+      e.N = g.N;
+      e.HW = g.H * g.W;
+      e.ld = g.Ci;
+      e.c0 = 0;
+      e.C = g.Ci;
+      e.a_prev = a_prev;
+      e.dpre_out = dpre_out;
+      e.g_out = g_out;
+      e.partial = partial;
+      e.relu_prev = relu_prev ? 1 : 0;
+      launch_splitk_epilogue(e, st);
+      c->launches++;
+    }
     c->prof.end(st, P.split3 ? "conv_dgrad_tc_3xtf32_fisher" : "conv_dgrad_tc_tf32_fisher",
                 lp.dgrad_flops, by);
   } else {
@@ -462,13 +522,22 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     fail(NB_ERR_CONFIG, "network class count does not match the session batch");
   const int64_t N = s->n, L = net.L(), K = net.num_classes;
   cudaStream_t st = c->stream;
-  NetPlan P = lower(net, N, prec);
+  using clk = std::chrono::steady_clock;
+  auto tp = clk::now();
+  auto phase = [&](const char* name) {
+    const auto now = clk::now();
+    c->prof.host(name, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
+  NetPlan P = lower(net, N, prec, c->num_sms);
   const bool want_grads = out.grads != nullptr;
+  phase("host_lower");
 
   c->act.ensure(size_t(P.act_total) * 4);
   const bool explicit_w = w && w->layer;
   if (explicit_w) c->wpack.ensure(size_t(P.w_total) * 4);
   c->part.ensure(size_t(P.part_total) * 8);
+  if (P.ws_floats) c->ws.ensure(size_t(P.ws_floats) * 4);
   c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
   c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
   if (want_grads) c->gtmp.ensure(size_t(P.act_total) * 4);
@@ -483,6 +552,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   float* act = c->act.as<float>();
   double* part = c->part.as<double>();
 
+  phase("host_alloc");
   // ---- weights: z-stream prefix (init_weights) or explicit, packed on device
   int64_t wsrc_need = 0;
   if (w && w->layer)
@@ -537,6 +607,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     head_scale = 1.0 / std::sqrt(double(net.c_last()));  // I/nnet.hpp:72-73
   }
 
+  phase("host_weights");
   // ---- forward (I/nnet.hpp:180-197)
   const float* x = s->x.as<float>();
   for (int64_t l = 0; l < L; ++l) {
@@ -599,6 +670,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     c->launches++;
   }
 
+  phase("host_launch");
   // ---- results back to the host
   std::vector<double> probs(static_cast<size_t>(N * K)), exl(static_cast<size_t>(N)),
       perch(static_cast<size_t>(P.ch_total));
@@ -627,6 +699,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   }
   NB_CUDA(cudaGetLastError());
   NB_CUDA(cudaStreamSynchronize(st));
+  phase("host_wait_gpu");
   c->prof.resolve();
 
   double lsum = 0.0;
@@ -668,13 +741,14 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   ctx_activate(ctx);
   cudaStream_t st = ctx->stream;
-  NetPlan P = lower(d, n, prec);
+  NetPlan P = lower(d, n, prec, ctx->num_sms);
   LayerPlan& lp = P.layers.back();
   const int64_t x_cnt = n * s.ci * s.h * s.w, y_cnt = lp.act_floats;
   ctx->io.ensure(size_t(std::max(x_cnt, y_cnt)) * 8);
   ctx->gtmp.ensure(size_t(align64(x_cnt) + align64(y_cnt)) * 4);
   ctx->wsrc.ensure(size_t(s.weight_count()) * 8);
   ctx->wpack.ensure(size_t(P.w_total) * 4);
+  if (P.ws_floats) ctx->ws.ensure(size_t(P.ws_floats) * 4);
   P.layers.back().wbase = ctx->wpack.as<float>() + P.layers.back().w_off;
   float* xb = ctx->gtmp.as<float>();
   float* yb = xb + align64(x_cnt);
@@ -849,6 +923,19 @@ nb_status nb_ctx_reset_stats(nb_ctx* ctx) {
     need(ctx, "context");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx->prof.stats.clear();
+  });
+}
+
+nb_status nb_ctx_clear_caches(nb_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "context");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx_activate(ctx);
+    NB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->wcache.clear();
+    ctx->wcache_bytes = 0;
+    ctx->zdev.clear();
+    ctx->zlen.clear();
   });
 }
 

@@ -71,11 +71,12 @@ struct LayerPlan {
 struct NetPlan {
   std::vector<LayerPlan> layers;
   int64_t act_total = 0, w_total = 0, part_total = 0, dpre_floats = 0;
+  int64_t ws_floats = 0;  // split-K workspace (floats)
   int64_t ch_total = 0;  // sum_l C_l
   bool split3 = false;    // 3xTF32 tensor-core numerics (NB_PREC_FP32)
 };
 
-NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec);
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms = 148);
 
 struct KStat {
   int64_t launches = 0;
@@ -89,6 +90,13 @@ class Profiler {
   void begin(cudaStream_t st);
   void end(cudaStream_t st, const char* family, double flops, double bytes);
   void resolve();  // stream must be synchronized
+  // host-side wall time of a pipeline phase (recorded while profiling)
+  void host(const char* phase, double ms) {
+    if (!on) return;
+    KStat& k = stats[phase];
+    k.launches += 1;
+    k.ms += ms;
+  }
   std::map<std::string, KStat> stats;
   ~Profiler();
 
@@ -110,7 +118,7 @@ struct nb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::recursive_mutex mu;
-  nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io;
+  nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws;
   int num_sms = 148;
   nb::PinnedBuf host_io;
   // device copies of z streams keyed by (seed, stream index)

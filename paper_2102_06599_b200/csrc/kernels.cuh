@@ -67,6 +67,26 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
 void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
                          const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                          double* partial, cudaStream_t st);
+// Epilogue of a split-K tensor-core GEMM: v = sum_k ws[k] (fixed order) over
+// an (N, H, W) pixel grid and channels [c0, c0+C) of tensors with `ld`
+// channels.  fprop (mode 0): out = relu?(v).  dgrad (mode 1): g_out = v,
+// dpre_out = v masked by a_prev > 0 (when relu_prev), partial[n][0][c] =
+// sum over the image of a_prev * v (fixed order; one partial tile per image).
+struct SplitEpi {
+  const float* ws;
+  int64_t ws_stride;
+  int ksplit, mode;
+  int N, HW, ld, c0, C;
+  float* out;
+  int relu;
+  const float* a_prev;
+  float* dpre_out;
+  float* g_out;
+  double* partial;
+  int relu_prev;
+};
+void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st);
+
 // GAP + linear head + softmax-CE (+ backward, + last-layer Fisher partial,
 // + the masked head gradient dpre of the last layer).
 struct HeadArgs {

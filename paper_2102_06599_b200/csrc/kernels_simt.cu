@@ -278,6 +278,43 @@ __global__ void __launch_bounds__(512) k_fisher_reduce(const FisherLayer* __rest
   }
 }
 
+// Split-K epilogue: block = 32 channels x 8 pixel lanes, grid = (channel
+// tiles, N); each thread walks pixels p = lane, lane+8, ... of one image.
+__global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int64_t n = blockIdx.y;
+  float contrib = 0.f;
+  if (c < e.C) {
+    for (int p = threadIdx.y; p < e.HW; p += 8) {
+      const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
+      float v = 0.f;
+      for (int k = 0; k < e.ksplit; ++k) v += e.ws[k * e.ws_stride + idx];
+      if (e.mode == 0) {
+        e.out[idx] = (e.relu && !(v > 0.f)) ? 0.f : v;  // I/nnet.hpp:138-139
+      } else {
+        if (e.g_out) e.g_out[idx] = v;
+        if (e.a_prev) {
+          const float a = e.a_prev[idx];
+          contrib = fmaf(a, v, contrib);
+          if (e.dpre_out) e.dpre_out[idx] = (e.relu_prev && !(a > 0.f)) ? 0.f : v;
+        } else if (e.dpre_out) {
+          e.dpre_out[idx] = v;
+        }
+      }
+    }
+  }
+  if (e.mode == 0 || !e.partial) return;
+  red[threadIdx.y][threadIdx.x] = contrib;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < e.C) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    e.partial[n * e.ld + e.c0 + c] = double(s);
+  }
+}
+
 int grid_for(int64_t total, int block) {
   int64_t g = (total + block - 1) / block;
   const int64_t cap = 148 * 32;
@@ -318,6 +355,11 @@ void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbas
   dim3 grid((g.Ci + 31) / 32, dgrad_tiles(g.H, g.W), g.N);
   k_dgrad_direct<<<grid, dim3(32, 8), 0, st>>>(g, dpre, wbase, a_prev, relu_prev, dpre_out,
                                                g_out, partial);
+}
+
+void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st) {
+  dim3 grid((e.C + 31) / 32, e.N);
+  k_splitk_epilogue<<<grid, dim3(32, 8), 0, st>>>(e);
 }
 
 void launch_head(const HeadArgs& a, cudaStream_t st) {

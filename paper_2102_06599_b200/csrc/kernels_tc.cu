@@ -16,9 +16,10 @@
 //               K=8 per instruction, accumulator in TMEM (double-buffered)
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
-//   warps 8-11  (3xTF32 only) split converter: A_hi = rn_tf32(A) in place,
-//               A_lo = rn_tf32(A - A_hi), so the MMA warp can issue
-//               A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (fp32-accurate mode)
+//   warps 8-11  (3xTF32 only) split converter: A_hi = rn_tf32(A),
+//               A_lo = rn_tf32(A - A_hi), written to TMEM (tcgen05.st), so the
+//               MMA warp issues A_hi*B_hi + A_hi*B_lo + A_lo*B_hi with A read
+//               from TMEM and only B from shared memory (fp32-accurate mode)
 // Epilogues: fprop -> ReLU + store; dgrad -> store g, mask with the previous
 // layer's ReLU (dpre for the next dgrad) and per-(image, tile, channel)
 // partial sums of A*g for the Fisher Potential (fixed order, deterministic).
@@ -109,6 +110,31 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
       "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]: the 3xTF32 path keeps its split A halves in
+// TMEM so the tensor core reads only B from shared memory.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+
+// 32 consecutive TMEM columns of this thread's lane <- v[0..31]
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -146,14 +172,41 @@ constexpr int kABytes = 128 * 128;  // 128 pixels x 32 fp32 channels
 template <int BN, bool SPLIT3>
 struct Cfg {
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStageBytes = kABytes * (SPLIT3 ? 2 : 1) + kBBytes * (SPLIT3 ? 2 : 1);
-  static constexpr int kStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
+  // smem stage: [A fp32 (TMA) | B_hi | B_lo?]; in 3xTF32 the split A halves
+  // live in TMEM (64 columns per stage, after the two accumulators)
+  static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
+  static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
+  static constexpr int kTmemStages = SPLIT3 ? (512 - 2 * BN) / 64 : 99;
+  static constexpr int kStages = kSmemStages < kTmemStages ? kSmemStages : kTmemStages;
   static constexpr int kThreads = SPLIT3 ? 384 : 256;
-  static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
+  static constexpr int kTmemCols = SPLIT3 ? 512
+                                 : (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
                                  : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int kAcol0 = 2 * BN;  // first TMEM column of the A stages
   static constexpr int kRedBytes = 128 * 17 * 4;
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
 };
+
+// Work unit t of a launch: phase-major, then M tile, N tile, K split
+// (innermost, so CTAs working on the same output tile run side by side).
+struct Tile {
+  int ph, m, nt, ks, kb0, kb1;
+};
+
+__device__ __forceinline__ Tile decode(const TcArgs& a, int t) {
+  Tile d;
+  d.ks = t % a.ksplit;
+  const int r = t / a.ksplit;
+  const int per_phase = a.m_tiles * a.n_tiles;
+  d.ph = r / per_phase;
+  const int tt = r % per_phase;
+  d.m = tt / a.n_tiles;
+  d.nt = tt % a.n_tiles;
+  const int total = a.ntaps[d.ph] * a.a_cblocks;
+  d.kb0 = d.ks * total / a.ksplit;
+  d.kb1 = (d.ks + 1) * total / a.ksplit;
+  return d;
+}
 
 template <int BN, bool SPLIT3>
 __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
@@ -164,13 +217,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage layout: [A_hi | A_lo? | B_hi | B_lo?]
+  // stage layout: [A | B_hi | B_lo?]
   auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
-  auto a_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
-  auto b_hi = [&](int s) { return smem + s * C::kStageBytes + kABytes * (SPLIT3 ? 2 : 1); };
-  auto b_lo = [&](int s) {
-    return smem + s * C::kStageBytes + kABytes * (SPLIT3 ? 2 : 1) + C::kBBytes;
-  };
+  auto b_hi = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
+  auto b_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes + C::kBBytes; };
   float* red = reinterpret_cast<float*>(smem + S * C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kRedBytes);
   uint64_t* full = bars;            // S
@@ -208,8 +258,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int tiles_per_phase = a.m_tiles * a.n_tiles;
-  const int num_tiles = a.nphase * tiles_per_phase;
+  const int num_tiles = a.nphase * a.m_tiles * a.n_tiles * a.ksplit;
   const uint32_t a_box_bytes = uint32_t(a.BW) * a.BH * a.BNI * 128;
 
   if (warp == 0) {
@@ -218,29 +267,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int ph = t / tiles_per_phase, tt = t % tiles_per_phase;
-        const int m = tt / a.n_tiles, nt = tt % a.n_tiles;
+        const Tile d = decode(a, t);
+        const int m = d.m, nt = d.nt;
         const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
         const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
         const int c_base = a.a_c_base + g * a.a_c_per_group;
         const int row = a.b_row_base + g * a.b_row_per_group + nn * BN;
         const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
-        const int nt_ph = a.ntaps[ph];
-        for (int ti = 0; ti < nt_ph; ++ti) {
-          const int32_t tp = a.taps[ph][ti];
+        for (int kb = d.kb0; kb < d.kb1; ++kb) {
+          const int32_t tp = a.taps[d.ph][kb / a.a_cblocks];
+          const int cb = kb % a.a_cblocks;
           const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
-          const int kbase = tap_kidx(tp) * a.b_k_per_tap;
-          for (int cb = 0; cb < a.a_cblocks; ++cb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
-            tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
-            const int kcoord = kbase + cb * 32;
-            tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
-            if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
-            }
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
+          tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+          const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
+          tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
+          if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -254,7 +300,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-        const int kblocks = a.ntaps[t / tiles_per_phase] * a.a_cblocks;
+        const Tile d = decode(a, t);
+        const int kblocks = d.kb1 - d.kb0;
         const int acc = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -263,18 +310,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(SPLIT3 ? &conv[stage] : &full[stage], phase);
           tc_fence_after();
-          const uint64_t dah = sw128_desc(smem_u32(a_hi(stage)));
           const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
+          if (SPLIT3) {
+            // A_hi / A_lo of this stage in TMEM columns [a_t, a_t+32) / [a_t+32, a_t+64)
+            const uint32_t a_t = tmem_base + uint32_t(C::kAcol0 + stage * 64);
+            const uint64_t dbl = sw128_desc(smem_u32(b_lo(stage)));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t koff = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 B along K
-            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-            mma_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
-            if (SPLIT3) {
-              const uint64_t dal = sw128_desc(smem_u32(a_lo(stage)));
-              const uint64_t dbl = sw128_desc(smem_u32(b_lo(stage)));
-              mma_tf32(d_tmem, dah + koff, dbl + koff, idesc, 1u);
-              mma_tf32(d_tmem, dal + koff, dbh + koff, idesc, 1u);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t koff = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 B along K
+              const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+              mma_tf32_ts(d_tmem, a_t + 8 * k, dbh + koff, idesc, accum);
+              mma_tf32_ts(d_tmem, a_t + 8 * k, dbl + koff, idesc, 1u);
+              mma_tf32_ts(d_tmem, a_t + 32 + 8 * k, dbh + koff, idesc, 1u);
+            }
+          } else {
+            const uint64_t dah = sw128_desc(smem_u32(a_hi(stage)));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t koff = uint64_t(k * 32) >> 4;
+              const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+              mma_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
             }
           }
           mma_commit(&empty[stage]);
@@ -296,8 +351,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int ph = t / tiles_per_phase, tt = t % tiles_per_phase;
-      const int m = tt / a.n_tiles, nt = tt % a.n_tiles;
+      const Tile d = decode(a, t);
+      const int ph = d.ph, m = d.m, nt = d.nt;
       const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
       const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
       const int wi = r % a.BW, hi = (r / a.BW) % a.BH, ni = r / rows_per_img;
@@ -319,7 +374,17 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        if (a.mode == 0) {
+        if (a.ksplit > 1) {
+          // split-K: raw partial sums into this split's copy of the output;
+          // k_splitk_epilogue adds the copies in order and runs the epilogue
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(a.ws + int64_t(d.ks) * a.ws_stride +
+                                                  pix * a.out_ld + col0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        } else if (a.mode == 0) {
           if (valid) {
             float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
 #pragma unroll
@@ -378,8 +443,33 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
                 dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           }
-          if (a.partial) {
-            // deterministic per-(image, channel) sums over this tile's rows
+          if (a.partial && rows_per_img % 32 == 0) {
+            // deterministic per-(image, channel) sums: each warp's 32 rows lie
+            // in one image -- xor-butterfly within the warp, then the image's
+            // warps in order
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+#pragma unroll
+              for (int o = 16; o; o >>= 1) contrib[i] += __shfl_xor_sync(0xffffffffu, contrib[i], o);
+            if (lane == 0) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) red[q * 17 + i] = contrib[i];
+            }
+            named_bar(1, 128);
+            const int wpi = rows_per_img / 32;
+            if (r < a.BNI * 16) {
+              const int img = r / 16, j = r % 16;
+              const int nimg = nb * a.BNI + img;
+              if (nimg < a.nimg) {
+                float s = 0.f;
+                for (int w = img * wpi; w < (img + 1) * wpi; ++w) s += red[w * 17 + j];
+                a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
+                          col0 + c + j] = double(s);
+              }
+            }
+            named_bar(1, 128);
+          } else if (a.partial) {
+            // small images (several per tile): serial sums over each image's rows
 #pragma unroll
             for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
             named_bar(1, 128);
@@ -402,29 +492,33 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       mbar_arrive(&tempty[acc]);
     }
   } else if (SPLIT3 && warp >= 8) {
-    // ---------------- 3xTF32 split converter: A_hi = rn_tf32(A), A_lo = rn_tf32(A - A_hi)
-    const int ct = threadIdx.x - 256;  // 0..127
+    // ---------------- 3xTF32 split converter: thread r owns A row r (TMEM
+    // lane r): reads its 128-byte row from the swizzled stage (16-byte chunk
+    // c sits at c ^ (r & 7)), splits it into rn_tf32 hi/lo halves and stores
+    // them to the stage's 64 TMEM columns
+    const int ct = threadIdx.x - 256;  // 0..127 == TMEM lane
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int kblocks = a.ntaps[t / tiles_per_phase] * a.a_cblocks;
-      for (int kb = 0; kb < kblocks; ++kb) {
+      const Tile d = decode(a, t);
+      for (int kb = d.kb0; kb < d.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
-        uint4* hi = reinterpret_cast<uint4*>(a_hi(stage));
-        uint4* lo = reinterpret_cast<uint4*>(a_lo(stage));
+        const uint4* row = reinterpret_cast<const uint4*>(a_hi(stage) + ct * 128);
+        uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int i = 0; i < kABytes / 16 / 128; ++i) {
-          const int idx = ct + i * 128;
-          const uint4 x = hi[idx];
-          uint4 h, l;
-          split_tf32(x.x, h.x, l.x);
-          split_tf32(x.y, h.y, l.y);
-          split_tf32(x.z, h.z, l.z);
-          split_tf32(x.w, h.w, l.w);
-          hi[idx] = h;
-          lo[idx] = l;
+        for (int c = 0; c < 8; ++c) {
+          const uint4 x = row[c ^ (ct & 7)];
+          split_tf32(x.x, hi[4 * c], lo[4 * c]);
+          split_tf32(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+          split_tf32(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+          split_tf32(x.w, hi[4 * c + 3], lo[4 * c + 3]);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + stage * 64);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
         mbar_arrive(&conv[stage]);
         if (++stage == S) {
           stage = 0;
@@ -489,7 +583,7 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = L.args.nphase * L.args.m_tiles * L.args.n_tiles;
+  const int tiles = L.args.nphase * L.args.m_tiles * L.args.n_tiles * L.args.ksplit;
   const int grid = tiles < L.num_sms ? tiles : L.num_sms;
   k_conv_tc<BN, SPLIT3><<<grid, C::kThreads, C::kSmem, st>>>(L.mapA, L.mapBh, L.mapBl, L.args);
   return cudaGetLastError();

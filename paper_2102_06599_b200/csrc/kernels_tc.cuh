@@ -39,6 +39,13 @@ struct TcArgs {
   int OH, OW;  // largest phase grid
   int BW, BH, BNI, tiles_w, tiles_h, tiles_n, m_tiles;
   int n_tiles, n_tiles_per_group;
+  // split-K: the (tap, channel-chunk) K blocks of a tile are divided into
+  // ksplit contiguous ranges, each accumulated by its own work unit into its
+  // own copy of the output (ws + ks * ws_stride, same layout as out);
+  // k_splitk_epilogue then sums the copies in order and runs the epilogue
+  int ksplit;
+  float* ws;
+  int64_t ws_stride;
   int S;  // element stride of the A box (fprop stride; 1 for dgrad)
   // phases
   int nphase, PS;
