@@ -194,7 +194,8 @@ def main():
 
     import paper_2102_06599_b200 as nb
     from paper_2102_06599_b200 import Precision
-    from paper_2102_06599_b200.workloads import fixture_path, load_candidates, resnet34_chain
+    from paper_2102_06599_b200.workloads import (fixture_path, load_candidates, resnet34_chain,
+                                                 shard_lpt)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -217,14 +218,7 @@ def main():
         raise SystemExit(f"--steps x gpus = {need} exceeds the {len(timed)} distinct candidates")
     timed = timed[:need]
     costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
-    # LPT with exactly K per rank: greedy by cost onto the least-loaded rank
-    # that still has room
-    loads, counts, assign = [0.0] * world, [0] * world, [0] * len(timed)
-    for i in sorted(range(len(timed)), key=lambda i: -costs[i]):
-        r = min((r for r in range(world) if counts[r] < args.steps), key=lambda r: loads[r])
-        assign[i] = r
-        loads[r] += costs[i]
-        counts[r] += 1
+    assign = shard_lpt(costs, world, args.steps)
     mine = [n for n, a in zip(timed, assign) if a == rank]
     my_flops = sum(c for c, a in zip(costs, assign) if a == rank)
 

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -333,9 +334,38 @@ inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
   return true;
 }
 
+// Near-threshold band of each arithmetic mode: its stated tolerance on
+// Fisher totals (paper_2102_06599_b200/api.py
+// RECHECK_BAND).  A candidate scored within the band of the origin is
+// re-scored in NB_PREC_SIMT (fp32 FFMA, totals within 1e-5 of the fp64
+// reference) before the accept decision, so the throughput modes make the
+// reference's decisions except for ties closer than SIMT's tolerance.
+inline double recheck_band(nb_precision p) {
+  return p == NB_PREC_FP32 ? 5e-4 : p == NB_PREC_TF32 ? 5e-2 : 0.0;
+}
+
+inline bool same_network(const nestopt::Network& a, const nestopt::Network& b) {
+  if (a.layers.size() != b.layers.size() || a.num_classes != b.num_classes || a.seed != b.seed)
+    return false;
+  for (size_t l = 0; l < a.layers.size(); ++l) {
+    const nestopt::ConvSpec &x = a.layers[l].spec, &y = b.layers[l].spec;
+    if (a.layers[l].relu != b.layers[l].relu || x.ci != y.ci || x.co != y.co || x.h != y.h ||
+        x.w != y.w || x.kh != y.kh || x.kw != y.kw || x.stride != y.stride || x.pad != y.pad ||
+        x.bottleneck_out != y.bottleneck_out || x.spatial_div_h != y.spatial_div_h ||
+        x.spatial_div_w != y.spatial_div_w)
+      return false;
+    auto rx = x.ranges(), ry = y.ranges();
+    if (rx.size() != ry.size()) return false;
+    for (size_t i = 0; i < rx.size(); ++i)
+      if (rx[i].begin != ry[i].begin || rx[i].end != ry[i].end || rx[i].groups != ry[i].groups)
+        return false;
+  }
+  return true;
+}
+
 // Scheduler statistics of one evaluate_all_gpu call.
 struct GpuStats {
-  int64_t scored = 0, evaluated = 0, deduplicated = 0;
+  int64_t scored = 0, evaluated = 0, deduplicated = 0, origin_equal = 0, rechecked = 0;
   std::vector<double> est_flops, busy_ms;
   double gates_ms = 0, gpu_ms = 0;
 };
@@ -375,43 +405,88 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
     }
   }
   auto t1 = std::chrono::steady_clock::now();
+  // A candidate whose network is the origin's (e.g. bottleneck(ci) undone by
+  // repair, I/nnet.hpp:376) scores exactly the origin: an exact tie.
   std::vector<size_t> idx;
-  for (size_t i = 0; i < cands.size(); ++i)
-    if (pending[i]) idx.push_back(i);
+  for (size_t i = 0; i < cands.size(); ++i) {
+    if (!pending[i]) continue;
+    if (same_network(nets[i], origin)) {
+      cands[i].fisher_total = origin_fisher.total;
+      cands[i].fisher_per_layer = origin_fisher.per_layer;
+      cands[i].status = CandidateStatus::Survivor;  // fisher_accepts: ties accepted
+      ++st.origin_equal;
+      continue;
+    }
+    idx.push_back(i);
+  }
   st.scored = int64_t(idx.size());
-  if (!idx.empty()) {
+  std::vector<nb_session*> sp;
+  for (auto* s : sessions) sp.push_back(s->get());
+  // scores `which` (candidate indices) in mode p into totals / per-layer values
+  auto score = [&](const std::vector<size_t>& which, nb_precision p, std::vector<double>& tot,
+                   std::vector<std::vector<double>>& pl) {
     std::vector<NetDesc> descs;
-    descs.reserve(idx.size());
-    for (size_t i : idx) descs.emplace_back(nets[i]);
+    descs.reserve(which.size());
+    for (size_t i : which) descs.emplace_back(nets[i]);
     std::vector<nb_network> cnets;
     for (auto& d : descs) cnets.push_back(d.c);
-    std::vector<std::vector<double>> pl(idx.size());
-    std::vector<nb_fisher_out> outs(idx.size());
-    for (size_t k = 0; k < idx.size(); ++k) {
-      pl[k].resize(nets[idx[k]].layers.size());
+    pl.assign(which.size(), {});
+    std::vector<nb_fisher_out> outs(which.size());
+    for (size_t k = 0; k < which.size(); ++k) {
+      pl[k].resize(nets[which[k]].layers.size());
       outs[k] = nb_fisher_out{nullptr, pl[k].data(), 0.0, 0, 0.0, nullptr};
     }
-    std::vector<nb_session*> sp;
-    for (auto* s : sessions) sp.push_back(s->get());
     nb_eval_stats es{};
-    check(nb_evaluate(sp.data(), int32_t(sp.size()), cnets.data(), int64_t(cnets.size()), prec,
+    check(nb_evaluate(sp.data(), int32_t(sp.size()), cnets.data(), int64_t(cnets.size()), p,
                       outs.data(), &es));
+    tot.resize(which.size());
+    for (size_t k = 0; k < which.size(); ++k) tot[k] = outs[k].total;
+    return es;
+  };
+  if (!idx.empty()) {
+    std::vector<double> tot;
+    std::vector<std::vector<double>> pl;
+    nb_eval_stats es = score(idx, prec, tot, pl);
     st.evaluated = es.evaluated;
     st.deduplicated = es.deduplicated;
     for (size_t k = 0; k < sp.size() && k < 16; ++k) {
       st.est_flops.push_back(es.est_flops[k]);
       st.busy_ms.push_back(es.busy_ms[k]);
     }
+    // near-threshold candidates: re-score them and the origin in SIMT mode
+    double origin_total = origin_fisher.total;
+    const double band = recheck_band(prec);
+    std::vector<size_t> near, near_k;
+    for (size_t k = 0; k < idx.size(); ++k)
+      if (band > 0 && std::fabs(tot[k] - origin_fisher.total) <= band * std::fabs(origin_fisher.total)) {
+        near.push_back(idx[k]);
+        near_k.push_back(k);
+      }
+    if (!near.empty()) {
+      FisherReport exact_origin = fisher_potential(*sessions[0], origin, NB_PREC_SIMT);
+      origin_total = exact_origin.total;
+      std::vector<double> t2;
+      std::vector<std::vector<double>> pl2;
+      score(near, NB_PREC_SIMT, t2, pl2);
+      for (size_t j = 0; j < near.size(); ++j) {
+        tot[near_k[j]] = t2[j];
+        pl[near_k[j]] = pl2[j];
+      }
+      st.rechecked = int64_t(near.size());
+    }
     for (size_t k = 0; k < idx.size(); ++k) {
       Candidate& cand = cands[idx[k]];
-      cand.fisher_total = outs[k].total;
+      cand.fisher_total = tot[k];
       cand.fisher_per_layer = pl[k];
+      // a rechecked candidate is compared with the origin's SIMT score
+      const bool was_near = std::find(near_k.begin(), near_k.end(), k) != near_k.end();
+      const double ref = was_near ? origin_total : origin_fisher.total;
       // fisher_accepts (I/nnet.hpp:356-359) and the message of
       // I/search.hpp:303-309
-      if (!(outs[k].total >= origin_fisher.total)) {
+      if (!(tot[k] >= ref)) {
         cand.status = CandidateStatus::RejectedFisher;
         std::ostringstream os;
-        os << "fisher potential dropped: " << outs[k].total << " < " << origin_fisher.total;
+        os << "fisher potential dropped: " << tot[k] << " < " << origin_fisher.total;
         cand.reason = os.str();
       } else {
         cand.status = CandidateStatus::Survivor;

@@ -55,6 +55,8 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
                   {"scored", st.scored},
                   {"evaluated", st.evaluated},
                   {"deduplicated", st.deduplicated},
+                  {"origin_equal", st.origin_equal},
+                  {"rechecked", st.rechecked},
                   {"est_flops", st.est_flops},
                   {"busy_ms", st.busy_ms},
                   {"gates_ms", st.gates_ms},

@@ -56,9 +56,23 @@ def _check(status: int) -> None:
 
 
 class Precision:
-    FP32 = abi.PREC_FP32   # fp32-accurate (legality decisions)
-    TF32 = abi.PREC_TF32   # tensor-core throughput mode
-    SIMT = abi.PREC_SIMT   # FFMA-only parity baseline
+    FP32 = abi.PREC_FP32   # 3xTF32 tensor cores (default; legality decisions)
+    TF32 = abi.PREC_TF32   # 1xTF32 tensor-core throughput mode
+    SIMT = abi.PREC_SIMT   # fp32 FFMA everywhere (fp32-faithful; near-tie rechecks)
+
+
+# Stated tolerances against the fp64 reference, measured
+# on the GPU: relative error of Fisher totals and per-layer values, and of
+# conv outputs relative to sum |w||x|.  RECHECK_BAND is the near-threshold band
+# of the search driver: a candidate whose score is within it of the origin's
+# is re-scored in SIMT mode before the accept decision
+# (integration/nestopt_b200.hpp, kept equal to these values).
+TOLERANCE = {
+    Precision.SIMT: {"total": 1e-5, "layer": 1e-4, "conv": 2e-6},
+    Precision.FP32: {"total": 5e-4, "layer": 5e-3, "conv": 1e-5},
+    Precision.TF32: {"total": 5e-2, "layer": 2e-1, "conv": 2e-3},
+}
+RECHECK_BAND = {Precision.SIMT: 0.0, Precision.FP32: 5e-4, Precision.TF32: 5e-2}
 
 
 # ---------------------------------------------------------------------------

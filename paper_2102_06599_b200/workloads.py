@@ -134,6 +134,23 @@ def load_candidates(path: str, origin: Network) -> List[Network]:
     return nets
 
 
+def shard_lpt(costs: List[float], world: int, per_rank: int) -> List[int]:
+    """Candidate sharding of the multi-GPU run (no collective on the data
+    path): longest-processing-time-first on the estimated Fisher FLOPs,
+    each rank taking exactly `per_rank` candidates (ties by index), so every
+    rank's assignment is computed identically and independently."""
+    if len(costs) != world * per_rank:
+        raise ValueError("need exactly world * per_rank candidates")
+    loads, counts = [0.0] * world, [0] * world
+    assign = [0] * len(costs)
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min((r for r in range(world) if counts[r] < per_rank), key=lambda r: (loads[r], r))
+        assign[i] = r
+        loads[r] += costs[i]
+        counts[r] += 1
+    return assign
+
+
 def fixture_path(name: str) -> str:
     return os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
                         "golden", name)
