@@ -379,7 +379,7 @@ std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) 
   return k;
 }
 
-constexpr size_t kWCacheCap = size_t(8) << 30;  // packed-weight cache bytes per context
+constexpr size_t kWCacheCap = size_t(2) << 30;  // packed-weight slab bytes per context
 
 void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
                 cudaStream_t st) {
@@ -560,6 +560,27 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   if (w && w->head) wsrc_need += align64(K * net.c_last());
   if (wsrc_need) c->wsrc.ensure(size_t(wsrc_need) * 8);
   int64_t wsrc_off = 0;
+  // init_weights draws: W_l = z_l * 1/sqrt(Ci*Kh*Kw) (I/nnet.hpp:64-68),
+  // packed once per distinct (seed, layer, lowering) into the context's slab.
+  // The slab is reset before (never during) a run whose misses do not fit,
+  // so no pointer handed to this run is overwritten by it.
+  std::vector<std::string> keys;
+  if (!explicit_w) {
+    size_t miss = 0, all = 0;
+    for (int64_t l = 0; l < L; ++l) {
+      keys.push_back(wkey(net.seed, l, net.specs[l], P.layers[l]));
+      const size_t bytes = (size_t(P.layers[l].wpack_floats) * 4 + 255) & ~size_t(255);
+      all += bytes;
+      if (!c->wcache.count(keys.back())) miss += bytes;
+    }
+    if (!c->wslab.p) c->wslab.ensure(std::max(kWCacheCap, all));
+    if (c->wcache_bytes + miss > c->wslab.bytes) {
+      NB_CUDA(cudaStreamSynchronize(st));
+      c->wcache.clear();
+      c->wcache_bytes = 0;
+      if (all > c->wslab.bytes) c->wslab.ensure(all);
+    }
+  }
   for (int64_t l = 0; l < L; ++l) {
     const Spec& sp = net.specs[l];
     LayerPlan& lp = P.layers[l];
@@ -572,27 +593,16 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       pack_layer(c, lp, dst, 1.0, st);
       continue;
     }
-    // init_weights draws: W_l = z_l * 1/sqrt(Ci*Kh*Kw) (I/nnet.hpp:64-68),
-    // packed once per distinct (seed, layer, lowering) and cached
-    const std::string key = wkey(net.seed, l, sp, lp);
-    auto it = c->wcache.find(key);
-    if (it == c->wcache.end()) {
-      const size_t bytes = size_t(lp.wpack_floats) * 4;
-      if (c->wcache_bytes + bytes > kWCacheCap) {
-        NB_CUDA(cudaStreamSynchronize(st));
-        c->wcache.clear();
-        c->wcache_bytes = 0;
-      }
-      auto buf = std::make_unique<DevBuf>();
-      buf->ensure(bytes);
-      c->wcache_bytes += buf->bytes;
-      lp.wbase = buf->as<float>();
-      const double* src = ensure_z(c, net.seed, l, sp.weight_count());
-      pack_layer(c, lp, src, 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw)), st);
-      c->wcache.emplace(key, std::move(buf));
-    } else {
-      lp.wbase = it->second->as<float>();
+    auto it = c->wcache.find(keys[size_t(l)]);
+    if (it != c->wcache.end()) {
+      lp.wbase = it->second;
+      continue;
     }
+    lp.wbase = reinterpret_cast<float*>(static_cast<char*>(c->wslab.p) + c->wcache_bytes);
+    c->wcache_bytes += (size_t(lp.wpack_floats) * 4 + 255) & ~size_t(255);
+    const double* src = ensure_z(c, net.seed, l, sp.weight_count());
+    pack_layer(c, lp, src, 1.0 / std::sqrt(double(sp.ci * sp.kh * sp.kw)), st);
+    c->wcache.emplace(keys[size_t(l)], lp.wbase);
   }
   const double* head_src;
   double head_scale;

@@ -127,7 +127,9 @@ struct nb_ctx {
   // packed init_weights weights per (seed, layer, lowering) -- candidates of
   // one search share most layers with the origin, so each distinct layer is
   // packed once per context
-  std::map<std::string, std::unique_ptr<nb::DevBuf>> wcache;
+  // (bump-allocated from one slab, so no cudaMalloc runs per candidate)
+  std::map<std::string, float*> wcache;
+  nb::DevBuf wslab;
   size_t wcache_bytes = 0;
   nb::Profiler prof;
   int64_t launches = 0;

@@ -84,43 +84,112 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
   }
 }
 
-// Direct conv fprop of one range: one thread per (output pixel, channel),
-// channel fastest.  out[n,oh,ow,b+c] = sum_{kh,kw,j} Wf[tap][j][c] *
-// x[n, s*oh-p+kh, s*ow-p+kw, g*slice_ci + j], padded taps skipped
-// (I/nnet.hpp:121-123).
-__global__ void k_fprop_direct(ConvGeom g, int ri, const float* __restrict__ x,
-                               const float* __restrict__ wbase, float* __restrict__ y,
-                               bool relu) {
+// Direct conv fprop of one range, register-blocked: a block owns 128 output
+// pixels x CO_T output channels of one group; the group's weights for those
+// channels are staged in shared memory K-chunk by K-chunk (Wf[tap][j][co]),
+// every thread keeps its pixel's CO_T accumulators in registers and each
+// input value it loads feeds CO_T FMAs (weights are shared-memory
+// broadcasts).  Padded taps are skipped (I/nnet.hpp:121-123).
+constexpr int kFpPix = 128;
+constexpr int kFpKChunk = 128;
+
+template <int CO_T>
+__global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
+                                                          const float* __restrict__ x,
+                                                          const float* __restrict__ wbase,
+                                                          float* __restrict__ y, bool relu) {
+  __shared__ float ws[kFpKChunk][CO_T];
   const RangeDesc r = g.r[ri];
   const float* __restrict__ wf = wbase + r.wf_off;
-  const int64_t total = int64_t(g.N) * g.OH * g.OW * r.len;
-  const int taps = g.KH * g.KW;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int(i % r.len);
-    int64_t p = i / r.len;
-    const int ow = int(p % g.OW);
-    p /= g.OW;
-    const int oh = int(p % g.OH);
-    const int64_t n = p / g.OH;
-    const int grp = c / r.slice_co;
-    float acc = 0.f;
-    for (int kh = 0; kh < g.KH; ++kh) {
-      const int ih = g.S * oh - g.P + kh;
-      if (ih < 0 || ih >= g.H) continue;
-      for (int kw = 0; kw < g.KW; ++kw) {
-        const int iw = g.S * ow - g.P + kw;
-        if (iw < 0 || iw >= g.W) continue;
-        const float* __restrict__ xr =
-            x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci;
-        const float* __restrict__ wr = wf + int64_t(kh * g.KW + kw) * r.slice_ci * r.len + c;
-#pragma unroll 4
-        for (int j = 0; j < r.slice_ci; ++j) acc = fmaf(xr[j], wr[int64_t(j) * r.len], acc);
+  const int co_chunks = (r.slice_co + CO_T - 1) / CO_T;
+  const int grp = blockIdx.y / co_chunks;
+  const int co0 = (blockIdx.y % co_chunks) * CO_T;  // within the group
+  const int nco = min(CO_T, r.slice_co - co0);
+  const int64_t npix = int64_t(g.N) * g.OH * g.OW;
+  const int64_t pix = int64_t(blockIdx.x) * kFpPix + threadIdx.x;
+  const bool valid = pix < npix;
+  int ow = 0, oh = 0;
+  int64_t n = 0;
+  if (valid) {
+    ow = int(pix % g.OW);
+    oh = int((pix / g.OW) % g.OH);
+    n = pix / (int64_t(g.OW) * g.OH);
+  }
+  float acc[CO_T];
+#pragma unroll
+  for (int t = 0; t < CO_T; ++t) acc[t] = 0.f;
+  const int K = r.slice_ci * g.KH * g.KW;
+  for (int k0 = 0; k0 < K; k0 += kFpKChunk) {
+    const int kn = min(kFpKChunk, K - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kn * CO_T; e += kFpPix) {
+      const int kk = e / CO_T, t = e % CO_T;
+      ws[kk][t] = t < nco ? wf[int64_t(k0 + kk) * r.len + grp * r.slice_co + co0 + t] : 0.f;
+    }
+    __syncthreads();
+    if (valid) {
+      for (int kk = 0; kk < kn; ++kk) {
+        const int k = k0 + kk;
+        const int tap = k / r.slice_ci, j = k - tap * r.slice_ci;
+        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+        const int ih = g.S * oh - g.P + kh, iw = g.S * ow - g.P + kw;
+        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
+        const float xv =
+            __ldg(x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci + j);
+#pragma unroll
+        for (int t = 0; t < CO_T; ++t) acc[t] = fmaf(xv, ws[kk][t], acc[t]);
       }
     }
-    (void)taps;
-    if (relu) acc = acc > 0.f ? acc : 0.f;  // I/nnet.hpp:138-139
-    y[((n * g.OH + oh) * g.OW + ow) * g.Co + r.b + c] = acc;
+  }
+  if (!valid) return;
+  float* yo = y + pix * g.Co + r.b + grp * r.slice_co + co0;
+#pragma unroll
+  for (int t = 0; t < CO_T; ++t)
+    if (t < nco) yo[t] = (relu && !(acc[t] > 0.f)) ? 0.f : acc[t];  // I/nnet.hpp:138-139
+}
+
+// Depthwise fprop (slice_ci = slice_co = 1): threads run over channels
+// (coalesced NHWC loads and stores), each computing kDwRun consecutive
+// output pixels of one row with its channel's taps held in registers.
+constexpr int kDwRun = 4;
+
+__global__ void __launch_bounds__(256) k_fprop_dw(ConvGeom g, int ri,
+                                                  const float* __restrict__ x,
+                                                  const float* __restrict__ wbase,
+                                                  float* __restrict__ y, bool relu) {
+  const RangeDesc r = g.r[ri];
+  const int c = blockIdx.x * 32 + threadIdx.x;  // channel within the range
+  if (c >= r.len) return;
+  const int runs_w = (g.OW + kDwRun - 1) / kDwRun;
+  const int64_t unit = int64_t(blockIdx.y) * 8 + threadIdx.y;  // (n, oh, run)
+  if (unit >= int64_t(g.N) * g.OH * runs_w) return;
+  const int run = int(unit % runs_w);
+  const int oh = int((unit / runs_w) % g.OH);
+  const int64_t n = unit / (int64_t(runs_w) * g.OH);
+  const int ci = c * r.slice_ci / r.slice_co;  // == c for depthwise
+  const float* __restrict__ wf = wbase + r.wf_off;
+  float acc[kDwRun];
+#pragma unroll
+  for (int q = 0; q < kDwRun; ++q) acc[q] = 0.f;
+  for (int kh = 0; kh < g.KH; ++kh) {
+    const int ih = g.S * oh - g.P + kh;
+    if (ih < 0 || ih >= g.H) continue;
+    const float* __restrict__ xr = x + (n * g.H + ih) * int64_t(g.W) * g.Ci + r.b + ci;
+    for (int kw = 0; kw < g.KW; ++kw) {
+      const float wv = __ldg(wf + int64_t(kh * g.KW + kw) * r.len + c);
+#pragma unroll
+      for (int q = 0; q < kDwRun; ++q) {
+        const int ow = run * kDwRun + q;
+        const int iw = g.S * ow - g.P + kw;
+        if (ow < g.OW && iw >= 0 && iw < g.W) acc[q] = fmaf(__ldg(xr + int64_t(iw) * g.Ci), wv, acc[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kDwRun; ++q) {
+    const int ow = run * kDwRun + q;
+    if (ow < g.OW)
+      y[((n * g.OH + oh) * g.OW + ow) * g.Co + r.b + c] = (relu && !(acc[q] > 0.f)) ? 0.f : acc[q];
   }
 }
 
@@ -345,8 +414,24 @@ void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int
 
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
                          float* y, bool relu, cudaStream_t st) {
-  const int64_t total = int64_t(g.N) * g.OH * g.OW * g.r[range].len;
-  k_fprop_direct<<<grid_for(total, 256), 256, 0, st>>>(g, range, x, wbase, y, relu);
+  const RangeDesc& r = g.r[range];
+  if (r.slice_ci == 1 && r.slice_co == 1) {
+    const int64_t units = int64_t(g.N) * g.OH * ((g.OW + kDwRun - 1) / kDwRun);
+    dim3 grid((r.len + 31) / 32, unsigned((units + 7) / 8));
+    k_fprop_dw<<<grid, dim3(32, 8), 0, st>>>(g, range, x, wbase, y, relu);
+    return;
+  }
+  const int64_t npix = int64_t(g.N) * g.OH * g.OW;
+  const unsigned gx = unsigned((npix + kFpPix - 1) / kFpPix);
+  if (r.slice_co <= 16) {
+    k_fprop_blocked<16><<<dim3(gx, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
+  } else if (r.slice_co <= 32) {
+    k_fprop_blocked<32><<<dim3(gx, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
+  } else {
+    const int chunks = (r.slice_co + 63) / 64;
+    k_fprop_blocked<64><<<dim3(gx, r.groups * chunks), kFpPix, 0, st>>>(g, range, x, wbase, y,
+                                                                        relu);
+  }
 }
 
 void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
