@@ -37,7 +37,7 @@ struct ConvGeom {
 
 // Pixel tile of the fused dgrad/Fisher epilogue: partial sums of A*g are
 // produced per (image, tile, channel) and combined in a fixed order.
-constexpr int kDgradTilePix = 64;
+constexpr int kDgradTilePix = 128;
 inline int dgrad_tiles(int H, int W) { return (H * W + kDgradTilePix - 1) / kDgradTilePix; }
 
 // ---- launchers (kernels_simt.cu) -----------------------------------------
