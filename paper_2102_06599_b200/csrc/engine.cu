@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -123,13 +124,36 @@ int pick_bn(int n_per_group, bool split3) {
 // Split-K factor of a tensor-core launch: when its output tiles cannot fill
 // one wave of SMs, divide the K blocks (taps x 32-channel chunks, at least 4
 // per split) so that tiles x splits still fits in one wave.
-int choose_ksplit(const tc::TcArgs& t, int num_sms) {
-  const int tiles = t.nphase * t.m_tiles * t.n_tiles;
+int choose_ksplit(const tc::TcArgs& t, int num_sms, bool pair) {
+  const int tiles = t.nphase * (pair ? (t.m_tiles + 1) / 2 : t.m_tiles) * t.n_tiles;
+  if (pair) num_sms /= 2;
   int mink = 1 << 30;
   for (int p = 0; p < t.nphase; ++p) mink = std::min(mink, t.ntaps[p] * t.a_cblocks);
   if (tiles * 2 > num_sms || mink < 8) return 1;
   int ks = std::min({num_sms / tiles, mink / 4, 8});
   return ks >= 2 ? ks : 1;
+}
+
+// CTA-pair N tile for a range whose per-group width is n: the pair runs
+// M = 256 and each CTA stages half of B, halving the weight-operand traffic
+// per SM.  Measured slower than single-CTA tiles on the R34 layers (fprop
+// 128@16x16: 88 us vs 61 us, tensor pipe 39% vs 56%, profiles/): the
+// single-CTA kernel is not shared-memory or L2 bound at BN=128, and the
+// pair adds a cross-SM handshake per stage.  Off by default; NB_TC_PAIR=1
+// enables it (NB_TC_PAIR_BN=256 allows the single-accumulator 256-wide
+// 3xTF32 pair).  0 = no pair.
+int pick_pair_bn(int n, int m_tiles, bool split3) {
+  static const int mode = [] {
+    const char* e = std::getenv("NB_TC_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const char* cap_env = std::getenv("NB_TC_PAIR_BN");
+  // 3xTF32 at 256 keeps a single TMEM accumulator (no epilogue overlap)
+  const int cap = cap_env ? std::atoi(cap_env) : (split3 ? 128 : 256);
+  if (!mode || m_tiles < 2) return 0;
+  if (n % 256 == 0 && cap >= 256) return 256;
+  if (n % 128 == 0 && cap >= 128) return 128;
+  return 0;
 }
 
 // fprop: one phase over the OH x OW output, every tap, A box at
@@ -232,7 +256,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
-          const int bn = pick_bn(r.slice_co, P.split3);
+          const int pbn = pick_pair_bn(r.slice_co, t.m_tiles, P.split3);
+          const int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
           if (bn) {
             t.mode = 0;
             t.n_tiles_per_group = r.slice_co / bn;
@@ -248,11 +273,12 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = r.slice_co;
-            t.ksplit = choose_ksplit(t, num_sms);
+            t.ksplit = choose_ksplit(t, num_sms, pbn != 0);
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
             tp.bn = bn;
+            tp.pair = pbn != 0;
             tp.tile = t;
             tp.w_n = align64(used);
             tp.w_off = off;
@@ -272,7 +298,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
-        const int bn = pick_bn(r.slice_ci, P.split3);
+        const int pbn = pick_pair_bn(r.slice_ci, t.m_tiles * t.nphase, P.split3);
+        const int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
         if (bn) {
           t.mode = 1;
           t.n_tiles_per_group = r.slice_ci / bn;
@@ -289,7 +316,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          t.ksplit = choose_ksplit(t, num_sms);
+          t.ksplit = choose_ksplit(t, num_sms, pbn != 0);
           // split-K dgrad: k_splitk_epilogue writes one partial per image
           t.part_tiles_per_img =
               t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
@@ -297,6 +324,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
           tp.bn = bn;
+          tp.pair = pbn != 0;
           tp.tile = t;
           tp.w_n = align64(int64_t(g.Ci) * taps * r.slice_co);
           tp.w_off = off;
@@ -406,6 +434,7 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   L.args = args;
   L.bn = tp.bn;
   L.split3 = split3;
+  L.pair = tp.pair;
   L.num_sms = c->num_sms;
   if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");

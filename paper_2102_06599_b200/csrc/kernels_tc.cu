@@ -169,38 +169,103 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 
 constexpr int kABytes = 128 * 128;  // 128 pixels x 32 fp32 channels
 
-template <int BN, bool SPLIT3>
+// ---- cluster (CTA pair) helpers for the cta_group::2 variant
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mma2_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                             uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+// completion of the pair's MMAs -> the barrier at this offset in both CTAs
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+// Kernel configuration.  PAIR = a CTA pair (cluster of 2) runs one
+// M=256 x N=BN MMA (tcgen05 cta_group::2): each CTA stages its own 128 A
+// rows and BN/2 of the B rows, and the pair's tensor cores share both.
+template <int BN, bool SPLIT3, bool PAIR>
 struct Cfg {
-  static constexpr int kBBytes = BN * 128;
+  static constexpr int kBRows = PAIR ? BN / 2 : BN;  // B rows staged per CTA
+  static constexpr int kBBytes = kBRows * 128;
+  // accumulator buffers: two (epilogue overlaps the next tile) unless the
+  // 3xTF32 A stages would not fit next to them in TMEM
+  static constexpr int kAcc = (SPLIT3 && BN >= 256) ? 1 : 2;
   // smem stage: [A fp32 (TMA) | B_hi | B_lo?]; in 3xTF32 the split A halves
-  // live in TMEM (64 columns per stage, after the two accumulators)
+  // live in TMEM (64 columns per stage, after the accumulators)
   static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
   static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
-  static constexpr int kTmemStages = SPLIT3 ? (512 - 2 * BN) / 64 : 99;
+  static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * BN) / 64 : 99;
   static constexpr int kStages = kSmemStages < kTmemStages ? kSmemStages : kTmemStages;
   static constexpr int kThreads = SPLIT3 ? 384 : 256;
   static constexpr int kTmemCols = SPLIT3 ? 512
-                                 : (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
-                                 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int kAcol0 = 2 * BN;  // first TMEM column of the A stages
+                                 : (kAcc * BN) <= 32 ? 32 : (kAcc * BN) <= 64 ? 64
+                                 : (kAcc * BN) <= 128 ? 128 : (kAcc * BN) <= 256 ? 256 : 512;
+  static constexpr int kAcol0 = kAcc * BN;  // first TMEM column of the A stages
   static constexpr int kRedBytes = 128 * 17 * 4;
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
 };
 
-// Work unit t of a launch: phase-major, then M tile, N tile, K split
-// (innermost, so CTAs working on the same output tile run side by side).
+// Work unit u of a launch: phase-major, then M tile (M tile pair for PAIR),
+// N tile, K split (innermost, so units of one output tile run side by side).
 struct Tile {
   int ph, m, nt, ks, kb0, kb1;
 };
 
-__device__ __forceinline__ Tile decode(const TcArgs& a, int t) {
+template <bool PAIR>
+__device__ __forceinline__ Tile decode(const TcArgs& a, int u, int rank) {
   Tile d;
-  d.ks = t % a.ksplit;
-  const int r = t / a.ksplit;
-  const int per_phase = a.m_tiles * a.n_tiles;
+  d.ks = u % a.ksplit;
+  const int r = u / a.ksplit;
+  const int m_units = PAIR ? (a.m_tiles + 1) / 2 : a.m_tiles;
+  const int per_phase = m_units * a.n_tiles;
   d.ph = r / per_phase;
   const int tt = r % per_phase;
-  d.m = tt / a.n_tiles;
+  d.m = PAIR ? 2 * (tt / a.n_tiles) + rank : tt / a.n_tiles;
   d.nt = tt % a.n_tiles;
   const int total = a.ntaps[d.ph] * a.a_cblocks;
   d.kb0 = d.ks * total / a.ksplit;
@@ -208,12 +273,13 @@ __device__ __forceinline__ Tile decode(const TcArgs& a, int t) {
   return d;
 }
 
-template <int BN, bool SPLIT3>
-__global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
+template <int BN, bool SPLIT3, bool PAIR>
+__global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
               const __grid_constant__ CUtensorMap mapBl, const TcArgs a) {
-  using C = Cfg<BN, SPLIT3>;
+  using C = Cfg<BN, SPLIT3, PAIR>;
   constexpr int S = C::kStages;
+  constexpr int NACC = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -223,23 +289,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
   auto b_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes + C::kBBytes; };
   float* red = reinterpret_cast<float*>(smem + S * C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kRedBytes);
-  uint64_t* full = bars;            // S
-  uint64_t* conv = bars + S;        // S (3xTF32 converter done)
-  uint64_t* empty = bars + 2 * S;   // S
-  uint64_t* tfull = bars + 3 * S;   // 2
-  uint64_t* tempty = bars + 3 * S + 2;  // 2
+  uint64_t* full = bars;            // S: this CTA's TMA bytes landed
+  uint64_t* ready = bars + S;       // S: stage ready for the MMA (split A in TMEM /
+                                    //    both CTAs' data landed) -- MMA CTA's copy
+  uint64_t* empty = bars + 2 * S;   // S: the MMAs reading the stage are done
+  uint64_t* tfull = bars + 3 * S;   // 2: accumulator complete
+  uint64_t* tempty = bars + 3 * S + 2;  // 2: accumulator drained (MMA CTA's copy)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  constexpr int kCtas = PAIR ? 2 : 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&ready[s], kCtas);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], kCtas);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -248,31 +317,48 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     if (SPLIT3) prefetch_map(&mapBl);
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(C::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the barriers the other CTA's threads signal live in the MMA CTA (rank 0)
+  const uint32_t ready_remote = PAIR ? mapa(ready, 0) : 0;
+  const uint32_t tempty_remote = PAIR ? mapa(tempty, 0) : 0;
 
-  const int num_tiles = a.nphase * a.m_tiles * a.n_tiles * a.ksplit;
+  const int m_units = PAIR ? (a.m_tiles + 1) / 2 : a.m_tiles;
+  const int num_units = a.nphase * m_units * a.n_tiles * a.ksplit;
+  const int unit0 = PAIR ? int(blockIdx.x) / 2 : int(blockIdx.x);
+  const int ustep = PAIR ? int(gridDim.x) / 2 : int(gridDim.x);
   const uint32_t a_box_bytes = uint32_t(a.BW) * a.BH * a.BNI * 128;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (both CTAs: own A rows, own B rows)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const Tile d = decode(a, t);
+      for (int u = unit0; u < num_units; u += ustep) {
+        const Tile d = decode<PAIR>(a, u, int(rank));
         const int m = d.m, nt = d.nt;
         const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
         const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
         const int c_base = a.a_c_base + g * a.a_c_per_group;
-        const int row = a.b_row_base + g * a.b_row_per_group + nn * BN;
+        const int row = a.b_row_base + g * a.b_row_per_group + nn * BN + int(rank) * C::kBRows;
         const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
         for (int kb = d.kb0; kb < d.kb1; ++kb) {
           const int32_t tp = a.taps[d.ph][kb / a.a_cblocks];
@@ -292,23 +378,31 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (the pair's rank-0 CTA)
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
-                                 (uint32_t(128 >> 4) << 24);
+                                 (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-        const Tile d = decode(a, t);
+      for (int u = unit0; u < num_units; u += ustep, ++local) {
+        const Tile d = decode<PAIR>(a, u, 0);
         const int kblocks = d.kb1 - d.kb0;
-        const int acc = local & 1;
-        const uint32_t aphase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], aphase ^ 1);
+        const int acc = local % NACC;
+        const uint32_t aphase = (local / NACC) & 1;
+        if (PAIR) {
+          mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        } else {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(SPLIT3 ? &conv[stage] : &full[stage], phase);
+          if (PAIR) {
+            mbar_wait_cluster(&ready[stage], phase);
+          } else {
+            mbar_wait(SPLIT3 ? &ready[stage] : &full[stage], phase);
+          }
           tc_fence_after();
           const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
           if (SPLIT3) {
@@ -319,9 +413,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
             for (int k = 0; k < 4; ++k) {
               const uint64_t koff = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 B along K
               const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-              mma_tf32_ts(d_tmem, a_t + 8 * k, dbh + koff, idesc, accum);
-              mma_tf32_ts(d_tmem, a_t + 8 * k, dbl + koff, idesc, 1u);
-              mma_tf32_ts(d_tmem, a_t + 32 + 8 * k, dbh + koff, idesc, 1u);
+              if (PAIR) {
+                mma2_tf32_ts(d_tmem, a_t + 8 * k, dbh + koff, idesc, accum);
+                mma2_tf32_ts(d_tmem, a_t + 8 * k, dbl + koff, idesc, 1u);
+                mma2_tf32_ts(d_tmem, a_t + 32 + 8 * k, dbh + koff, idesc, 1u);
+              } else {
+                mma_tf32_ts(d_tmem, a_t + 8 * k, dbh + koff, idesc, accum);
+                mma_tf32_ts(d_tmem, a_t + 8 * k, dbl + koff, idesc, 1u);
+                mma_tf32_ts(d_tmem, a_t + 32 + 8 * k, dbh + koff, idesc, 1u);
+              }
             }
           } else {
             const uint64_t dah = sw128_desc(smem_u32(a_hi(stage)));
@@ -329,16 +429,46 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
             for (int k = 0; k < 4; ++k) {
               const uint64_t koff = uint64_t(k * 32) >> 4;
               const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-              mma_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
+              if (PAIR) {
+                mma2_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
+              } else {
+                mma_tf32(d_tmem, dah + koff, dbh + koff, idesc, accum);
+              }
             }
           }
-          mma_commit(&empty[stage]);
+          if (PAIR) {
+            mma2_commit_both(&empty[stage]);
+          } else {
+            mma_commit(&empty[stage]);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);  // with no taps (empty phase) this arrives at once
+        // with no taps (empty phase) this arrives at once
+        if (PAIR) {
+          mma2_commit_both(&tfull[acc]);
+        } else {
+          mma_commit(&tfull[acc]);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (PAIR && !SPLIT3 && lane == 0) {
+      // ---------------- relay (1xTF32 pair): this CTA's stage landed -> MMA CTA
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = unit0; u < num_units; u += ustep) {
+        const Tile d = decode<PAIR>(a, u, int(rank));
+        for (int kb = d.kb0; kb < d.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -348,21 +478,23 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     const int rows_per_img = a.BW * a.BH;
     const int part_per_phase = a.BNI == 1 ? a.tiles_h * a.tiles_w : 1;
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t aphase = (local >> 1) & 1;
-      const Tile d = decode(a, t);
+    for (int u = unit0; u < num_units; u += ustep, ++local) {
+      const int acc = local % NACC;
+      const uint32_t aphase = (local / NACC) & 1;
+      const Tile d = decode<PAIR>(a, u, int(rank));
       const int ph = d.ph, m = d.m, nt = d.nt;
       const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
       const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
       const int wi = r % a.BW, hi = (r / a.BW) % a.BH, ni = r / rows_per_img;
       const int n = nb * a.BNI + ni, oh = hb * a.BH + hi, ow = wb * a.BW + wi;
-      const bool valid = ni < a.BNI && n < a.nimg && oh < a.OHp[ph] && ow < a.OWp[ph];
+      const bool valid = m < a.m_tiles && ni < a.BNI && n < a.nimg && oh < a.OHp[ph] &&
+                         ow < a.OWp[ph];
       const int64_t pix =
           (int64_t(n) * a.OutH + oh * a.PS + a.py[ph]) * a.OutW + ow * a.PS + a.px[ph];
       const int col0 = a.out_c_base + g * a.out_c_per_group + nn * BN;
       const bool empty_phase = a.ntaps[ph] == 0;
       const int tile_in_img = ph * part_per_phase + (a.BNI == 1 ? hb * a.tiles_w + wb : 0);
+      const bool tile_real = m < a.m_tiles;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
@@ -443,7 +575,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
                 dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           }
-          if (a.partial && rows_per_img % 32 == 0) {
+          if (a.partial && tile_real && rows_per_img % 32 == 0) {
             // deterministic per-(image, channel) sums: each warp's 32 rows lie
             // in one image -- xor-butterfly within the warp, then the image's
             // warps in order
@@ -468,7 +600,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
               }
             }
             named_bar(1, 128);
-          } else if (a.partial) {
+          } else if (a.partial && tile_real) {
             // small images (several per tile): serial sums over each image's rows
 #pragma unroll
             for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
@@ -488,8 +620,16 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
           }
         }
       }
+      // all 128 rows drained -> one arrival per CTA on the MMA CTA's barrier
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      named_bar(1, 128);
+      if (r == 0) {
+        if (PAIR) {
+          mbar_arrive_remote(tempty_remote + uint32_t(acc * 8));
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
+      }
     }
   } else if (SPLIT3 && warp >= 8) {
     // ---------------- 3xTF32 split converter: thread r owns A row r (TMEM
@@ -500,15 +640,18 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const Tile d = decode(a, t);
+    for (int u = unit0; u < num_units; u += ustep) {
+      const Tile d = decode<PAIR>(a, u, int(rank));
       for (int kb = d.kb0; kb < d.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
-        const uint4* row = reinterpret_cast<const uint4*>(a_hi(stage) + ct * 128);
+        const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint4 x = row[c ^ (ct & 7)];
+          uint4 x;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                       : "r"(row + uint32_t((c ^ (ct & 7)) << 4)));
           split_tf32(x.x, hi[4 * c], lo[4 * c]);
           split_tf32(x.y, hi[4 * c + 1], lo[4 * c + 1]);
           split_tf32(x.z, hi[4 * c + 2], lo[4 * c + 2]);
@@ -518,8 +661,16 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        // all 128 rows stored -> one arrival per CTA on the MMA CTA's barrier
         tc_fence_before();
-        mbar_arrive(&conv[stage]);
+        named_bar(2, 128);
+        if (ct == 0) {
+          if (PAIR) {
+            mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+          } else {
+            mbar_arrive(&ready[stage]);
+          }
+        }
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -528,11 +679,20 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3>::kThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(C::kTmemCols));
+    if (PAIR) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::kTmemCols));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::kTmemCols));
+    }
   }
 }
 
@@ -573,20 +733,34 @@ bool make_map_2d(CUtensorMap* m, const float* base, int K, int rows, int box_row
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, bool PAIR>
 cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
-  using C = Cfg<BN, SPLIT3>;
+  using C = Cfg<BN, SPLIT3, PAIR>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3>,
+    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3, PAIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = L.args.nphase * L.args.m_tiles * L.args.n_tiles * L.args.ksplit;
-  const int grid = tiles < L.num_sms ? tiles : L.num_sms;
-  k_conv_tc<BN, SPLIT3><<<grid, C::kThreads, C::kSmem, st>>>(L.mapA, L.mapBh, L.mapBl, L.args);
-  return cudaGetLastError();
+  const TcArgs& a = L.args;
+  const int m_units = PAIR ? (a.m_tiles + 1) / 2 : a.m_tiles;
+  const int units = a.nphase * m_units * a.n_tiles * a.ksplit;
+  const int slots = PAIR ? L.num_sms / 2 : L.num_sms;
+  const int workers = units < slots ? units : slots;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(workers * (PAIR ? 2 : 1)));
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = PAIR ? 2 : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = PAIR ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, PAIR>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
 }  // namespace
@@ -612,24 +786,39 @@ bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, cons
                const float* Blo, int BK, int Brows) {
   const TcArgs& a = L.args;
   if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
-  if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, L.bn)) return false;
-  if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, L.bn)) return false;
+  const int box_rows = L.pair ? L.bn / 2 : L.bn;  // a pair stages half of B per CTA
+  if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, box_rows)) return false;
+  if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, box_rows)) return false;
   return true;
 }
 
 cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
+  if (L.pair) {
+    if (L.split3) {
+      switch (L.bn) {
+        case 128: return launch_t<128, true, true>(L, st);
+        case 256: return launch_t<256, true, true>(L, st);
+      }
+    } else {
+      switch (L.bn) {
+        case 128: return launch_t<128, false, true>(L, st);
+        case 256: return launch_t<256, false, true>(L, st);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
   if (L.split3) {
     switch (L.bn) {
-      case 32: return launch_t<32, true>(L, st);
-      case 64: return launch_t<64, true>(L, st);
-      case 128: return launch_t<128, true>(L, st);
+      case 32: return launch_t<32, true, false>(L, st);
+      case 64: return launch_t<64, true, false>(L, st);
+      case 128: return launch_t<128, true, false>(L, st);
     }
   } else {
     switch (L.bn) {
-      case 32: return launch_t<32, false>(L, st);
-      case 64: return launch_t<64, false>(L, st);
-      case 128: return launch_t<128, false>(L, st);
-      case 256: return launch_t<256, false>(L, st);
+      case 32: return launch_t<32, false, false>(L, st);
+      case 64: return launch_t<64, false, false>(L, st);
+      case 128: return launch_t<128, false, false>(L, st);
+      case 256: return launch_t<256, false, false>(L, st);
     }
   }
   return cudaErrorInvalidValue;

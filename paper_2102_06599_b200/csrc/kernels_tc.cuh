@@ -72,8 +72,9 @@ struct TcArgs {
 struct TcLaunch {
   CUtensorMap mapA, mapBh, mapBl;
   TcArgs args;
-  int bn;
-  bool split3;
+  int bn;       // N tile (of the pair, when pair)
+  bool split3;  // 3xTF32
+  bool pair;    // CTA pair (cluster of 2): M = 256 per tcgen05.mma.cta_group::2
   int num_sms;
 };
 
