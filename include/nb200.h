@@ -197,6 +197,52 @@ nb_status nb_conv_dgrad(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n,
                         const double* dy, const double* w, double* dx,
                         nb_precision prec);
 
+/* ---- general loop nests (execute, I/interp.hpp:67-145) -------------------- */
+/* A transformed conv loop nest in executable form, for nests with no
+ * ConvSpec (derived_spec == nullopt, e.g. the paper's Sequence 1,
+ * I/transforms.hpp:531-550).  Built from the reference's LoopNest by the
+ * bridge (integration/nestopt_b200.hpp nb200::execute): one entry per
+ * multiply-accumulate statement of each block of compute_blocks
+ * (I/ir.hpp:163-218); Init statements are not passed (the output starts at
+ * zero, as execute's provenance-allocated tensor does).
+ * Expressions are postfix programs of (op, arg) int64 pairs:
+ *   0 const arg | 1 slot arg | 2 add the top arg values | 3 mul by arg |
+ *   4 floor-div by arg | 5 floor-mod by arg   (AffineExpr, I/affine.hpp:17-111)
+ */
+typedef struct nb_nest_expr {
+  int32_t nops;
+  const int64_t* code; /* 2 * nops */
+} nb_nest_expr;
+
+typedef struct nb_nest_access {
+  int32_t tensor;   /* 0 = the written tensor O (read-modify-write), 1 = I, 2 = K */
+  int32_t zero_pad; /* out-of-range reads yield zero (else an error) */
+  int32_t rank;
+  const nb_nest_expr* idx; /* rank expressions over the statement's domain values */
+} nb_nest_access;
+
+typedef struct nb_nest_stmt {
+  int32_t depth;           /* loops enclosing the statement */
+  const int64_t* extents;  /* depth trip counts, outermost first */
+  int32_t ndomain;
+  const nb_nest_expr* coord; /* ndomain expressions over the loop values */
+  int32_t naccess;
+  const nb_nest_access* access;
+} nb_nest_stmt;
+
+typedef struct nb_nest {
+  int64_t num_stmts;
+  const nb_nest_stmt* stmts;
+  int64_t out_shape[4], in_shape[4], w_shape[4]; /* unused trailing dims = 1 */
+  int32_t out_rank, in_rank, w_rank;
+} nb_nest;
+
+/* execute<T> (I/interp.hpp:67-145) on the GPU: every MAC instance of the
+ * nest adds prod(reads) into the output cell it addresses (int64 exactly,
+ * or fp64).  is_int != 0: in/w/out are int64, else double. */
+nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int, const void* in,
+                          const void* w, void* out);
+
 /* ---- network-level entry points ----------------------------------------- */
 /* forward, I/nnet.hpp:180-197: probs n x classes, example_loss n, loss. */
 nb_status nb_forward(nb_ctx* ctx, const nb_network* net, const nb_weights* w,

@@ -26,8 +26,10 @@
 #include <cmath>
 #include <memory>
 #include <sstream>
+#include <map>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "nb200.h"
@@ -230,6 +232,146 @@ inline nestopt::TensorF layer_forward(Context& ctx, const nestopt::Layer& layer,
                                       const nestopt::TensorF& input,
                                       nb_precision prec = NB_PREC_FP32) {
   return reference_conv(ctx, layer.spec, input, weights, prec, layer.relu);
+}
+
+// ---- general loop nests (execute, I/interp.hpp:67-145) ----------------------
+
+// A LoopNest in the executable form of nb_nest (include/nb200.h): per block
+// of compute_blocks (I/ir.hpp:163-218), its multiply-accumulate statements
+// with their coordinate programs over the block's loop values and their
+// access programs over the statement's domain values.
+class NestProgram {
+ public:
+  NestProgram(const nestopt::LoopNest& nest, const std::string& out_name,
+              const std::vector<long long>& out_shape, const std::vector<long long>& in_shape,
+              const std::vector<long long>& w_shape) {
+    using namespace nestopt;
+    std::vector<StmtRec> recs;
+    for (const Block& b : compute_blocks(nest)) {
+      const NestPart& part = nest.parts[size_t(b.part)];
+      std::map<std::string, int> slots;
+      for (size_t i = 0; i < b.iters.size(); ++i) slots[b.iters[i].name] = int(i);
+      for (auto [si, depth] : b.stmts) {
+        const Statement& st = part.stmts[size_t(si)];
+        if (st.kind != StmtKind::Mac) continue;  // the output starts at zero
+        StmtRec r;
+        for (int d = 0; d < depth; ++d) r.extents.push_back(b.iters[size_t(d)].extent);
+        std::map<std::string, int> dslots;
+        for (size_t i = 0; i < st.domain.size(); ++i) {
+          dslots[st.domain[i]] = int(i);
+          r.coord.push_back(emit(st.coord.at(st.domain[i]), slots));
+        }
+        for (const AccessMap& acc : st.accesses) {
+          AccRec ar;
+          ar.tensor = acc.tensor == out_name ? 0 : acc.tensor == "I" ? 1 : acc.tensor == "K" ? 2 : -1;
+          if (ar.tensor < 0) throw UnboundTensor("tensor '" + acc.tensor + "' is not bound");
+          if (ar.tensor != 0 && acc.mode != AccessMode::Read)
+            throw Error("nest writes more than one tensor");
+          ar.zero_pad = acc.zero_pad ? 1 : 0;
+          for (const auto& e : acc.indices) ar.idx.push_back(emit(e, dslots));
+          r.acc.push_back(std::move(ar));
+        }
+        recs.push_back(std::move(r));
+      }
+    }
+    recs_ = std::move(recs);
+    for (auto& r : recs_) {
+      r.coord_c.clear();
+      for (auto& c : r.coord) r.coord_c.push_back(nb_nest_expr{int32_t(c.size() / 2), c.data()});
+      r.acc_c.clear();
+      for (auto& a : r.acc) {
+        a.idx_c.clear();
+        for (auto& c : a.idx) a.idx_c.push_back(nb_nest_expr{int32_t(c.size() / 2), c.data()});
+        r.acc_c.push_back(nb_nest_access{a.tensor, a.zero_pad, int32_t(a.idx_c.size()),
+                                         a.idx_c.data()});
+      }
+      stmts_.push_back(nb_nest_stmt{int32_t(r.extents.size()), r.extents.data(),
+                                    int32_t(r.coord_c.size()), r.coord_c.data(),
+                                    int32_t(r.acc_c.size()), r.acc_c.data()});
+    }
+    c_ = nb_nest{};
+    c_.num_stmts = int64_t(stmts_.size());
+    c_.stmts = stmts_.data();
+    auto fill = [](int64_t* d, int32_t& rank, const std::vector<long long>& s) {
+      rank = int32_t(s.size());
+      for (int i = 0; i < 4; ++i) d[i] = i < rank ? s[size_t(i)] : 1;
+    };
+    fill(c_.out_shape, c_.out_rank, out_shape);
+    fill(c_.in_shape, c_.in_rank, in_shape);
+    fill(c_.w_shape, c_.w_rank, w_shape);
+  }
+  const nb_nest* get() const { return &c_; }
+
+ private:
+  struct AccRec {
+    int32_t tensor = 0, zero_pad = 0;
+    std::vector<std::vector<int64_t>> idx;
+    std::vector<nb_nest_expr> idx_c;
+  };
+  struct StmtRec {
+    std::vector<int64_t> extents;
+    std::vector<std::vector<int64_t>> coord;
+    std::vector<nb_nest_expr> coord_c;
+    std::vector<AccRec> acc;
+    std::vector<nb_nest_access> acc_c;
+  };
+  // AffineExpr (I/affine.hpp:17-72) -> postfix (op, arg) pairs over slots
+  static std::vector<int64_t> emit(const nestopt::AffineExpr& e,
+                                   const std::map<std::string, int>& slots) {
+    std::vector<int64_t> out;
+    emit_into(e, slots, out);
+    return out;
+  }
+  static void emit_into(const nestopt::AffineExpr& e, const std::map<std::string, int>& slots,
+                        std::vector<int64_t>& out) {
+    using K = nestopt::AffineExpr::Kind;
+    switch (e.kind) {
+      case K::Const: out.insert(out.end(), {0, e.k}); return;
+      case K::Var: {
+        auto it = slots.find(e.var);
+        if (it == slots.end()) throw nestopt::Error("unbound iterator '" + e.var + "'");
+        out.insert(out.end(), {1, it->second});
+        return;
+      }
+      case K::Add:
+        for (const auto& a : e.args) emit_into(a, slots, out);
+        out.insert(out.end(), {2, int64_t(e.args.size())});
+        return;
+      case K::Mul: emit_into(e.args[0], slots, out); out.insert(out.end(), {3, e.k}); return;
+      case K::Div: emit_into(e.args[0], slots, out); out.insert(out.end(), {4, e.k}); return;
+      case K::Mod: emit_into(e.args[0], slots, out); out.insert(out.end(), {5, e.k}); return;
+    }
+  }
+  std::vector<StmtRec> recs_;
+  std::vector<nb_nest_stmt> stmts_;
+  nb_nest c_{};
+};
+
+// execute<T> (I/interp.hpp:67-145) of any transformed conv nest on the GPU,
+// with the bindings "I" (Ci,H,W) and "K" (Co_eff,Ci,Kh,Kw) of the reference
+// and the output allocated from provenance.  T = long long (exact) or double.
+template <typename T>
+nestopt::Tensor<T> execute(Context& ctx, const nestopt::LoopNest& nest,
+                           const nestopt::ExecEnv<T>& env) {
+  using namespace nestopt;
+  if (!nest.provenance) throw UnboundTensor("output tensor 'O' is not bound");
+  std::string out_name;
+  for (const auto& part : nest.parts)
+    for (const auto& st : part.stmts)
+      for (const auto& acc : st.accesses)
+        if (acc.mode != AccessMode::Read) {
+          if (!out_name.empty() && out_name != acc.tensor)
+            throw Error("nest writes more than one tensor");
+          out_name = acc.tensor;
+        }
+  if (out_name.empty()) throw Error("nest has no written tensor");
+  const Tensor<T>& ti = env.bindings.at("I");
+  const Tensor<T>& tk = env.bindings.at("K");
+  Tensor<T> out(output_shape(*nest.provenance));
+  NestProgram prog(nest, out_name, out.shape, ti.shape, tk.shape);
+  check(nb_nest_execute(ctx.get(), prog.get(), std::is_integral<T>::value ? 1 : 0,
+                        ti.data.data(), tk.data.data(), out.data.data()));
+  return out;
 }
 
 // ---- the candidate scheduler -------------------------------------------

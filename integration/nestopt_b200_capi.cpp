@@ -75,6 +75,42 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
   }
 }
 
+// execute<T> (I/interp.hpp:67-145) on the GPU of conv_nest(spec) rewritten
+// by a DSL sequence (parse_sequence, I/transforms.hpp:756): any nest,
+// including the ones with no ConvSpec (Sequence 1).  in (Ci,H,W), w
+// (Co_eff,Ci,Kh,Kw), out (Co_eff,out_h,out_w); int64 when is_int else double.
+int nbi_execute(const char* spec_json, const char* dsl, int is_int, const void* in, const void* w,
+                void* out) {
+  try {
+    nestopt::ConvSpec s = nestopt::conv_spec_from_json(nlohmann::json::parse(spec_json));
+    nestopt::LoopNest nest = nestopt::apply(nestopt::conv_nest(s), nestopt::parse_sequence(dsl));
+    nb200::Context ctx(0);
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      nestopt::ExecEnv<T> env;
+      nestopt::Tensor<T> ti({s.ci, s.h, s.w}), tw({s.co_eff(), s.ci, s.kh, s.kw});
+      std::memcpy(ti.data.data(), in, ti.data.size() * 8);
+      std::memcpy(tw.data.data(), w, tw.data.size() * 8);
+      env.bindings["I"] = ti;
+      env.bindings["K"] = tw;
+      nestopt::Tensor<T> to = nb200::execute(ctx, nest, env);
+      std::memcpy(out, to.data.data(), to.data.size() * 8);
+    };
+    if (is_int) run((long long)0);
+    else run(0.0);
+    return 0;
+  } catch (const nb200::DeviceError& e) {
+    g_err = e.what();
+    return NB_ERR_CUDA;
+  } catch (const nestopt::Error& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
 // Host half of a search without a GPU: the reference's draw_candidates and
 // the gates of evaluate_candidate (nb200::host_gates).  Per candidate the
 // output holds its status after the gates ("fisher" = a neural candidate the

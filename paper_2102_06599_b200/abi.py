@@ -74,6 +74,28 @@ vp = C.c_void_p
 dp = P(C.c_double)
 
 # name -> (restype, argtypes); the exported symbol set of include/nb200.h.
+class NestExprC(C.Structure):
+    _fields_ = [("nops", C.c_int32), ("code", C.POINTER(C.c_int64))]
+
+
+class NestAccessC(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("zero_pad", C.c_int32), ("rank", C.c_int32),
+                ("idx", C.POINTER(NestExprC))]
+
+
+class NestStmtC(C.Structure):
+    _fields_ = [("depth", C.c_int32), ("extents", C.POINTER(C.c_int64)),
+                ("ndomain", C.c_int32), ("coord", C.POINTER(NestExprC)),
+                ("naccess", C.c_int32), ("access", C.POINTER(NestAccessC))]
+
+
+class NestC(C.Structure):
+    _fields_ = [("num_stmts", C.c_int64), ("stmts", C.POINTER(NestStmtC)),
+                ("out_shape", C.c_int64 * 4), ("in_shape", C.c_int64 * 4),
+                ("w_shape", C.c_int64 * 4), ("out_rank", C.c_int32), ("in_rank", C.c_int32),
+                ("w_rank", C.c_int32)]
+
+
 SIGNATURES = {
     "nb_version": (C.c_char_p, []),
     "nb_abi_version": (C.c_int, []),
@@ -98,6 +120,7 @@ SIGNATURES = {
     "nb_ctx_launch_count": (C.c_int64, [vp]),
     "nb_conv_forward": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int32, C.c_int]),
     "nb_conv_dgrad": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int]),
+    "nb_nest_execute": (C.c_int, [vp, P(NestC), C.c_int32, vp, vp, vp]),
     "nb_forward": (C.c_int, [vp, P(NetworkC), P(WeightsC), P(BatchC), C.c_int, dp, dp, dp]),
     "nb_activation_gradients": (C.c_int, [vp, P(NetworkC), P(WeightsC), P(BatchC), C.c_int,
                                           dp, dp]),

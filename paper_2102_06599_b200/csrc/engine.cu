@@ -432,6 +432,11 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
                cudaStream_t st) {
   tc::TcLaunch L;
   L.args = args;
+  static const int dbg = [] {
+    const char* e = std::getenv("NB_TC_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  L.args.debug = dbg;
   L.bn = tp.bn;
   L.split3 = split3;
   L.pair = tp.pair;

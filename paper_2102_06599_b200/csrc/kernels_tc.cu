@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
               const __grid_constant__ CUtensorMap mapBl, const TcArgs a) {
   using C = Cfg<BN, SPLIT3, PAIR>;
-  constexpr int S = C::kStages;
+  // ring depth: the configured stage count, or fewer for experiments
+  const int S = (a.debug >> 4) > 0 && (a.debug >> 4) < C::kStages ? (a.debug >> 4) : C::kStages;
   constexpr int NACC = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =
@@ -287,8 +288,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
   auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
   auto b_hi = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
   auto b_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes + C::kBBytes; };
-  float* red = reinterpret_cast<float*>(smem + S * C::kStageBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kRedBytes);
+  float* red = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kRedBytes);
   uint64_t* full = bars;            // S: this CTA's TMA bytes landed
   uint64_t* ready = bars + S;       // S: stage ready for the MMA (split A in TMEM /
                                     //    both CTAs' data landed) -- MMA CTA's copy

@@ -67,6 +67,9 @@ struct TcArgs {
   float* g_out;
   double* partial;
   int relu_prev, part_tiles_per_img, part_ld;
+  // experiments only (NB_TC_DEBUG): bits 4.. = ring depth cap (0 = the
+  // configured stage count)
+  int debug;
 };
 
 struct TcLaunch {

@@ -34,6 +34,9 @@ def load() -> C.CDLL:
         lib.nbi_run_search.restype = C.c_int
         lib.nbi_run_search.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p)]
+        lib.nbi_execute.restype = C.c_int
+        lib.nbi_execute.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]
         lib.nbi_gate_candidates.restype = C.c_int
         lib.nbi_gate_candidates.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         _lib = lib
@@ -72,3 +75,22 @@ def gate_candidates(cfg: dict) -> list:
         return json.loads(C.cast(p, C.c_char_p).value.decode())["candidates"]
     finally:
         lib.nbi_free(p)
+
+
+def execute_gpu(spec, dsl: str, x, w):
+    """execute (I/interp.hpp:67-145) on the GPU of conv_nest(spec) rewritten
+    by the DSL sequence `dsl` -- any rewritten nest, including those with no
+    ConvSpec such as the paper's Sequence 1.  Integer inputs run in int64
+    (exact), floating inputs in fp64.  Returns (Co_eff, out_h, out_w)."""
+    import numpy as np
+    lib = load()
+    is_int = np.asarray(x).dtype.kind in "iu"
+    dt = np.int64 if is_int else np.float64
+    x = np.ascontiguousarray(x, dt)
+    w = np.ascontiguousarray(w, dt)
+    y = np.zeros(spec.output_shape(), dt)
+    rc = lib.nbi_execute(json.dumps(spec.to_json()).encode(), dsl.encode(), int(is_int),
+                         x.ctypes.data, w.ctypes.data, y.ctypes.data)
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    return y
