@@ -174,6 +174,8 @@ nb_status nb_ctx_create(int device, nb_ctx** out);
 nb_status nb_ctx_destroy(nb_ctx* ctx);
 /* The CUDA stream (cudaStream_t) all of the context's kernels run on. */
 void* nb_ctx_stream(nb_ctx* ctx);
+/* enable = 0: off; k >= 1: CUDA events around every launch of every k-th
+ * evaluation (sampling keeps the event overhead out of long runs). */
 nb_status nb_ctx_set_profiling(nb_ctx* ctx, int enable);
 /* Copies up to `cap` stats, returns the number of families in *count. */
 nb_status nb_ctx_kernel_stats(nb_ctx* ctx, nb_kernel_stat* stats, int32_t cap,

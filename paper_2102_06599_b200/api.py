@@ -348,8 +348,10 @@ class Context:
         except Exception:
             pass
 
-    def set_profiling(self, on: bool) -> None:
-        _check(abi.load().nb_ctx_set_profiling(self.ptr, 1 if on else 0))
+    def set_profiling(self, on, every: int = 1) -> None:
+        """Per-launch CUDA events (kernel_stats) on every `every`-th
+        evaluation while `on`."""
+        _check(abi.load().nb_ctx_set_profiling(self.ptr, max(1, int(every)) if on else 0))
 
     def reset_stats(self) -> None:
         _check(abi.load().nb_ctx_reset_stats(self.ptr))

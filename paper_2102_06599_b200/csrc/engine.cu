@@ -67,13 +67,13 @@ cudaEvent_t Profiler::get() {
 }
 
 void Profiler::begin(cudaStream_t st) {
-  if (!on) return;
+  if (!active) return;
   cur_ = get();
   NB_CUDA(cudaEventRecord(cur_, st));
 }
 
 void Profiler::end(cudaStream_t st, const char* fam, double flops, double bytes) {
-  if (!on || !cur_) return;
+  if (!active || !cur_) return;
   cudaEvent_t b = get();
   NB_CUDA(cudaEventRecord(b, st));
   pending_.push_back({cur_, b, fam, flops, bytes});
@@ -544,8 +544,8 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
 
 }  // namespace
 
-void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
-                 bool backward, const RunOut& out) {
+void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
+                 bool backward, const RunOut& out, Pending& pend) {
   nb_ctx* c = s->ctx;
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   ctx_activate(c);
@@ -556,6 +556,7 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     fail(NB_ERR_CONFIG, "network class count does not match the session batch");
   const int64_t N = s->n, L = net.L(), K = net.num_classes;
   cudaStream_t st = c->stream;
+  c->prof.start_eval();
   using clk = std::chrono::steady_clock;
   auto tp = clk::now();
   auto phase = [&](const char* name) {
@@ -715,13 +716,16 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   }
 
   phase("host_launch");
-  // ---- results back to the host
-  std::vector<double> probs(static_cast<size_t>(N * K)), exl(static_cast<size_t>(N)),
-      perch(static_cast<size_t>(P.ch_total));
-  NB_CUDA(cudaMemcpyAsync(probs.data(), d_probs, probs.size() * 8, cudaMemcpyDeviceToHost, st));
-  NB_CUDA(cudaMemcpyAsync(exl.data(), d_exloss, exl.size() * 8, cudaMemcpyDeviceToHost, st));
+  // ---- results back to the host (pinned staging; completed by run_finish)
+  const int64_t stage_doubles = N * K + N + P.ch_total;
+  c->host_out.ensure(size_t(stage_doubles) * 8);
+  double* h_probs = c->host_out.as<double>();
+  double* h_exl = h_probs + N * K;
+  double* h_perch = h_exl + N;
+  NB_CUDA(cudaMemcpyAsync(h_probs, d_probs, size_t(N * K) * 8, cudaMemcpyDeviceToHost, st));
+  NB_CUDA(cudaMemcpyAsync(h_exl, d_exloss, size_t(N) * 8, cudaMemcpyDeviceToHost, st));
   if (backward)
-    NB_CUDA(cudaMemcpyAsync(perch.data(), d_perch, perch.size() * 8, cudaMemcpyDeviceToHost,
+    NB_CUDA(cudaMemcpyAsync(h_perch, d_perch, size_t(P.ch_total) * 8, cudaMemcpyDeviceToHost,
                             st));
   if (out.acts || out.grads) {
     c->io.ensure(size_t(P.dpre_floats) * 8);
@@ -742,29 +746,60 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     }
   }
   NB_CUDA(cudaGetLastError());
-  NB_CUDA(cudaStreamSynchronize(st));
-  phase("host_wait_gpu");
-  c->prof.resolve();
+  pend.s = s;
+  pend.out = out;
+  pend.backward = backward;
+  pend.active = true;
+  pend.N = N;
+  pend.K = K;
+  pend.layer_co.clear();
+  for (int64_t l = 0; l < L; ++l) pend.layer_co.push_back(P.layers[l].geom.Co);
+  pend.ch_total = P.ch_total;
+  pend.h_probs = h_probs;
+  pend.h_exl = h_exl;
+  pend.h_perch = h_perch;
+}
 
+void run_finish(Pending& pend) {
+  if (!pend.active) return;
+  pend.active = false;
+  nb_ctx* c = pend.s->ctx;
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  ctx_activate(c);
+  const auto t0 = std::chrono::steady_clock::now();
+  NB_CUDA(cudaStreamSynchronize(c->stream));
+  c->prof.host("host_wait_gpu",
+               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                   .count());
+  c->prof.resolve();
+  const RunOut& out = pend.out;
+  const int64_t N = pend.N, K = pend.K;
   double lsum = 0.0;
-  for (int64_t i = 0; i < N; ++i) lsum += exl[size_t(i)];
+  for (int64_t i = 0; i < N; ++i) lsum += pend.h_exl[i];
   if (out.loss) *out.loss = lsum / double(N);
-  if (out.probs) std::memcpy(out.probs, probs.data(), probs.size() * 8);
-  if (out.ex_loss) std::memcpy(out.ex_loss, exl.data(), exl.size() * 8);
-  if (backward) {
+  if (out.probs) std::memcpy(out.probs, pend.h_probs, size_t(N * K) * 8);
+  if (out.ex_loss) std::memcpy(out.ex_loss, pend.h_exl, size_t(N) * 8);
+  if (pend.backward) {
     // per_layer / total in the reference's order (I/nnet.hpp:345-349)
     double tot = 0.0;
     int64_t o = 0;
-    for (int64_t l = 0; l < L; ++l) {
+    for (size_t l = 0; l < pend.layer_co.size(); ++l) {
       double layer = 0.0;
-      for (int64_t ch = 0; ch < P.layers[l].geom.Co; ++ch) layer += perch[size_t(o + ch)];
+      for (int64_t ch = 0; ch < pend.layer_co[l]; ++ch) layer += pend.h_perch[o + ch];
       if (out.per_layer) out.per_layer[l] = layer;
-      o += P.layers[l].geom.Co;
+      o += pend.layer_co[l];
       tot += layer;
     }
-    if (out.per_channel) std::memcpy(out.per_channel, perch.data(), perch.size() * 8);
+    if (out.per_channel) std::memcpy(out.per_channel, pend.h_perch, size_t(pend.ch_total) * 8);
     if (out.total) *out.total = tot;
   }
+}
+
+void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
+                 bool backward, const RunOut& out) {
+  Pending p;
+  run_enqueue(s, net, w, prec, backward, out, p);
+  run_finish(p);
 }
 
 // Single-layer entry points (reference_conv / the dgrad step) through the
@@ -785,6 +820,7 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   ctx_activate(ctx);
   cudaStream_t st = ctx->stream;
+  ctx->prof.start_eval();
   NetPlan P = lower(d, n, prec, ctx->num_sms);
   LayerPlan& lp = P.layers.back();
   const int64_t x_cnt = n * s.ci * s.h * s.w, y_cnt = lp.act_floats;
@@ -938,6 +974,8 @@ nb_status nb_ctx_set_profiling(nb_ctx* ctx, int enable) {
     need(ctx, "context");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx->prof.on = enable != 0;
+    ctx->prof.every = enable > 1 ? enable : 1;
+    ctx->prof.calls = 0;
   });
 }
 

@@ -88,6 +88,10 @@ struct KStat {
 class Profiler {
  public:
   bool on = false;
+  int every = 1;        // events on every `every`-th evaluation (sampling)
+  int64_t calls = 0;
+  bool active = false;  // this evaluation records kernel events
+  void start_eval() { active = on && (calls++ % every == 0); }
   void begin(cudaStream_t st);
   void end(cudaStream_t st, const char* family, double flops, double bytes);
   void resolve();  // stream must be synchronized
@@ -121,7 +125,7 @@ struct nb_ctx {
   std::recursive_mutex mu;
   nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws;
   int num_sms = 148;
-  nb::PinnedBuf host_io;
+  nb::PinnedBuf host_io, host_out;
   // device copies of z streams keyed by (seed, stream index)
   std::map<std::pair<uint64_t, int64_t>, std::unique_ptr<nb::DevBuf>> zdev;
   std::map<std::pair<uint64_t, int64_t>, int64_t> zlen;
@@ -159,8 +163,23 @@ struct RunOut {
   double* grads = nullptr;
 };
 
+// An evaluation enqueued on its session's stream, not yet collected.
+struct Pending {
+  nb_session* s = nullptr;
+  RunOut out;
+  bool backward = false, active = false;
+  int64_t N = 0, K = 0, ch_total = 0;
+  std::vector<int> layer_co;
+  double *h_probs = nullptr, *h_exl = nullptr, *h_perch = nullptr;  // pinned staging
+};
+
 // Runs forward (and, when `backward`, activation gradients + Fisher) of `net`
-// on the session's resident batch.
+// on the session's resident batch: run_enqueue issues every kernel and the
+// result copies asynchronously on the session's stream, run_finish waits for
+// them and fills `out`.  One evaluation per session may be in flight.
+void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
+                 bool backward, const RunOut& out, Pending& pend);
+void run_finish(Pending& pend);
 void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
                  bool backward, const RunOut& out);
 

@@ -4,9 +4,10 @@
 // de-duplicated (identical networks score bit-identically, so one run
 // answers all copies -- this is what makes the reference's exact ties,
 // I/nnet.hpp:358, reproducible), then assigned to GPUs longest-processing-
-// time-first on their estimated FLOPs, and one host worker per GPU session
-// evaluates its queue.  Results land in fixed slots, so the output does not
-// depend on the number of GPUs.
+// time-first on their estimated FLOPs, and one host worker per GPU keeps
+// one evaluation in flight on each of that GPU's sessions (streams).
+// Results land in fixed slots, so the output does not depend on the number
+// of GPUs or sessions.
 #include <algorithm>
 #include <chrono>
 #include <exception>
@@ -69,51 +70,79 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
       nb_status st = nb_schedule_lpt(cost.data(), int64_t(uniq.size()), num_sessions, bin.data());
       if (st != NB_OK) fail(st, nb_last_error());
     }
-    std::vector<std::vector<size_t>> queue(static_cast<size_t>(num_sessions));
     // within a worker, largest first (the LPT order)
     std::vector<size_t> order(uniq.size());
     for (size_t u = 0; u < order.size(); ++u) order[u] = u;
     std::stable_sort(order.begin(), order.end(),
                      [&](size_t a, size_t b) { return cost[a] > cost[b]; });
-    for (size_t u : order) queue[size_t(bin[u])].push_back(u);
 
+    // One host worker per GPU drives all of that GPU's sessions round-robin:
+    // it enqueues an evaluation on each session's stream and collects the
+    // oldest only when its session comes round again, so up to
+    // (sessions per GPU) evaluations are in flight without several host
+    // threads contending for the same device.
     std::vector<Result> res(uniq.size());
+    for (size_t u = 0; u < uniq.size(); ++u) {
+      const NetDesc& d = descs[uniq[u]];
+      int64_t ch = 0;
+      for (const auto& sp : d.specs) ch += sp.co_eff();
+      res[u].per_channel.resize(size_t(ch));
+      res[u].per_layer.resize(size_t(d.L()));
+      res[u].probs.resize(size_t(N * d.num_classes));
+    }
+    std::vector<int> devs;
+    for (int32_t k = 0; k < num_sessions; ++k)
+      if (std::find(devs.begin(), devs.end(), sessions[k]->ctx->device) == devs.end())
+        devs.push_back(sessions[k]->ctx->device);
     std::vector<double> busy(size_t(num_sessions), 0.0), est(size_t(num_sessions), 0.0);
     std::exception_ptr err;
     std::mutex err_mu;
-    auto worker = [&](int32_t k) {
+    auto worker = [&](int dev) {
       auto t0 = std::chrono::steady_clock::now();
+      std::vector<int32_t> mine;  // this GPU's sessions
+      for (int32_t k = 0; k < num_sessions; ++k)
+        if (sessions[k]->ctx->device == dev) mine.push_back(k);
+      // this GPU's networks, largest first, interleaved from its sessions' LPT bins
+      std::vector<std::pair<size_t, int32_t>> work;
+      for (size_t u : order)
+        if (std::find(mine.begin(), mine.end(), bin[u]) != mine.end())
+          work.emplace_back(u, bin[u]);
+      std::vector<Pending> pend(mine.size());
       try {
-        for (size_t u : queue[size_t(k)]) {
-          const NetDesc& d = descs[uniq[u]];
+        for (size_t i = 0; i < work.size(); ++i) {
+          const size_t slot = i % mine.size();
+          run_finish(pend[slot]);
+          const size_t u = work[i].first;
           Result& r = res[u];
-          int64_t ch = 0;
-          for (const auto& s : d.specs) ch += s.co_eff();
-          r.per_channel.resize(size_t(ch));
-          r.per_layer.resize(size_t(d.L()));
-          r.probs.resize(size_t(N * d.num_classes));
           RunOut ro;
           ro.per_channel = r.per_channel.data();
           ro.per_layer = r.per_layer.data();
           ro.total = &r.total;
           ro.loss = &r.loss;
           ro.probs = r.probs.data();
-          run_network(sessions[k], d, nullptr, prec, true, ro);
-          est[size_t(k)] += cost[u];
+          run_enqueue(sessions[mine[slot]], descs[uniq[u]], nullptr, prec, true, ro, pend[slot]);
+          est[size_t(mine[slot])] += cost[u];
         }
+        for (auto& p : pend) run_finish(p);
       } catch (...) {
         std::lock_guard<std::mutex> lk(err_mu);
         if (!err) err = std::current_exception();
+        for (auto& p : pend) {
+          try {
+            run_finish(p);
+          } catch (...) {
+          }
+        }
       }
-      busy[size_t(k)] =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
-              .count();
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      for (int32_t k : mine) busy[size_t(k)] = ms;
     };
-    if (num_sessions == 1) {
-      worker(0);
+    if (devs.size() == 1) {
+      worker(devs[0]);
     } else {
       std::vector<std::thread> pool;
-      for (int32_t k = 0; k < num_sessions; ++k) pool.emplace_back(worker, k);
+      for (int d : devs) pool.emplace_back(worker, d);
       for (auto& t : pool) t.join();
     }
     if (err) std::rethrow_exception(err);
