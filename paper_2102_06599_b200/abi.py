@@ -11,6 +11,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libnb200.so")
+# A/B experiments only: load another in-tree build of the same ABI
+if os.environ.get("NB200_LIB"):
+    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ["NB200_LIB"])
 
 # nb_status (include/nb200.h) -- values map 1:1 onto nestopt exception classes.
 NB_OK = 0
