@@ -654,7 +654,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
 
   phase("host_weights");
   // ---- forward (I/nnet.hpp:180-197)
-  const float* x = s->x.as<float>();
+  const float* x = s->x->as<float>();
   for (int64_t l = 0; l < L; ++l) {
     float* y = act + P.layers[l].act_off;
     fprop_layer(c, P, P.layers[l], x, y, net.relu[l], st);
@@ -671,7 +671,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   ha.K = int(K);
   ha.head_src = head_src;
   ha.head_scale = head_scale;
-  ha.labels = s->labels.as<int32_t>();
+  ha.labels = s->labels->as<int32_t>();
   ha.probs = d_probs;
   ha.ex_loss = d_exloss;
   ha.backward = backward;
@@ -893,15 +893,31 @@ nb_session* make_session(nb_ctx* c, const NetDesc& net, const nb_batch* b) {
   s->seed = b->seed;
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   ctx_activate(c);
-  s->x.ensure(size_t(b->n * per) * 4);
-  s->labels.ensure(size_t(b->n) * 4);
+  auto take = [&](size_t bytes) {
+    // the smallest spare buffer that fits, else a new one
+    auto best = c->spare.end();
+    for (auto it = c->spare.begin(); it != c->spare.end(); ++it)
+      if ((*it)->bytes >= bytes && (best == c->spare.end() || (*it)->bytes < (*best)->bytes))
+        best = it;
+    std::unique_ptr<DevBuf> buf;
+    if (best != c->spare.end()) {
+      buf = std::move(*best);
+      c->spare.erase(best);
+    } else {
+      buf = std::make_unique<DevBuf>();
+      buf->ensure(bytes);
+    }
+    return buf;
+  };
+  s->x = take(size_t(b->n * per) * 4);
+  s->labels = take(size_t(b->n) * 4);
   c->io.ensure(size_t(b->n * per) * 8);
   NB_CUDA(cudaMemcpyAsync(c->io.p, xp, size_t(b->n * per) * 8, cudaMemcpyHostToDevice,
                           c->stream));
-  launch_nchw64_to_nhwc32(c->io.as<double>(), s->x.as<float>(), b->n, int(s0.ci), int(s0.h),
+  launch_nchw64_to_nhwc32(c->io.as<double>(), s->x->as<float>(), b->n, int(s0.ci), int(s0.h),
                           int(s0.w), c->stream);
   c->launches++;
-  NB_CUDA(cudaMemcpyAsync(s->labels.p, lp, size_t(b->n) * 4, cudaMemcpyHostToDevice,
+  NB_CUDA(cudaMemcpyAsync(s->labels->p, lp, size_t(b->n) * 4, cudaMemcpyHostToDevice,
                           c->stream));
   NB_CUDA(cudaStreamSynchronize(c->stream));
   return s.release();
@@ -1041,6 +1057,11 @@ nb_status nb_session_destroy(nb_session* s) {
     if (!s) return;
     std::lock_guard<std::recursive_mutex> lk(s->ctx->mu);
     ctx_activate(s->ctx);
+    // keep the batch buffers for the context's next session (bounded)
+    if (s->ctx->spare.size() < 8) {
+      s->ctx->spare.push_back(std::move(s->x));
+      s->ctx->spare.push_back(std::move(s->labels));
+    }
     delete s;
   });
 }

@@ -138,6 +138,9 @@ struct nb_ctx {
   size_t wcache_bytes = 0;
   nb::Profiler prof;
   int64_t launches = 0;
+  // batch buffers of destroyed sessions, reused by the next ones (no
+  // cudaMalloc / cudaFree per session)
+  std::vector<std::unique_ptr<nb::DevBuf>> spare;
 };
 
 struct nb_session {
@@ -145,8 +148,8 @@ struct nb_session {
   int64_t n = 0;
   int64_t ci = 0, h = 0, w = 0, num_classes = 0;
   uint64_t seed = 0;
-  nb::DevBuf x;       // (N, H, W, Ci) fp32
-  nb::DevBuf labels;  // N int32
+  std::unique_ptr<nb::DevBuf> x;       // (N, H, W, Ci) fp32
+  std::unique_ptr<nb::DevBuf> labels;  // N int32
 };
 
 namespace nb {
