@@ -112,24 +112,46 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref: the unmodified nestopt compiled in place)
 
-def reference_sample(layers: int, threads: int):
+def timed_pool(args, world):
+    """The candidate networks the nb200 arm times (both arms use the same
+    selection): the reference's R34 per-layer pool in a fixed shuffled order,
+    the first W for warm-up, the next K x world timed."""
+    import numpy as np
+    from paper_2102_06599_b200.workloads import fixture_path, load_candidates, resnet34_chain
+
+    origin = resnet34_chain()
+    pool = load_candidates(fixture_path("r34_candidates.json"), origin)
+    order = np.random.default_rng(0).permutation(len(pool))
+    pool = [pool[i] for i in order]
+    warm = pool[:max(1, args.warmup)]
+    timed = pool[len(warm):]
+    need = args.steps * world
+    if need > len(timed):
+        raise SystemExit(f"--steps x gpus = {need} exceeds the {len(timed)} distinct candidates")
+    return origin, warm, timed[:need]
+
+
+def fisher_macs(net, n):
+    """MACs of one fisher_potential: forward of every layer + dgrad of layers
+    >= 1 (I/nnet.hpp:225), per example, times n."""
+    from paper_2102_06599_b200.api import count_macs
+    m = [count_macs(l.spec) for l in net.layers]
+    return n * (sum(m) + sum(m[1:]))
+
+
+def reference_sample(layers: int, threads: int, target_macs: float):
     """Times the reference's fisher_potential on a bounded slice of the R34
     chain (its first `layers` convs, one image) on `threads` host threads at
     once (one evaluation per thread, like evaluate_all's jobs), and scales it
-    to candidates/s of the full chain at N=128 by the Fisher-MAC ratio (the
+    to candidates/s of candidates costing `target_macs` Fisher MACs (the
     reference's cost is linear in MACs and examples, I/nnet.hpp:184,206)."""
     from oracle.oracle import Reference
-    from paper_2102_06599_b200.api import Network, count_macs
+    from paper_2102_06599_b200.api import Network
     from paper_2102_06599_b200.workloads import resnet34_chain
 
     full = resnet34_chain()
     sl = Network(full.layers[:layers], num_classes=10, seed=42)
     R = Reference()
-
-    def fisher_macs(net, n):
-        m = [count_macs(l.spec) for l in net.layers]
-        return n * (sum(m) + sum(m[1:]))
-
     errs = []
 
     def one():
@@ -147,12 +169,12 @@ def reference_sample(layers: int, threads: int):
     dt = time.perf_counter() - t0
     if errs:
         raise errs[0]
-    scale = fisher_macs(full, N_BATCH) / fisher_macs(sl, 1)
+    scale = target_macs / fisher_macs(sl, 1)
     cand_per_s = threads / (dt * scale)
     return cand_per_s, dt, (f"reference fisher_potential (oracle/_ref) on R34 layers 0-{layers - 1}"
                             f" at N=1, {threads} concurrent on {threads} host threads, "
-                            f"{dt:.2f} s wall, scaled x{scale:.0f} by Fisher MACs to the origin "
-                            f"chain at N={N_BATCH} (extrapolated)")
+                            f"{dt:.2f} s wall, scaled x{scale:.0f} by Fisher MACs to the mean "
+                            f"candidate of the timed pool at N={N_BATCH} (extrapolated)")
 
 
 def run_reference(args):
@@ -160,13 +182,15 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    _, _, timed = timed_pool(args, int(os.environ.get("WORLD_SIZE", "1")))
+    target = sum(fisher_macs(n, N_BATCH) for n in timed) / len(timed)
     # each step is a ~6-10 s sample; keep the whole arm within a few minutes
     warm, steps = min(args.warmup, 1), min(args.steps, 8)
     for _ in range(warm):
-        reference_sample(args.cpu_sample_layers, threads)
+        reference_sample(args.cpu_sample_layers, threads, target)
     vals, walls, sample = [], [], ""
     for _ in range(steps):
-        v, dt, sample = reference_sample(args.cpu_sample_layers, threads)
+        v, dt, sample = reference_sample(args.cpu_sample_layers, threads, target)
         vals.append(v)
         walls.append(dt)
     v = statistics.mean(vals)
@@ -196,8 +220,7 @@ def main():
 
     import paper_2102_06599_b200 as nb
     from paper_2102_06599_b200 import Precision
-    from paper_2102_06599_b200.workloads import (fixture_path, load_candidates, resnet34_chain,
-                                                 shard_lpt)
+    from paper_2102_06599_b200.workloads import shard_lpt
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -207,18 +230,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prec = {"fp32": Precision.FP32, "tf32": Precision.TF32, "simt": Precision.SIMT}[args.precision]
 
-    origin = resnet34_chain()
-    pool = load_candidates(fixture_path("r34_candidates.json"), origin)
-    order = np.random.default_rng(0).permutation(len(pool))
-    pool = [pool[i] for i in order]
     # warm-up networks and the timed pool are disjoint; the timed pool is
     # K per rank, LPT-sharded over the ranks by estimated FLOPs
-    warm_pool = pool[:max(1, args.warmup)]
-    timed = pool[len(warm_pool):]
-    need = args.steps * world
-    if need > len(timed):
-        raise SystemExit(f"--steps x gpus = {need} exceeds the {len(timed)} distinct candidates")
-    timed = timed[:need]
+    origin, warm_pool, timed = timed_pool(args, world)
     costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
     assign = shard_lpt(costs, world, args.steps)
     mine = [n for n, a in zip(timed, assign) if a == rank]
@@ -360,7 +374,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, dt, sample = reference_sample(args.cpu_sample_layers, threads)
+        target = sum(fisher_macs(n, N_BATCH) for n in timed) / len(timed)
+        v, dt, sample = reference_sample(args.cpu_sample_layers, threads, target)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                "sample": sample}
 
