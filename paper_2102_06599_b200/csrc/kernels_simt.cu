@@ -148,6 +148,204 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
     if (t < nco) yo[t] = (relu && !(acc[t] > 0.f)) ? 0.f : acc[t];  // I/nnet.hpp:138-139
 }
 
+// Grouped / depthwise fprop with a shared-memory halo tile (ranges whose
+// groups are too narrow for the tensor cores).  A block owns a tile of
+// kGTH x kGTW output pixels of one image and CC output channels (whole
+// groups); it stages the input halo rows x cols x (the groups' input
+// channels) with coalesced float4 loads, and every thread keeps one output
+// channel's weights in registers and accumulates its pixels from smem.
+constexpr int kGPix = 256, kGThreads = 256;
+
+// Output tile of the grouped kernel: up to 32 columns, rows filling 256 pixels.
+struct GTile {
+  int tw, th;
+};
+inline __host__ __device__ GTile gtile(int OH, int OW) {
+  GTile t;
+  t.tw = OW < 32 ? OW : 32;
+  t.th = kGPix / t.tw;
+  if (t.th > OH) t.th = OH;
+  return t;
+}
+
+template <int CC, int KMAX>
+__global__ void __launch_bounds__(kGThreads, KMAX <= 9 ? 4 : KMAX <= 36 ? 2 : 1)
+    k_fprop_grouped(ConvGeom g, int ri,
+                                                             const float* __restrict__ x,
+                                                             const float* __restrict__ wbase,
+                                                             float* __restrict__ y, bool relu) {
+  extern __shared__ float halo[];  // [IH][IW][CIc]
+  const RangeDesc r = g.r[ri];
+  const float* __restrict__ wf = wbase + r.wf_off;
+  const GTile T = gtile(g.OH, g.OW);
+  const int tiles_w = (g.OW + T.tw - 1) / T.tw;
+  const int oh0 = (blockIdx.x / tiles_w) * T.th, ow0 = (blockIdx.x % tiles_w) * T.tw;
+  const int64_t n = blockIdx.y;
+  const int c0 = blockIdx.z * CC;                     // first output channel (range-local)
+  const int nco = min(CC, r.len - c0);
+  const int gsb = c0 / r.slice_co;                    // first group of the chunk
+  const int ci0 = gsb * r.slice_ci;                   // its first input channel
+  const int gse = (c0 + nco - 1) / r.slice_co;        // last group
+  const int cic = (gse - gsb + 1) * r.slice_ci;       // input channels staged
+  const int IH = (T.th - 1) * g.S + g.KH, IW = (T.tw - 1) * g.S + g.KW;
+  const int ih0 = oh0 * g.S - g.P, iw0 = ow0 * g.S - g.P;
+  // ---- stage the halo (zero outside the image: padded taps add nothing)
+  const bool vec = (cic % 4 == 0) && (ci0 % 4 == 0) && (g.Ci % 4 == 0);
+  if (vec) {
+    const int q4 = cic / 4;
+    for (int e = threadIdx.x; e < IH * IW * q4; e += kGThreads) {
+      const int q = e % q4, pc = e / q4, iw = pc % IW, ih = pc / IW;
+      const int gh = ih0 + ih, gw = iw0 + iw;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W)
+        v = __ldg(reinterpret_cast<const float4*>(x + ((n * g.H + gh) * g.W + gw) * g.Ci + ci0) + q);
+      reinterpret_cast<float4*>(halo)[(ih * IW + iw) * q4 + q] = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < IH * IW * cic; e += kGThreads) {
+      const int q = e % cic, pc = e / cic, iw = pc % IW, ih = pc / IW;
+      const int gh = ih0 + ih, gw = iw0 + iw;
+      halo[e] = (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W)
+                    ? __ldg(x + ((n * g.H + gh) * g.W + gw) * g.Ci + ci0 + q)
+                    : 0.f;
+    }
+  }
+  __syncthreads();
+  const int col = threadIdx.x % CC, lane_p = threadIdx.x / CC;
+  constexpr int PL = kGThreads / CC;  // pixel lanes
+  if (col >= nco) return;
+  const int co = c0 + col;                       // range-local output channel
+  const int cil = (co / r.slice_co - gsb) * r.slice_ci;  // its group's first staged input
+  const int K = r.slice_ci * g.KH * g.KW;
+  // per K element: its weight and its smem offset relative to the pixel
+  float wr[KMAX];
+  int off[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int kc = k < K ? k : K - 1;
+    const int tap = kc / r.slice_ci, j = kc - tap * r.slice_ci;
+    const int kh = tap / g.KW, kw = tap - kh * g.KW;
+    wr[k] = k < K ? __ldg(wf + int64_t(k) * r.len + co) : 0.f;  // Wf[tap][j][co]
+    off[k] = (kh * IW + kw) * cic + cil + j;
+  }
+  for (int p = lane_p; p < T.th * T.tw; p += PL) {
+    const int th = p / T.tw, tw = p % T.tw;
+    const int oh = oh0 + th, ow = ow0 + tw;
+    if (oh >= g.OH || ow >= g.OW) continue;
+    const float* hp = halo + (th * g.S * IW + tw * g.S) * cic;
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) acc = fmaf(hp[off[k]], wr[k], acc);
+    y[((n * g.OH + oh) * g.OW + ow) * g.Co + r.b + co] = (relu && !(acc > 0.f)) ? 0.f : acc;
+  }
+}
+
+// 3x3 stride-1 grouped / depthwise fprop (groups of SLICE input channels):
+// the halo is staged channel-major ([channel][row][col], plane stride = 1
+// mod 32 so the 32 channels of a warp hit 32 banks), each thread owns one
+// output channel with its 9*SLICE weights in registers and produces 4
+// adjacent output pixels of a row per step: 6 shared loads per (input
+// channel, tap row) feed 12 FMAs, with constant-offset addressing.
+template <int SLICE>
+__global__ void __launch_bounds__(kGThreads, SLICE <= 2 ? 4 : 2)
+    k_fprop_grouped3(ConvGeom g, int ri, const float* __restrict__ x,
+                     const float* __restrict__ wbase, float* __restrict__ y, bool relu) {
+  extern __shared__ float halo[];  // [cic][IH][IW] with plane stride PS
+  const RangeDesc r = g.r[ri];
+  const float* __restrict__ wf = wbase + r.wf_off;
+  const GTile T = gtile(g.OH, g.OW);
+  const int tiles_w = (g.OW + T.tw - 1) / T.tw;
+  const int oh0 = (blockIdx.x / tiles_w) * T.th, ow0 = (blockIdx.x % tiles_w) * T.tw;
+  const int64_t n = blockIdx.y;
+  const int c0 = blockIdx.z * 32;
+  const int nco = min(32, r.len - c0);
+  const int gsb = c0 / r.slice_co, gse = (c0 + nco - 1) / r.slice_co;
+  const int ci0 = gsb * SLICE, cic = (gse - gsb + 1) * SLICE;
+  const int IH = T.th + 2, IW = T.tw + 2 + 3;  // +3: the last quad may read past the tile
+  const int PS = ((IH * IW + 31) / 32) * 32 + 1;
+  const int ih0 = oh0 - g.P, iw0 = ow0 - g.P;
+  if ((cic & 3) == 0 && (ci0 & 3) == 0 && (g.Ci & 3) == 0) {
+    const int q4 = cic / 4;
+    for (int e = threadIdx.x; e < IH * IW * q4; e += kGThreads) {
+      const int q = e % q4, pc = e / q4, iw = pc % IW, ih = pc / IW;
+      const int gh = ih0 + ih, gw = iw0 + iw;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W && iw < T.tw + 2)
+        v = __ldg(reinterpret_cast<const float4*>(x + ((n * g.H + gh) * g.W + gw) * g.Ci + ci0) + q);
+      float* d = halo + 4 * q * PS + pc;
+      d[0] = v.x;
+      d[PS] = v.y;
+      d[2 * PS] = v.z;
+      d[3 * PS] = v.w;
+    }
+  } else {
+    for (int e = threadIdx.x; e < IH * IW * cic; e += kGThreads) {
+      const int q = e % cic, pc = e / cic, iw = pc % IW, ih = pc / IW;
+      const int gh = ih0 + ih, gw = iw0 + iw;
+      halo[q * PS + pc] = (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W && iw < T.tw + 2)
+                              ? __ldg(x + ((n * g.H + gh) * g.W + gw) * g.Ci + ci0 + q)
+                              : 0.f;
+    }
+  }
+  __syncthreads();
+  // weights: registers for narrow groups, else a [tap*SLICE + j][32] smem
+  // block after the halo (column = the thread's output channel)
+  constexpr bool kRegW = SLICE <= 4;
+  float* wsm = halo + cic * PS;
+  if (!kRegW) {
+    for (int e = threadIdx.x; e < 9 * SLICE * 32; e += kGThreads) {
+      const int cc = e & 31, k = e >> 5;
+      wsm[e] = cc < nco ? __ldg(wf + int64_t(k) * r.len + c0 + cc) : 0.f;
+    }
+    __syncthreads();
+  }
+  const int col = threadIdx.x & 31, lane_p = threadIdx.x >> 5;
+  constexpr int PL = kGThreads / 32;
+  if (col >= nco) return;
+  const int co = c0 + col;
+  const int cil = (co / r.slice_co - gsb) * SLICE;
+  float w3[kRegW ? SLICE : 1][9];
+  if (kRegW) {
+#pragma unroll
+    for (int j = 0; j < (kRegW ? SLICE : 1); ++j)
+#pragma unroll
+      for (int t = 0; t < 9; ++t) w3[j][t] = __ldg(wf + int64_t(t * SLICE + j) * r.len + co);
+  }
+  auto wt = [&](int j, int t) {
+    if constexpr (kRegW) return w3[j][t];
+    else return wsm[(t * SLICE + j) * 32 + col];
+  };
+  const int quads_w = (T.tw + 3) / 4;
+  float* yb = y + r.b + co;
+  for (int qd = lane_p; qd < T.th * quads_w; qd += PL) {
+    const int th = qd / quads_w, tw = (qd - th * quads_w) * 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll(kRegW ? SLICE : 1)
+    for (int j = 0; j < SLICE; ++j) {
+      const float* hp = halo + (cil + j) * PS + th * IW + tw;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        float v[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) v[i] = hp[kh * IW + i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) acc[q] = fmaf(v[q + kw], wt(j, kh * 3 + kw), acc[q]);
+      }
+    }
+    const int oh = oh0 + th;
+    if (oh >= g.OH) continue;
+    const int64_t rowb = (n * g.OH + oh) * int64_t(g.OW);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ow = ow0 + tw + q;
+      if (tw + q < T.tw && ow < g.OW)
+        yb[(rowb + ow) * g.Co] = (relu && !(acc[q] > 0.f)) ? 0.f : acc[q];
+    }
+  }
+}
+
 // Depthwise fprop (slice_ci = slice_co = 1): threads run over channels
 // (coalesced NHWC loads and stores), each computing kDwRun consecutive
 // output pixels of one row with its channel's taps held in registers.
@@ -412,9 +610,71 @@ void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int
   k_pack_weights<<<grid_for(total, 256), 256, 0, st>>>(src, scale, g.Ci, taps, r, d);
 }
 
+// shared memory of k_fprop_grouped3 for a 32-channel output chunk
+size_t grouped3_smem(const ConvGeom& g, const RangeDesc& r) {
+  const GTile T = gtile(g.OH, g.OW);
+  const int cic = ((32 + r.slice_co - 1) / r.slice_co + 1) * r.slice_ci;
+  const int IH3 = T.th + 2, IW3 = T.tw + 5;
+  return (size_t(cic) * (((IH3 * IW3 + 31) / 32) * 32 + 1) + 9 * size_t(r.slice_ci) * 32) * 4;
+}
+
+bool grouped3_ok(const ConvGeom& g, const RangeDesc& r) {
+  return r.groups >= 2 && g.KH == 3 && g.KW == 3 && g.S == 1 &&
+         (r.slice_ci == 1 || r.slice_ci == 2 || r.slice_ci == 4 || r.slice_ci == 8 ||
+          r.slice_ci == 16) &&
+         grouped3_smem(g, r) <= 200 * 1024;
+}
+
+bool grouped_smem_ok(const ConvGeom& g, const RangeDesc& r) {
+  if (grouped3_ok(g, r)) return true;
+  if (r.groups < 2 || g.S > 2) return false;
+  const int K = r.slice_ci * g.KH * g.KW;
+  if (K > 64) return false;
+  // the staged input channels of a 32-channel output chunk
+  const int groups_per_chunk = (32 + r.slice_co - 1) / r.slice_co + 1;
+  const int cic = groups_per_chunk * r.slice_ci;
+  const GTile T = gtile(g.OH, g.OW);
+  const int IH = (T.th - 1) * g.S + g.KH, IW = (T.tw - 1) * g.S + g.KW;
+  return size_t(IH) * IW * cic * 4 <= 96 * 1024;
+}
+
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
                          float* y, bool relu, cudaStream_t st) {
   const RangeDesc& r = g.r[range];
+  if (grouped_smem_ok(g, r)) {
+    const GTile T = gtile(g.OH, g.OW);
+    const int tiles = ((g.OH + T.th - 1) / T.th) * ((g.OW + T.tw - 1) / T.tw);
+    const int chunks = (r.len + 31) / 32;
+    // worst-case staged channels of a chunk (see grouped_smem_ok)
+    const int cic = ((32 + r.slice_co - 1) / r.slice_co + 1) * r.slice_ci;
+    const int IH = (T.th - 1) * g.S + g.KH, IW = (T.tw - 1) * g.S + g.KW;
+    const size_t smem = size_t(IH) * IW * cic * 4;
+    const int K = r.slice_ci * g.KH * g.KW;
+    dim3 grid(tiles, g.N, chunks);
+    auto go = [&](auto kern, size_t bytes) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+      kern<<<grid, kGThreads, bytes, st>>>(g, range, x, wbase, y, relu);
+    };
+    if (grouped3_ok(g, r)) {
+      const size_t smem3 = grouped3_smem(g, r);
+      switch (r.slice_ci) {
+        case 1: go(k_fprop_grouped3<1>, smem3); break;
+        case 2: go(k_fprop_grouped3<2>, smem3); break;
+        case 4: go(k_fprop_grouped3<4>, smem3); break;
+        case 8: go(k_fprop_grouped3<8>, smem3); break;
+        default: go(k_fprop_grouped3<16>, smem3); break;
+      }
+    } else if (K <= 9) {
+      go(k_fprop_grouped<32, 9>, smem);
+    } else if (K <= 18) {
+      go(k_fprop_grouped<32, 18>, smem);
+    } else if (K <= 36) {
+      go(k_fprop_grouped<32, 36>, smem);
+    } else {
+      go(k_fprop_grouped<32, 64>, smem);
+    }
+    return;
+  }
   if (r.slice_ci == 1 && r.slice_co == 1) {
     const int64_t units = int64_t(g.N) * g.OH * ((g.OW + kDwRun - 1) / kDwRun);
     dim3 grid((r.len + 31) / 32, unsigned((units + 7) / 8));
