@@ -356,7 +356,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
     } else {
       const LayerPlan& nx = P.layers[l + 1];
       lp.tiles = nx.dgrad_family == Family::TensorCore ? nx.tcd.tile.part_tiles_per_img
-                                                       : dgrad_tiles(lp.geom.OH, lp.geom.OW);
+                                                       : direct_dgrad_tiles(nx.geom);
     }
     lp.part_off = P.part_total;
     P.part_total += align64(n * lp.tiles * lp.geom.Co);

@@ -64,6 +64,8 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
 // g_in = convT(W, dpre) over all ranges; fused epilogue on the previous
 // layer's activation a_prev (nullable): partial[n][tile][ci] = sum A*g,
 // dpre_out = g * [a_prev > 0] (or g when !relu_prev), g_out = g (nullable).
+// Partial tiles per image of the direct dgrad launch_dgrad_direct picks for g.
+int direct_dgrad_tiles(const ConvGeom& g);
 void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
                          const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                          double* partial, cudaStream_t st);

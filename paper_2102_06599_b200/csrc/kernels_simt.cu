@@ -346,6 +346,132 @@ __global__ void __launch_bounds__(kGThreads, SLICE <= 2 ? 4 : 2)
   }
 }
 
+// 3x3 stride-1 dgrad of a single-range grouped / depthwise layer (groups of
+// SLICE = slice_co output channels), same structure as k_fprop_grouped3:
+// g[ih,iw,ci] = sum_t sum_{kh,kw} Wd[kh,kw][t][ci] * dpre[ih+P-kh, iw+P-kw,
+// co(t)] over the dpre halo (rows / cols past the cropped output are zero),
+// with the fused epilogue of k_dgrad_direct: g_out, the ReLU-masked dpre of
+// the previous layer and per-(image, tile, channel) partials of A*g summed in
+// a fixed order (tile = the gtile() grid over H x W).
+template <int SLICE>
+__global__ void __launch_bounds__(kGThreads, SLICE <= 2 ? 4 : 2)
+    k_dgrad_grouped3(ConvGeom g, const float* __restrict__ dpre, const float* __restrict__ wbase,
+                     const float* __restrict__ a_prev, bool relu_prev, float* __restrict__ dpre_out,
+                     float* __restrict__ g_out, double* __restrict__ partial) {
+  extern __shared__ float halo[];  // [cst][IH][IW] plane stride PS, then weights
+  __shared__ float red[kGThreads / 32][33];
+  const RangeDesc r = g.r[0];
+  const float* __restrict__ wd = wbase + r.wd_off;
+  const GTile T = gtile(g.H, g.W);
+  const int tiles_w = (g.W + T.tw - 1) / T.tw;
+  const int tile = blockIdx.x;
+  const int ih0t = (tile / tiles_w) * T.th, iw0t = (tile % tiles_w) * T.tw;
+  const int64_t n = blockIdx.y;
+  const int c0 = blockIdx.z * 32;              // first dgrad-output (input) channel
+  const int nci = min(32, g.Ci - c0);
+  const int gsb = c0 / r.slice_ci, gse = (c0 + nci - 1) / r.slice_ci;
+  const int co0 = r.b + gsb * SLICE, cst = (gse - gsb + 1) * SLICE;  // staged dpre channels
+  const int IH = T.th + 2, IW = T.tw + 2 + 3;
+  const int PS = ((IH * IW + 31) / 32) * 32 + 1;
+  const int oh0 = ih0t + g.P - 2, ow0 = iw0t + g.P - 2;  // first dpre row / col needed
+  if ((cst & 3) == 0 && (co0 & 3) == 0 && (g.Co & 3) == 0) {
+    const int q4 = cst / 4;
+    for (int e = threadIdx.x; e < IH * IW * q4; e += kGThreads) {
+      const int q = e % q4, pc = e / q4, iw = pc % IW, ih = pc / IW;
+      const int gh = oh0 + ih, gw = ow0 + iw;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gh >= 0 && gh < g.OH && gw >= 0 && gw < g.OW && iw < T.tw + 2)
+        v = __ldg(reinterpret_cast<const float4*>(dpre + ((n * g.OH + gh) * g.OW + gw) * g.Co + co0) + q);
+      float* d = halo + 4 * q * PS + pc;
+      d[0] = v.x;
+      d[PS] = v.y;
+      d[2 * PS] = v.z;
+      d[3 * PS] = v.w;
+    }
+  } else {
+    for (int e = threadIdx.x; e < IH * IW * cst; e += kGThreads) {
+      const int q = e % cst, pc = e / cst, iw = pc % IW, ih = pc / IW;
+      const int gh = oh0 + ih, gw = ow0 + iw;
+      halo[q * PS + pc] = (gh >= 0 && gh < g.OH && gw >= 0 && gw < g.OW && iw < T.tw + 2)
+                              ? __ldg(dpre + ((n * g.OH + gh) * g.OW + gw) * g.Co + co0 + q)
+                              : 0.f;
+    }
+  }
+  constexpr bool kRegW = SLICE <= 4;
+  float* wsm = halo + cst * PS;
+  if (!kRegW) {
+    for (int e = threadIdx.x; e < 9 * SLICE * 32; e += kGThreads) {
+      const int cc = e & 31, k = e >> 5;  // k = tap * SLICE + t
+      wsm[e] = cc < nci ? __ldg(wd + int64_t(k) * g.Ci + c0 + cc) : 0.f;
+    }
+  }
+  __syncthreads();
+  const int col = threadIdx.x & 31, lane_p = threadIdx.x >> 5;
+  constexpr int PL = kGThreads / 32;
+  const bool act = col < nci;
+  const int ci = c0 + col;
+  const int tl = act ? (ci / r.slice_ci - gsb) * SLICE : 0;  // first staged dpre channel of its group
+  float w3[kRegW ? SLICE : 1][9];
+  if (kRegW && act) {
+#pragma unroll
+    for (int t = 0; t < (kRegW ? SLICE : 1); ++t)
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) w3[t][tap] = __ldg(wd + int64_t(tap * SLICE + t) * g.Ci + ci);
+  }
+  auto wt = [&](int t, int tap) {
+    if constexpr (kRegW) return w3[t][tap];
+    else return wsm[(tap * SLICE + t) * 32 + col];
+  };
+  const int quads_w = (T.tw + 3) / 4;
+  float contrib = 0.f;
+  if (act) {
+    for (int qd = lane_p; qd < T.th * quads_w; qd += PL) {
+      const int th = qd / quads_w, tw = (qd - th * quads_w) * 4;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll(kRegW ? SLICE : 1)
+      for (int t = 0; t < SLICE; ++t) {
+        const float* hp = halo + (tl + t) * PS + th * IW + tw;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {  // staged row th + rr holds dpre row ih + P - (2 - rr)
+          float v[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) v[i] = hp[rr * IW + i];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+              acc[q] = fmaf(v[q + cc], wt(t, (2 - rr) * 3 + (2 - cc)), acc[q]);
+        }
+      }
+      const int ih = ih0t + th;
+      if (ih >= g.H) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int iw = iw0t + tw + q;
+        if (tw + q >= T.tw || iw >= g.W) continue;
+        const int64_t idx = ((n * g.H + ih) * g.W + iw) * g.Ci + ci;
+        if (g_out) g_out[idx] = acc[q];
+        if (a_prev) {
+          const float a = a_prev[idx];
+          contrib = fmaf(a, acc[q], contrib);
+          if (dpre_out) dpre_out[idx] = (relu_prev && !(a > 0.f)) ? 0.f : acc[q];  // I/nnet.hpp:229-233
+        } else if (dpre_out) {
+          dpre_out[idx] = acc[q];
+        }
+      }
+    }
+  }
+  if (!partial) return;
+  red[lane_p][col] = contrib;
+  __syncthreads();
+  if (lane_p == 0 && act) {
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < PL; ++k) sum += red[k][col];
+    partial[(n * gridDim.x + tile) * g.Ci + ci] = double(sum);
+  }
+}
+
 // Depthwise fprop (slice_ci = slice_co = 1): threads run over channels
 // (coalesced NHWC loads and stores), each computing kDwRun consecutive
 // output pixels of one row with its channel's taps held in registers.
@@ -694,9 +820,51 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
   }
 }
 
+size_t dgrad_grouped3_smem(const ConvGeom& g) {
+  const RangeDesc& r = g.r[0];
+  const GTile T = gtile(g.H, g.W);
+  const int cst = ((32 + r.slice_ci - 1) / r.slice_ci + 1) * r.slice_co;
+  const int IH = T.th + 2, IW = T.tw + 5;
+  return (size_t(cst) * (((IH * IW + 31) / 32) * 32 + 1) + 9 * size_t(r.slice_co) * 32) * 4;
+}
+
+bool dgrad_grouped3_ok(const ConvGeom& g) {
+  if (g.nranges != 1) return false;
+  const RangeDesc& r = g.r[0];
+  return r.groups >= 2 && g.KH == 3 && g.KW == 3 && g.S == 1 &&
+         (r.slice_co == 1 || r.slice_co == 2 || r.slice_co == 4 || r.slice_co == 8 ||
+          r.slice_co == 16) &&
+         dgrad_grouped3_smem(g) <= 200 * 1024;
+}
+
+int direct_dgrad_tiles(const ConvGeom& g) {
+  if (dgrad_grouped3_ok(g)) {
+    const GTile T = gtile(g.H, g.W);
+    return ((g.H + T.th - 1) / T.th) * ((g.W + T.tw - 1) / T.tw);
+  }
+  return dgrad_tiles(g.H, g.W);
+}
+
 void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
                          const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                          double* partial, cudaStream_t st) {
+  if (dgrad_grouped3_ok(g)) {
+    const size_t smem = dgrad_grouped3_smem(g);
+    dim3 grid(direct_dgrad_tiles(g), g.N, (g.Ci + 31) / 32);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      kern<<<grid, kGThreads, smem, st>>>(g, dpre, wbase, a_prev, relu_prev, dpre_out, g_out,
+                                          partial);
+    };
+    switch (g.r[0].slice_co) {
+      case 1: go(k_dgrad_grouped3<1>); break;
+      case 2: go(k_dgrad_grouped3<2>); break;
+      case 4: go(k_dgrad_grouped3<4>); break;
+      case 8: go(k_dgrad_grouped3<8>); break;
+      default: go(k_dgrad_grouped3<16>); break;
+    }
+    return;
+  }
   dim3 grid((g.Ci + 31) / 32, dgrad_tiles(g.H, g.W), g.N);
   k_dgrad_direct<<<grid, dim3(32, 8), 0, st>>>(g, dpre, wbase, a_prev, relu_prev, dpre_out,
                                                g_out, partial);

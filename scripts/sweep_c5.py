@@ -40,15 +40,33 @@ for c, hw in [(64, 56), (128, 28), (256, 14), (512, 7)]:
         tfs = flops / (ms / 1e3) / 1e12
         gbs = bytes_ / (ms / 1e3) / 1e9
         tc = "tc" in fam
+        # dgrad: the target conv as layer 1 behind a 1x1 conv (layer 0 has no
+        # dgrad), timed through a Fisher evaluation
+        net2 = Network([Layer(ConvSpec(c, c, hw, hw, 1, 1, 1, 0)),
+                        Layer(ConvSpec(c, c, hw, hw, 3, 3, 1, 1, groups=g))], num_classes=10, seed=42)
+        sess.fisher(net2, prec)
+        ctx.reset_stats()
+        ctx.set_profiling(True)
+        for _ in range(3):
+            sess.fisher(net2, prec)
+        ctx.set_profiling(False)
+        dst = {k: v for k, v in ctx.kernel_stats().items() if k.startswith("conv_dgrad")}
+        dms = sum(v["ms"] for v in dst.values()) / 3
+        dfam = max(dst, key=lambda k: dst[k]["ms"])
+        dbytes = bytes_ + 4.0 * 2 * N * hw * hw * c  # + a_prev read + dpre write (fused epilogue)
         row = {"C": c, "HW": hw, "G": g, "family": fam, "us": round(ms * 1e3, 2),
+               "dgrad_family": dfam, "dgrad_us": round(dms * 1e3, 2),
+               "dgrad_tflops": round(flops / (dms / 1e3) / 1e12, 2),
+               "dgrad_gbs": round(dbytes / (dms / 1e3) / 1e9, 1),
                "tflops": round(tfs, 2), "gbs": round(gbs, 1),
                "frac_tensor_bf16": round(tfs / BF16, 4), "frac_hbm": round(gbs / HBM, 4),
                "bound": "tensor" if tc else "hbm", "ai_flop_per_byte": round(flops / bytes_, 1)}
         rows.append(row)
         print(json.dumps(row), flush=True)
 print()
-print(f"| C@HW | G | kernel | us | TFLOP/s | GB/s | frac of bf16 peak | frac of HBM peak | AI |")
-print("|---|---|---|---|---|---|---|---|---|")
+print(f"| C@HW | G | fprop kernel | us | TFLOP/s | GB/s | frac bf16 | frac HBM | AI | dgrad kernel | us | TFLOP/s | GB/s |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 for r in rows:
     print(f"| {r['C']}@{r['HW']} | {r['G']} | `{r['family']}` | {r['us']} | {r['tflops']} | {r['gbs']} | "
-          f"{r['frac_tensor_bf16']:.3f} | {r['frac_hbm']:.3f} | {r['ai_flop_per_byte']} |")
+          f"{r['frac_tensor_bf16']:.3f} | {r['frac_hbm']:.3f} | {r['ai_flop_per_byte']} | "
+          f"`{r['dgrad_family']}` | {r['dgrad_us']} | {r['dgrad_tflops']} | {r['dgrad_gbs']} |")
