@@ -112,6 +112,12 @@ int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
 // SMs left idle by a small tile count are filled by the other candidates
 // the scheduler runs concurrently on the same GPU.
 int pick_bn(int n_per_group, bool split3) {
+  // NB_TC_BN3=256: the 256-wide single-accumulator 3xTF32 tile (experiment)
+  static const bool wide3 = [] {
+    const char* e = std::getenv("NB_TC_BN3");
+    return e && std::atoi(e) >= 256;
+  }();
+  if (split3 && wide3 && n_per_group % 256 == 0) return 256;
   static const int o3[] = {128, 64, 32};
   static const int o1[] = {256, 128, 64, 32};
   const int* o = split3 ? o3 : o1;

@@ -16,7 +16,8 @@
 //               K=8 per instruction, accumulator in TMEM (double-buffered)
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
-//   warps 8-11  (3xTF32 only) split converter: A_hi = rn_tf32(A),
+//   warps 8-15  (3xTF32 only) split converter, two groups on alternate K
+//               blocks: A_hi = rn_tf32(A),
 //               A_lo = rn_tf32(A - A_hi), written to TMEM (tcgen05.st), so the
 //               MMA warp issues A_hi*B_hi + A_hi*B_lo + A_lo*B_hi with A read
 //               from TMEM and only B from shared memory (fp32-accurate mode)
@@ -241,7 +242,7 @@ struct Cfg {
   static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
   static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * BN) / 64 : 99;
   static constexpr int kStages = kSmemStages < kTmemStages ? kSmemStages : kTmemStages;
-  static constexpr int kThreads = SPLIT3 ? 384 : 256;
+  static constexpr int kThreads = SPLIT3 ? 512 : 256;  // 3xTF32: two converter groups
   static constexpr int kTmemCols = SPLIT3 ? 512
                                  : (kAcc * BN) <= 32 ? 32 : (kAcc * BN) <= 64 ? 64
                                  : (kAcc * BN) <= 128 ? 128 : (kAcc * BN) <= 256 ? 256 : 512;
@@ -338,6 +339,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the next kernel on the stream may start
+  // its own prologue on SMs this grid leaves free; everything above (barrier
+  // init, TMEM allocation, descriptor prefetch) overlapped the previous
+  // kernel's tail.  Every global read and write below waits for that kernel.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // the barriers the other CTA's threads signal live in the MMA CTA (rank 0)
   const uint32_t ready_remote = PAIR ? mapa(ready, 0) : 0;
   const uint32_t tempty_remote = PAIR ? mapa(tempty, 0) : 0;
@@ -366,11 +373,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
           const int cb = kb % a.a_cblocks;
           const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], a_box_bytes + uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1));
-          tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+          const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
+          mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
+                                           (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
+          if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
           const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
-          tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
-          if (SPLIT3) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
+          if (ld_b) tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
+          if (SPLIT3 && ld_b) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -406,7 +415,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
           }
           tc_fence_after();
           const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
-          if (SPLIT3) {
+          if (a.debug & 2) {
+            // experiment: no MMAs (measures the TMA + converter pipeline alone)
+          } else if (SPLIT3) {
             // A_hi / A_lo of this stage in TMEM columns [a_t, a_t+32) / [a_t+32, a_t+64)
             const uint32_t a_t = tmem_base + uint32_t(C::kAcol0 + stage * 64);
             const uint64_t dbl = sw128_desc(smem_u32(b_lo(stage)));
@@ -500,7 +511,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
       tc_fence_after();
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = 0; c < ((a.debug & 16) ? 0 : BN); c += 16) {  // experiment: no epilogue
         float v[16];
         tmem_ld16(trow + uint32_t(c), v);
         if (empty_phase) {
@@ -637,14 +648,27 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
     // lane r): reads its 128-byte row from the swizzled stage (16-byte chunk
     // c sits at c ^ (r & 7)), splits it into rn_tf32 hi/lo halves and stores
     // them to the stage's 64 TMEM columns
-    const int ct = threadIdx.x - 256;  // 0..127 == TMEM lane
+    // two groups of four warps take alternate K blocks, so one group's
+    // shared-memory reads and splits overlap the other's TMEM stores
+    const int cg = (warp - 8) >> 2;
+    const int ct = threadIdx.x - 256 - cg * 128;  // 0..127 == TMEM lane
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    int stage = 0;
-    uint32_t phase = 0;
+    int it = 0;  // K blocks seen by this CTA (both groups count all of them)
     for (int u = unit0; u < num_units; u += ustep) {
       const Tile d = decode<PAIR>(a, u, int(rank));
-      for (int kb = d.kb0; kb < d.kb1; ++kb) {
+      for (int kb = d.kb0; kb < d.kb1; ++kb, ++it) {
+        if ((it & 1) != cg) continue;
+        const int stage = it % S;
+        const uint32_t phase = uint32_t(it / S) & 1u;
         mbar_wait(&full[stage], phase);
+        if (a.debug & 32) {  // experiment: no conversion work
+          named_bar(2 + cg, 128);
+          if (ct == 0) {
+            if (PAIR) mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+            else mbar_arrive(&ready[stage]);
+          }
+          continue;
+        }
         const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
         uint32_t hi[32], lo[32];
 #pragma unroll
@@ -664,17 +688,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         // all 128 rows stored -> one arrival per CTA on the MMA CTA's barrier
         tc_fence_before();
-        named_bar(2, 128);
+        named_bar(2 + cg, 128);
         if (ct == 0) {
           if (PAIR) {
             mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
           } else {
             mbar_arrive(&ready[stage]);
           }
-        }
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
         }
       }
     }
@@ -754,13 +774,15 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = PAIR ? 2 : 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = PAIR ? 2 : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = PAIR ? 1 : 0;
+  cfg.numAttrs = PAIR ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, PAIR>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
@@ -813,6 +835,7 @@ cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
       case 32: return launch_t<32, true, false>(L, st);
       case 64: return launch_t<64, true, false>(L, st);
       case 128: return launch_t<128, true, false>(L, st);
+      case 256: return launch_t<256, true, false>(L, st);
     }
   } else {
     switch (L.bn) {

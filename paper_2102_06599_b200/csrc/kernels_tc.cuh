@@ -67,8 +67,9 @@ struct TcArgs {
   float* g_out;
   double* partial;
   int relu_prev, part_tiles_per_img, part_ld;
-  // experiments only (NB_TC_DEBUG): bits 4.. = ring depth cap (0 = the
-  // configured stage count)
+  // experiments only (NB_TC_DEBUG): bit 1 = issue no MMAs (results
+  // garbage; times the operand pipeline alone), bits 4.. = ring depth cap
+  // (0 = the configured stage count)
   int debug;
 };
 

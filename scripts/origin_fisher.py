@@ -11,7 +11,8 @@ prec = {"fp32": Precision.FP32, "tf32": Precision.TF32, "simt": Precision.SIMT}[
     sys.argv[2] if len(sys.argv) > 2 else "fp32"]
 net = resnet34_chain()
 ctx = nb.Context(0)
-s = nb.Session(net, nb.make_batch(net, 128, 1), ctx=ctx)
+N = int(os.environ.get("ORIGIN_N", "128"))
+s = nb.Session(net, nb.make_batch(net, N, 1), ctx=ctx)
 for i in range(reps):
     t = time.perf_counter()
     r = s.fisher(net, prec)
