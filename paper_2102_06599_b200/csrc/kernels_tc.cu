@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
   const uint32_t tempty_remote = PAIR ? mapa(tempty, 0) : 0;
 
   const int m_units = PAIR ? (a.m_tiles + 1) / 2 : a.m_tiles;
-  const int num_units = a.nphase * m_units * a.n_tiles * a.ksplit;
+  const int num_units = (a.debug & 64) ? 0 : a.nphase * m_units * a.n_tiles * a.ksplit;
   const int unit0 = PAIR ? int(blockIdx.x) / 2 : int(blockIdx.x);
   const int ustep = PAIR ? int(gridDim.x) / 2 : int(gridDim.x);
   const uint32_t a_box_bytes = uint32_t(a.BW) * a.BH * a.BNI * 128;

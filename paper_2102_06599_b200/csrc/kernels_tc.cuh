@@ -67,9 +67,10 @@ struct TcArgs {
   float* g_out;
   double* partial;
   int relu_prev, part_tiles_per_img, part_ld;
-  // experiments only (NB_TC_DEBUG): bit 1 = issue no MMAs (results
-  // garbage; times the operand pipeline alone), bits 4.. = ring depth cap
-  // (0 = the configured stage count)
+  // experiments only (NB_TC_DEBUG; every bit but the stage cap gives
+  // garbage results): 2 = no MMAs, 4 = no A loads, 8 = no B loads, 16 = no
+  // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all; bits 4.. of
+  // (debug >> 4) also cap the ring depth (0 = the configured stage count)
   int debug;
 };
 
