@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -157,8 +158,10 @@ int pick_pair_bn(int n, int m_tiles, bool split3) {
   // 3xTF32 at 256 keeps a single TMEM accumulator (no epilogue overlap)
   const int cap = cap_env ? std::atoi(cap_env) : (split3 ? 128 : 256);
   if (!mode || m_tiles < 2) return 0;
+  if (mode == 2) return n % 64 == 0 && n < 128 ? 64 : 0;  // pairs only for 64-wide groups
   if (n % 256 == 0 && cap >= 256) return 256;
   if (n % 128 == 0 && cap >= 128) return 128;
+  if (n % 64 == 0) return 64;
   return 0;
 }
 
@@ -443,6 +446,19 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
     return e ? std::atoi(e) : 0;
   }();
   L.args.debug = dbg;
+  // NB_TC_TRACE=<launch index>: record CTA 0's stage timeline of that TC
+  // launch of this context and dump it to nb_tc_trace.txt (experiments)
+  static const int trace_at = [] {
+    const char* e = std::getenv("NB_TC_TRACE");
+    return e ? std::atoi(e) : -1;
+  }();
+  static int tc_launch_no = 0;
+  const bool tracing = trace_at >= 0 && tc_launch_no++ == trace_at;
+  if (tracing) {
+    c->trace.ensure(5 * tc::kTraceStages * 8);
+    NB_CUDA(cudaMemsetAsync(c->trace.p, 0, 5 * tc::kTraceStages * 8, st));
+    L.args.trace = c->trace.as<long long>();
+  }
   L.bn = tp.bn;
   L.split3 = split3;
   L.pair = tp.pair;
@@ -451,6 +467,21 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   NB_CUDA(tc::launch(L, st));
   c->launches++;
+  if (tracing) {
+    std::vector<long long> h(5 * tc::kTraceStages);
+    NB_CUDA(cudaMemcpyAsync(h.data(), c->trace.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaStreamSynchronize(st));
+    FILE* f = std::fopen("nb_tc_trace.txt", "w");
+    if (f) {
+      std::fprintf(f, "# bn=%d split3=%d stages tiles=%d kblocks/tile=%d\n", L.bn, int(L.split3),
+                   args.m_tiles * args.n_tiles, args.ntaps[0] * args.a_cblocks);
+      for (int i = 0; i < tc::kTraceStages; ++i)
+        std::fprintf(f, "%d %lld %lld %lld %lld %lld\n", i, h[i], h[tc::kTraceStages + i],
+                     h[2 * tc::kTraceStages + i], h[3 * tc::kTraceStages + i],
+                     h[4 * tc::kTraceStages + i]);
+      std::fclose(f);
+    }
+  }
 }
 
 // One layer's fprop (all ranges): y = relu?(conv(x)).

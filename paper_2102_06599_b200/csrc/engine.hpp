@@ -123,7 +123,7 @@ struct nb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::recursive_mutex mu;
-  nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws;
+  nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws, tilecnt, trace;
   int num_sms = 148;
   nb::PinnedBuf host_io, host_out;
   // device copies of z streams keyed by (seed, stream index)

@@ -251,6 +251,14 @@ struct Cfg {
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
 };
 
+// Trace slots (CTA 0, first kTraceStages K blocks): [role][it]
+//   0 producer issues TMA   1 converter sees the data   2 converter done
+//   3 MMA thread sees ready 4 MMA thread committed
+__device__ __forceinline__ void trace(const TcArgs& a, int role, int it) {
+  if (a.trace && blockIdx.x == 0 && it < kTraceStages)
+    a.trace[role * kTraceStages + it] = clock64();
+}
+
 // Work unit u of a launch: phase-major, then M tile (M tile pair for PAIR),
 // N tile, K split (innermost, so units of one output tile run side by side).
 struct Tile {
@@ -358,7 +366,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs: own A rows, own B rows)
-      int stage = 0;
+      int stage = 0, pit = 0;
       uint32_t phase = 0;
       for (int u = unit0; u < num_units; u += ustep) {
         const Tile d = decode<PAIR>(a, u, int(rank));
@@ -373,6 +381,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
           const int cb = kb % a.a_cblocks;
           const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
           mbar_wait(&empty[stage], phase ^ 1);
+          trace(a, 0, pit++);
           const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
           mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
                                            (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
@@ -392,7 +401,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
       // ---------------- MMA issuer (the pair's rank-0 CTA)
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
                                  (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
-      int stage = 0;
+      int stage = 0, mit = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int u = unit0; u < num_units; u += ustep, ++local) {
@@ -413,6 +422,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
           } else {
             mbar_wait(SPLIT3 ? &ready[stage] : &full[stage], phase);
           }
+          trace(a, 3, mit);
           tc_fence_after();
           const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
           if (a.debug & 2) {
@@ -453,6 +463,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
           } else {
             mma_commit(&empty[stage]);
           }
+          trace(a, 4, mit++);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -661,6 +672,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
         const int stage = it % S;
         const uint32_t phase = uint32_t(it / S) & 1u;
         mbar_wait(&full[stage], phase);
+        trace(a, 1, it);
         if (a.debug & 32) {  // experiment: no conversion work
           named_bar(2 + cg, 128);
           if (ct == 0) {
@@ -689,6 +701,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, PAIR>::kThreads, 1)
         // all 128 rows stored -> one arrival per CTA on the MMA CTA's barrier
         tc_fence_before();
         named_bar(2 + cg, 128);
+        if (ct == 0) trace(a, 2, it);
         if (ct == 0) {
           if (PAIR) {
             mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
@@ -819,11 +832,13 @@ cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
   if (L.pair) {
     if (L.split3) {
       switch (L.bn) {
+        case 64: return launch_t<64, true, true>(L, st);
         case 128: return launch_t<128, true, true>(L, st);
         case 256: return launch_t<256, true, true>(L, st);
       }
     } else {
       switch (L.bn) {
+        case 64: return launch_t<64, false, true>(L, st);
         case 128: return launch_t<128, false, true>(L, st);
         case 256: return launch_t<256, false, true>(L, st);
       }

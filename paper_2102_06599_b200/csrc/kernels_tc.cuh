@@ -72,7 +72,11 @@ struct TcArgs {
   // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all; bits 4.. of
   // (debug >> 4) also cap the ring depth (0 = the configured stage count)
   int debug;
+  // experiments only (NB_TC_TRACE): CTA 0 records clock64() stamps of its
+  // first kTraceStages K blocks here (see kernels_tc.cu)
+  long long* trace;
 };
+constexpr int kTraceStages = 256;
 
 struct TcLaunch {
   CUtensorMap mapA, mapBh, mapBl;
