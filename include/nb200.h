@@ -171,6 +171,8 @@ nb_status nb_make_batch(const nb_network* net, int64_t n, uint64_t seed,
 
 /* ---- contexts ------------------------------------------------------------ */
 nb_status nb_ctx_create(int device, nb_ctx** out);
+/* CUDA device ordinal of a context (-1 for NULL). */
+int nb_ctx_device(const nb_ctx* ctx);
 nb_status nb_ctx_destroy(nb_ctx* ctx);
 /* The CUDA stream (cudaStream_t) all of the context's kernels run on. */
 void* nb_ctx_stream(nb_ctx* ctx);
@@ -244,6 +246,73 @@ typedef struct nb_nest {
  * or fp64).  is_int != 0: in/w/out are int64, else double. */
 nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int, const void* in,
                           const void* w, void* out);
+
+/* ---- semantic legality (check_semantic_legality, I/transforms.hpp:598-663) */
+/* The brute-force dependence-preservation check of a semantic run (split /
+ * interchange / unroll steps) on the GPU.  Both nests are passed as
+ * statement entries of their compute_blocks (I/ir.hpp:163-218), Init
+ * statements included, in block order:
+ *  - schedule rank of an instance (its index in for_each_instance order,
+ *    I/ir.hpp:262-300) = rank_base + sum_k v_k * rank_stride[k];
+ *  - sid interns Statement::id across both nests (instance identity is the
+ *    (sid, domain coordinate) pair); gid is compute_dependences' per-nest
+ *    interning (I/ir.hpp:343-346) and only matters for the original;
+ *  - accesses (original only; transformed entries pass naccess = 0) are the
+ *    ones to tensors some statement of the original writes, tensor ids in
+ *    the reference's interning order -- touches of read-only tensors can
+ *    never form a dependence pair.
+ * lo/hi bound every domain value / cell index (any superset box is fine;
+ * the bridge uses interval arithmetic over the affine programs).  Instance
+ * caps (CapExceeded) stay with the caller; NB_ERR_UNSUPPORTED means the keys
+ * do not fit 64 bits and the caller must run the host check. */
+typedef struct nb_legal_access {
+  int32_t tensor;
+  int32_t mode; /* 0 Read, 1 Write, 2 ReadModifyWrite (AccessMode) */
+  int32_t rank;
+  const nb_nest_expr* idx; /* over the statement's domain values */
+  const int64_t* lo;       /* rank bounds of each index */
+  const int64_t* hi;
+} nb_legal_access;
+
+typedef struct nb_legal_stmt {
+  int32_t sid, gid;
+  int32_t depth;
+  const int64_t* extents;     /* depth trip counts, outermost first */
+  int64_t rank_base;
+  const int64_t* rank_stride; /* depth entries */
+  int32_t ndomain;
+  const nb_nest_expr* coord;  /* ndomain expressions over the loop values */
+  const int64_t* lo;          /* ndomain bounds of each coordinate */
+  const int64_t* hi;
+  int32_t naccess;
+  const nb_legal_access* access;
+} nb_legal_stmt;
+
+typedef struct nb_legal_nest {
+  int64_t num_stmts;
+  const nb_legal_stmt* stmts;
+} nb_legal_nest;
+
+typedef enum nb_legal_verdict {
+  NB_LEGAL = 0,
+  NB_ILLEGAL_DUPLICATE = 1, /* "transformed schedule duplicates an instance" */
+  NB_NOT_APPLICABLE = 2,    /* "instance sets differ (...)" */
+  NB_ILLEGAL_REORDER = 3    /* "dependence S(..) -> S(..) is reordered" */
+} nb_legal_verdict;
+
+typedef struct nb_legal_out {
+  int32_t verdict;
+  /* NB_ILLEGAL_REORDER: the first reordered pair in the reference's order,
+   * as original-schedule instance indices, entries of original->stmts and
+   * domain coordinates */
+  int64_t src_inst, dst_inst;
+  int32_t src_stmt, dst_stmt;
+  int64_t src_coord[8], dst_coord[8];
+  int64_t pairs; /* dependence pairs checked (reduction pairs excluded) */
+} nb_legal_out;
+
+nb_status nb_semantic_legality(nb_ctx* ctx, const nb_legal_nest* original,
+                               const nb_legal_nest* transformed, nb_legal_out* out);
 
 /* ---- network-level entry points ----------------------------------------- */
 /* forward, I/nnet.hpp:180-197: probs n x classes, example_loss n, loss. */

@@ -24,6 +24,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <sstream>
 #include <map>
@@ -240,6 +241,37 @@ inline nestopt::TensorF layer_forward(Context& ctx, const nestopt::Layer& layer,
 // of compute_blocks (I/ir.hpp:163-218), its multiply-accumulate statements
 // with their coordinate programs over the block's loop values and their
 // access programs over the statement's domain values.
+namespace detail {
+
+// AffineExpr (I/affine.hpp:17-72) -> postfix (op, arg) pairs over slots
+inline void emit_into(const nestopt::AffineExpr& e, const std::map<std::string, int>& slots,
+                      std::vector<int64_t>& out) {
+  using K = nestopt::AffineExpr::Kind;
+  switch (e.kind) {
+    case K::Const: out.insert(out.end(), {0, e.k}); return;
+    case K::Var: {
+      auto it = slots.find(e.var);
+      if (it == slots.end()) throw nestopt::Error("unbound iterator '" + e.var + "'");
+      out.insert(out.end(), {1, it->second});
+      return;
+    }
+    case K::Add:
+      for (const auto& a : e.args) emit_into(a, slots, out);
+      out.insert(out.end(), {2, int64_t(e.args.size())});
+      return;
+    case K::Mul: emit_into(e.args[0], slots, out); out.insert(out.end(), {3, e.k}); return;
+    case K::Div: emit_into(e.args[0], slots, out); out.insert(out.end(), {4, e.k}); return;
+    case K::Mod: emit_into(e.args[0], slots, out); out.insert(out.end(), {5, e.k}); return;
+  }
+}
+inline std::vector<int64_t> emit(const nestopt::AffineExpr& e,
+                                 const std::map<std::string, int>& slots) {
+  std::vector<int64_t> out;
+  emit_into(e, slots, out);
+  return out;
+}
+}  // namespace detail
+
 class NestProgram {
  public:
   NestProgram(const nestopt::LoopNest& nest, const std::string& out_name,
@@ -259,7 +291,7 @@ class NestProgram {
         std::map<std::string, int> dslots;
         for (size_t i = 0; i < st.domain.size(); ++i) {
           dslots[st.domain[i]] = int(i);
-          r.coord.push_back(emit(st.coord.at(st.domain[i]), slots));
+          r.coord.push_back(detail::emit(st.coord.at(st.domain[i]), slots));
         }
         for (const AccessMap& acc : st.accesses) {
           AccRec ar;
@@ -268,7 +300,7 @@ class NestProgram {
           if (ar.tensor != 0 && acc.mode != AccessMode::Read)
             throw Error("nest writes more than one tensor");
           ar.zero_pad = acc.zero_pad ? 1 : 0;
-          for (const auto& e : acc.indices) ar.idx.push_back(emit(e, dslots));
+          for (const auto& e : acc.indices) ar.idx.push_back(detail::emit(e, dslots));
           r.acc.push_back(std::move(ar));
         }
         recs.push_back(std::move(r));
@@ -315,33 +347,6 @@ class NestProgram {
     std::vector<AccRec> acc;
     std::vector<nb_nest_access> acc_c;
   };
-  // AffineExpr (I/affine.hpp:17-72) -> postfix (op, arg) pairs over slots
-  static std::vector<int64_t> emit(const nestopt::AffineExpr& e,
-                                   const std::map<std::string, int>& slots) {
-    std::vector<int64_t> out;
-    emit_into(e, slots, out);
-    return out;
-  }
-  static void emit_into(const nestopt::AffineExpr& e, const std::map<std::string, int>& slots,
-                        std::vector<int64_t>& out) {
-    using K = nestopt::AffineExpr::Kind;
-    switch (e.kind) {
-      case K::Const: out.insert(out.end(), {0, e.k}); return;
-      case K::Var: {
-        auto it = slots.find(e.var);
-        if (it == slots.end()) throw nestopt::Error("unbound iterator '" + e.var + "'");
-        out.insert(out.end(), {1, it->second});
-        return;
-      }
-      case K::Add:
-        for (const auto& a : e.args) emit_into(a, slots, out);
-        out.insert(out.end(), {2, int64_t(e.args.size())});
-        return;
-      case K::Mul: emit_into(e.args[0], slots, out); out.insert(out.end(), {3, e.k}); return;
-      case K::Div: emit_into(e.args[0], slots, out); out.insert(out.end(), {4, e.k}); return;
-      case K::Mod: emit_into(e.args[0], slots, out); out.insert(out.end(), {5, e.k}); return;
-    }
-  }
   std::vector<StmtRec> recs_;
   std::vector<nb_nest_stmt> stmts_;
   nb_nest c_{};
@@ -374,6 +379,231 @@ nestopt::Tensor<T> execute(Context& ctx, const nestopt::LoopNest& nest,
   return out;
 }
 
+// ---- semantic legality on the GPU -----------------------------------------
+
+namespace detail {
+
+// Interval of a postfix program over slot intervals (any enclosing box is a
+// valid packing bound for nb_semantic_legality).
+inline std::pair<int64_t, int64_t> interval(const std::vector<int64_t>& code,
+                                            const std::vector<std::pair<int64_t, int64_t>>& slot) {
+  auto fdiv = [](int64_t a, int64_t b) {
+    int64_t q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+  };
+  std::vector<std::pair<int64_t, int64_t>> st;
+  for (size_t i = 0; i + 1 < code.size(); i += 2) {
+    const int64_t op = code[i], arg = code[i + 1];
+    switch (op) {
+      case 0: st.push_back({arg, arg}); break;
+      case 1: st.push_back(slot.at(size_t(arg))); break;
+      case 2: {
+        std::pair<int64_t, int64_t> s{0, 0};
+        for (int64_t k = 0; k < arg; ++k) {
+          s.first += st.back().first;
+          s.second += st.back().second;
+          st.pop_back();
+        }
+        st.push_back(s);
+        break;
+      }
+      case 3: {
+        auto& t = st.back();
+        t = arg >= 0 ? std::pair<int64_t, int64_t>{t.first * arg, t.second * arg}
+                     : std::pair<int64_t, int64_t>{t.second * arg, t.first * arg};
+        break;
+      }
+      case 4: {
+        auto& t = st.back();
+        t = arg > 0 ? std::pair<int64_t, int64_t>{fdiv(t.first, arg), fdiv(t.second, arg)}
+                    : std::pair<int64_t, int64_t>{fdiv(t.second, arg), fdiv(t.first, arg)};
+        break;
+      }
+      default: {
+        auto& t = st.back();
+        if (arg > 0 && fdiv(t.first, arg) == fdiv(t.second, arg)) {
+          const int64_t q = fdiv(t.first, arg) * arg;
+          t = {t.first - q, t.second - q};
+        } else {
+          t = arg > 0 ? std::pair<int64_t, int64_t>{0, arg - 1}
+                      : std::pair<int64_t, int64_t>{arg + 1, 0};
+        }
+      }
+    }
+  }
+  return st.back();
+}
+
+// One nest in nb_legal_nest form: an entry per statement of each block of
+// compute_blocks (I/ir.hpp:169-204), with the schedule-rank formula of
+// for_each_instance's walk (I/ir.hpp:262-292): at loop level k the walk
+// first visits the n_k statements of that depth, then ext_k subtrees of
+// T(k+1) instances each, so an instance at depth d with loop values v has
+// rank block_base + sum_{k<d} (n_k + v_k T(k+1)) + its index among the
+// depth-d statements.
+class LegalNest {
+ public:
+  LegalNest(const nestopt::LoopNest& nest, std::map<std::string, int>& sid,
+            const std::map<std::string, int>* tensor_ids,
+            const std::vector<char>* written) {
+    using namespace nestopt;
+    std::map<std::string, int> gid_of;  // compute_dependences' interning, I/ir.hpp:343-346
+    for (const auto& part : nest.parts)
+      for (const auto& st : part.stmts) gid_of.emplace(st.id, int(gid_of.size()));
+    int64_t block_base = 0;
+    for (const Block& b : compute_blocks(nest)) {
+      const NestPart& part = nest.parts[size_t(b.part)];
+      const size_t D = b.iters.size();
+      std::vector<int64_t> n_at(D + 1, 0), T(D + 2, 0);
+      for (auto [si, depth] : b.stmts) n_at[size_t(depth)]++;
+      T[D] = n_at[D];
+      for (size_t k = D; k-- > 0;) T[k] = n_at[k] + b.iters[k].extent * T[k + 1];
+      std::map<std::string, int> slots;
+      std::vector<std::pair<int64_t, int64_t>> loop_rng;
+      for (size_t i = 0; i < D; ++i) {
+        slots[b.iters[i].name] = int(i);
+        loop_rng.push_back({0, std::max<int64_t>(0, b.iters[i].extent - 1)});
+      }
+      std::vector<int64_t> seen(D + 1, 0);
+      for (auto [si, depth] : b.stmts) {
+        const Statement& st = part.stmts[size_t(si)];
+        Rec r;
+        r.id = st.id;
+        r.sid = sid.emplace(st.id, int(sid.size())).first->second;
+        r.gid = gid_of.at(st.id);
+        r.rank_base = block_base + seen[size_t(depth)]++;
+        for (int k = 0; k < depth; ++k) {
+          r.rank_base += n_at[size_t(k)];
+          r.extents.push_back(b.iters[size_t(k)].extent);
+          r.stride.push_back(T[size_t(k) + 1]);
+        }
+        std::map<std::string, int> dslots;
+        std::vector<std::pair<int64_t, int64_t>> dom_rng;
+        for (size_t i = 0; i < st.domain.size(); ++i) {
+          dslots[st.domain[i]] = int(i);
+          r.coord.push_back(emit(st.coord.at(st.domain[i]), slots));
+          const auto iv = interval(r.coord.back(), loop_rng);
+          r.lo.push_back(iv.first);
+          r.hi.push_back(iv.second);
+          dom_rng.push_back(iv);
+        }
+        if (tensor_ids)
+          for (const AccessMap& acc : st.accesses) {
+            const int t = tensor_ids->at(acc.tensor);
+            if (!(*written)[size_t(t)]) continue;  // read-only: never in a pair
+            Acc a;
+            a.tensor = t;
+            a.mode = acc.mode == AccessMode::Read ? 0 : acc.mode == AccessMode::Write ? 1 : 2;
+            for (const auto& e : acc.indices) {
+              a.idx.push_back(emit(e, dslots));
+              const auto iv = interval(a.idx.back(), dom_rng);
+              a.lo.push_back(iv.first);
+              a.hi.push_back(iv.second);
+            }
+            r.acc.push_back(std::move(a));
+          }
+        recs_.push_back(std::move(r));
+      }
+      block_base += T[0];
+    }
+    for (auto& r : recs_) {
+      for (auto& c : r.coord) r.coord_c.push_back(nb_nest_expr{int32_t(c.size() / 2), c.data()});
+      for (auto& a : r.acc) {
+        for (auto& c : a.idx) a.idx_c.push_back(nb_nest_expr{int32_t(c.size() / 2), c.data()});
+        r.acc_c.push_back(nb_legal_access{a.tensor, a.mode, int32_t(a.idx_c.size()),
+                                          a.idx_c.data(), a.lo.data(), a.hi.data()});
+      }
+      stmts_.push_back(nb_legal_stmt{r.sid, r.gid, int32_t(r.extents.size()), r.extents.data(),
+                                     r.rank_base, r.stride.data(), int32_t(r.coord_c.size()),
+                                     r.coord_c.data(), r.lo.data(), r.hi.data(),
+                                     int32_t(r.acc_c.size()), r.acc_c.data()});
+    }
+    c_ = nb_legal_nest{int64_t(stmts_.size()), stmts_.data()};
+  }
+  const nb_legal_nest* get() const { return &c_; }
+  const std::string& id(int entry) const { return recs_.at(size_t(entry)).id; }
+  size_t ndomain(int entry) const { return recs_.at(size_t(entry)).coord.size(); }
+
+ private:
+  struct Acc {
+    int32_t tensor = 0, mode = 0;
+    std::vector<std::vector<int64_t>> idx;
+    std::vector<nb_nest_expr> idx_c;
+    std::vector<int64_t> lo, hi;
+  };
+  struct Rec {
+    std::string id;
+    int32_t sid = 0, gid = 0;
+    int64_t rank_base = 0;
+    std::vector<int64_t> extents, stride, lo, hi;
+    std::vector<std::vector<int64_t>> coord;
+    std::vector<nb_nest_expr> coord_c;
+    std::vector<Acc> acc;
+    std::vector<nb_legal_access> acc_c;
+  };
+  std::vector<Rec> recs_;
+  std::vector<nb_legal_stmt> stmts_;
+  nb_legal_nest c_{};
+};
+
+}  // namespace detail
+
+// check_semantic_legality (I/transforms.hpp:598-663) with the brute-force
+// dependence check on the GPU (nb_semantic_legality): the same CapExceeded
+// throws, verdicts and reasons.  Nests smaller than `gpu_min_instances` (a
+// device round trip costs more than the host check) and nests the kernel
+// cannot key in 64 bits run the reference's own function.
+inline nestopt::LegalityResult check_semantic_legality(
+    Context& ctx, const nestopt::LoopNest& original, const nestopt::LoopNest& transformed,
+    long long cap = nestopt::kDefaultInstanceCap, long long gpu_min_instances = 0) {
+  using namespace nestopt;
+  const long long nt = instance_count(transformed);
+  if (nt > cap) throw CapExceeded("transformed nest exceeds brute-force cap");
+  const long long no = instance_count(original);
+  if (no > cap)
+    throw CapExceeded("instance count exceeds brute-force cap of " + std::to_string(cap));
+  if (std::max(nt, no) < gpu_min_instances)
+    return nestopt::check_semantic_legality(original, transformed, cap);
+  std::map<std::string, int> tensor_ids;  // I/ir.hpp:347-352 interning order
+  for (const auto& part : original.parts)
+    for (const auto& st : part.stmts)
+      for (const auto& a : st.accesses) tensor_ids.emplace(a.tensor, int(tensor_ids.size()));
+  std::vector<char> written(tensor_ids.size(), 0);
+  for (const auto& part : original.parts)
+    for (const auto& st : part.stmts)
+      for (const auto& a : st.accesses)
+        if (a.mode != AccessMode::Read) written[size_t(tensor_ids.at(a.tensor))] = 1;
+  std::map<std::string, int> sid;
+  std::unique_ptr<detail::LegalNest> lo, lt;
+  try {
+    lo = std::make_unique<detail::LegalNest>(original, sid, &tensor_ids, &written);
+    lt = std::make_unique<detail::LegalNest>(transformed, sid, nullptr, nullptr);
+  } catch (const std::exception&) {
+    // a nest the bridge cannot compile: the reference reports its own error
+    return nestopt::check_semantic_legality(original, transformed, cap);
+  }
+  nb_legal_out out{};
+  const nb_status s = nb_semantic_legality(ctx.get(), lo->get(), lt->get(), &out);
+  if (s == NB_ERR_UNSUPPORTED) return nestopt::check_semantic_legality(original, transformed, cap);
+  check(s);
+  switch (out.verdict) {
+    case NB_LEGAL: return {Verdict::Legal, ""};
+    case NB_ILLEGAL_DUPLICATE:
+      return {Verdict::Illegal, "transformed schedule duplicates an instance"};
+    case NB_NOT_APPLICABLE:
+      return {Verdict::NotApplicable, "instance sets differ (neural rewrite changes the domain)"};
+    default: break;
+  }
+  std::ostringstream os;
+  os << "dependence " << lo->id(out.src_stmt) << "(";
+  for (size_t i = 0; i < lo->ndomain(out.src_stmt); ++i) os << (i ? "," : "") << out.src_coord[i];
+  os << ") -> " << lo->id(out.dst_stmt) << "(";
+  for (size_t i = 0; i < lo->ndomain(out.dst_stmt); ++i) os << (i ? "," : "") << out.dst_coord[i];
+  os << ") is reordered";
+  return {Verdict::Illegal, os.str()};
+}
+
 // ---- the candidate scheduler -------------------------------------------
 
 // The host half of evaluate_candidate (I/search.hpp:219-293): replays the
@@ -386,7 +616,8 @@ nestopt::Tensor<T> execute(Context& ctx, const nestopt::LoopNest& nest,
 // cached z-streams -- so only Network::validate() runs after propagation.
 inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
                        const nestopt::SearchConfig& cfg,
-                       const nestopt::FisherReport& origin_fisher, nestopt::Network& net) {
+                       const nestopt::FisherReport& origin_fisher, nestopt::Network& net,
+                       Context* legal_ctx = nullptr, long long legal_gpu_min = 0) {
   using namespace nestopt;
   std::vector<ConvSpec> specs;
   for (size_t l = 0; l < origin.layers.size(); ++l) {
@@ -395,7 +626,10 @@ inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
     bool pending_semantic = false;
     auto flush = [&](size_t s) {
       if (!pending_semantic) return true;
-      LegalityResult lr = check_semantic_legality(run_origin, nest, cfg.cap);
+      LegalityResult lr =
+          legal_ctx ? nb200::check_semantic_legality(*legal_ctx, run_origin, nest, cfg.cap,
+                                                     legal_gpu_min)
+                    : nestopt::check_semantic_legality(run_origin, nest, cfg.cap);
       pending_semantic = false;
       if (lr.verdict == Verdict::Illegal) {
         cand.status = CandidateStatus::RejectedSemantic;
@@ -505,6 +739,14 @@ inline bool same_network(const nestopt::Network& a, const nestopt::Network& b) {
   return true;
 }
 
+// Instance count from which a semantic run is checked on the GPU
+// (NB_LEGAL_GPU_MIN; -1 = always on the host).  Below it the host check is
+// faster than a device round trip.
+inline long long legal_gpu_min() {
+  const char* e = std::getenv("NB_LEGAL_GPU_MIN");
+  return e && *e ? std::atoll(e) : 20000;
+}
+
 // Scheduler statistics of one evaluate_all_gpu call.
 struct GpuStats {
   int64_t scored = 0, evaluated = 0, deduplicated = 0, origin_equal = 0, rechecked = 0;
@@ -531,18 +773,25 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
   {
     const int jobs = std::max(1, std::min<int>(cfg.jobs, int(cands.size())));
     std::atomic<size_t> next{0};
-    auto worker = [&]() {
+    // each gate thread checks semantic runs on its own context of a session's GPU
+    const long long gpu_min = legal_gpu_min();
+    auto worker = [&](int j) {
+      std::unique_ptr<Context> lctx;
       for (;;) {
         const size_t i = next.fetch_add(1);
         if (i >= cands.size()) return;
-        pending[i] = host_gates(cands[i], origin, cfg, origin_fisher, nets[i]) ? 1 : 0;
+        if (!lctx && gpu_min >= 0 && !sessions.empty())
+          lctx = std::make_unique<Context>(
+              nb_ctx_device(nb_session_ctx(sessions[size_t(j) % sessions.size()]->get())));
+        pending[i] =
+            host_gates(cands[i], origin, cfg, origin_fisher, nets[i], lctx.get(), gpu_min) ? 1 : 0;
       }
     };
     if (jobs == 1) {
-      worker();
+      worker(0);
     } else {
       std::vector<std::thread> pool;
-      for (int j = 0; j < jobs; ++j) pool.emplace_back(worker);
+      for (int j = 0; j < jobs; ++j) pool.emplace_back(worker, j);
       for (auto& t : pool) t.join();
     }
   }

@@ -3,7 +3,9 @@
 // search-config schema v1 with an embedded "network", as in
 // P/samples/search_toy.json), the reference's search report JSON out
 // (search_report_to_json, I/search.hpp:461-496) plus a "gpu" block.
+#include <chrono>
 #include <cstdlib>
+#include <memory>
 #include <limits>
 #include <cstring>
 #include <sstream>
@@ -26,6 +28,132 @@ std::vector<int> parse_devices(const char* devs) {
   std::stringstream ss(devs ? devs : "0");
   std::string tok;
   while (std::getline(ss, tok, ',')) out.push_back(std::stoi(tok));
+  return out;
+}
+
+// LoopNest <-> JSON (the reference has no nest serializer; this one lets
+// tests hand-build nests the DSL cannot express, as the reference's own
+// legality tests do, P/tests/test_transforms.cpp:311-408).  Expressions are
+// nested arrays: ["c", k] | ["v", name] | ["add", e...] | ["mul"|"div"|"mod", e, k].
+nlohmann::json expr_to_json(const nestopt::AffineExpr& e) {
+  using K = nestopt::AffineExpr::Kind;
+  switch (e.kind) {
+    case K::Const: return nlohmann::json::array({"c", e.k});
+    case K::Var: return nlohmann::json::array({"v", e.var});
+    case K::Add: {
+      nlohmann::json j = nlohmann::json::array({"add"});
+      for (const auto& a : e.args) j.push_back(expr_to_json(a));
+      return j;
+    }
+    case K::Mul: return nlohmann::json::array({"mul", expr_to_json(e.args[0]), e.k});
+    case K::Div: return nlohmann::json::array({"div", expr_to_json(e.args[0]), e.k});
+    case K::Mod: return nlohmann::json::array({"mod", expr_to_json(e.args[0]), e.k});
+  }
+  return {};
+}
+
+nestopt::AffineExpr expr_from_json(const nlohmann::json& j) {
+  using K = nestopt::AffineExpr::Kind;
+  nestopt::AffineExpr e;
+  const std::string op = j.at(0).get<std::string>();
+  if (op == "c") {
+    e.kind = K::Const;
+    e.k = j.at(1).get<long long>();
+  } else if (op == "v") {
+    e.kind = K::Var;
+    e.var = j.at(1).get<std::string>();
+  } else if (op == "add") {
+    e.kind = K::Add;
+    for (size_t i = 1; i < j.size(); ++i) e.args.push_back(expr_from_json(j[i]));
+  } else {
+    e.kind = op == "mul" ? K::Mul : op == "div" ? K::Div : op == "mod" ? K::Mod
+                                                                       : throw nestopt::ParseError("bad expression op " + op);
+    e.args.push_back(expr_from_json(j.at(1)));
+    e.k = j.at(2).get<long long>();
+  }
+  return e;
+}
+
+nlohmann::json nest_to_json(const nestopt::LoopNest& n) {
+  nlohmann::json parts = nlohmann::json::array();
+  for (const auto& p : n.parts) {
+    nlohmann::json spine = nlohmann::json::array(), stmts = nlohmann::json::array();
+    for (const auto& iv : p.spine) spine.push_back({iv.name, iv.extent, iv.unroll, iv.kernel});
+    for (const auto& st : p.stmts) {
+      nlohmann::json coord = nlohmann::json::object(), acc = nlohmann::json::array();
+      for (const auto& [k, e] : st.coord) coord[k] = expr_to_json(e);
+      for (const auto& a : st.accesses) {
+        nlohmann::json idx = nlohmann::json::array();
+        for (const auto& e : a.indices) idx.push_back(expr_to_json(e));
+        acc.push_back({{"tensor", a.tensor},
+                       {"mode", a.mode == nestopt::AccessMode::Read    ? "r"
+                                : a.mode == nestopt::AccessMode::Write ? "w"
+                                                                       : "rmw"},
+                       {"indices", idx},
+                       {"zero_pad", a.zero_pad}});
+      }
+      stmts.push_back({{"id", st.id},
+                       {"kind", st.kind == nestopt::StmtKind::Init ? "init" : "mac"},
+                       {"domain", st.domain},
+                       {"coord", coord},
+                       {"accesses", acc}});
+    }
+    parts.push_back({{"spine", spine}, {"stmts", stmts}});
+  }
+  return {{"parts", parts}};
+}
+
+nestopt::LoopNest nest_from_json(const nlohmann::json& j) {
+  nestopt::LoopNest n;
+  for (const auto& pj : j.at("parts")) {
+    nestopt::NestPart p;
+    for (const auto& iv : pj.at("spine"))
+      p.spine.push_back({iv.at(0).get<std::string>(), iv.at(1).get<long long>(),
+                         iv.size() > 2 ? iv.at(2).get<long long>() : 1,
+                         iv.size() > 3 ? iv.at(3).get<bool>() : false});
+    for (const auto& sj : pj.at("stmts")) {
+      nestopt::Statement st;
+      st.id = sj.at("id").get<std::string>();
+      st.kind = sj.at("kind").get<std::string>() == "init" ? nestopt::StmtKind::Init
+                                                            : nestopt::StmtKind::Mac;
+      st.domain = sj.at("domain").get<std::vector<std::string>>();
+      for (const auto& [k, e] : sj.at("coord").items()) st.coord[k] = expr_from_json(e);
+      for (const auto& aj : sj.at("accesses")) {
+        nestopt::AccessMap a;
+        a.tensor = aj.at("tensor").get<std::string>();
+        const std::string m = aj.at("mode").get<std::string>();
+        a.mode = m == "r" ? nestopt::AccessMode::Read
+                 : m == "w" ? nestopt::AccessMode::Write
+                            : nestopt::AccessMode::ReadModifyWrite;
+        for (const auto& e : aj.at("indices")) a.indices.push_back(expr_from_json(e));
+        a.zero_pad = aj.value("zero_pad", false);
+        st.accesses.push_back(std::move(a));
+      }
+      p.stmts.push_back(std::move(st));
+    }
+    n.parts.push_back(std::move(p));
+  }
+  return n;
+}
+
+nlohmann::json legality_json(const nestopt::LoopNest& orig, const nestopt::LoopNest& tr,
+                             long long cap, int device, double* ms) {
+  std::unique_ptr<nb200::Context> ctx;
+  if (device >= 0) ctx = std::make_unique<nb200::Context>(device);
+  nlohmann::json out;
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    nestopt::LegalityResult r = ctx ? nb200::check_semantic_legality(*ctx, orig, tr, cap, 0)
+                                    : nestopt::check_semantic_legality(orig, tr, cap);
+    out["verdict"] = r.verdict == nestopt::Verdict::Legal     ? "legal"
+                     : r.verdict == nestopt::Verdict::Illegal ? "illegal"
+                                                              : "not_applicable";
+    out["reason"] = r.reason;
+  } catch (const nestopt::CapExceeded& e) {
+    out["error"] = "CapExceeded";
+    out["what"] = e.what();
+  }
+  if (ms) *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return out;
 }
 }  // namespace
@@ -115,8 +243,10 @@ int nbi_execute(const char* spec_json, const char* dsl, int is_int, const void* 
 // the gates of evaluate_candidate (nb200::host_gates).  Per candidate the
 // output holds its status after the gates ("fisher" = a neural candidate the
 // GPU must score), reason, macs, and for "fisher" candidates the repaired
-// network (network_to_json, I/nnet.hpp:444-454).
-int nbi_gate_candidates(const char* cfg_json, char** out_json) {
+// network (network_to_json, I/nnet.hpp:444-454).  legal_device >= 0 checks
+// semantic runs on that GPU (nb200::check_semantic_legality, one context per
+// gate thread); -1 runs the reference's host check.
+int nbi_gate_candidates(const char* cfg_json, int legal_device, char** out_json) {
   try {
     nlohmann::json j = nlohmann::json::parse(cfg_json);
     nestopt::Network origin = nestopt::network_from_json(j.at("network"));
@@ -130,9 +260,13 @@ int nbi_gate_candidates(const char* cfg_json, char** out_json) {
     std::vector<char> pend(cands.size(), 0);
     {
       std::atomic<size_t> next{0};
+      const long long gpu_min = nb200::legal_gpu_min();
       auto worker = [&]() {
+        std::unique_ptr<nb200::Context> lctx;
+        if (legal_device >= 0 && gpu_min >= 0) lctx = std::make_unique<nb200::Context>(legal_device);
         for (size_t i; (i = next.fetch_add(1)) < cands.size();)
-          pend[i] = nb200::host_gates(cands[i], origin, cfg, dummy, nets[i]) ? 1 : 0;
+          pend[i] = nb200::host_gates(cands[i], origin, cfg, dummy, nets[i], lctx.get(), gpu_min)
+                        ? 1 : 0;
       };
       std::vector<std::thread> pool;
       const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
@@ -156,6 +290,62 @@ int nbi_gate_candidates(const char* cfg_json, char** out_json) {
   } catch (const nestopt::ConfigError& e) {
     g_err = e.what();
     return NB_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+// check_semantic_legality (I/transforms.hpp:598-663) of one semantic run:
+// original = conv_nest(spec) rewritten by `pre` (any steps, may be empty),
+// transformed = original rewritten by `seq`.  device < 0 runs the
+// reference's host function, else nb200::check_semantic_legality on that GPU
+// (gpu_min_instances 0: always on the device).  Output JSON: {"verdict":
+// "legal"|"illegal"|"not_applicable", "reason": ...} or {"error": class,
+// "what": message} when the check throws (CapExceeded).
+int nbi_legality(const char* spec_json, const char* pre, const char* seq, long long cap,
+                 int device, double* ms, char** out_json) {
+  try {
+    nestopt::ConvSpec s = nestopt::conv_spec_from_json(nlohmann::json::parse(spec_json));
+    nestopt::LoopNest orig = nestopt::conv_nest(s);
+    if (pre && *pre) orig = nestopt::apply(orig, nestopt::parse_sequence(pre));
+    nestopt::LoopNest tr = nestopt::apply(orig, nestopt::parse_sequence(seq));
+    *out_json = dup(legality_json(orig, tr, cap, device, ms).dump());
+    return 0;
+  } catch (const nb200::DeviceError& e) {
+    g_err = e.what();
+    return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+// The same check on two explicit nests (nest JSON above).
+int nbi_legality_nests(const char* orig_json, const char* tr_json, long long cap, int device,
+                       double* ms, char** out_json) {
+  try {
+    nestopt::LoopNest orig = nest_from_json(nlohmann::json::parse(orig_json));
+    nestopt::LoopNest tr = nest_from_json(nlohmann::json::parse(tr_json));
+    *out_json = dup(legality_json(orig, tr, cap, device, ms).dump());
+    return 0;
+  } catch (const nb200::DeviceError& e) {
+    g_err = e.what();
+    return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+// conv_nest(spec) rewritten by `dsl` (may be empty), as nest JSON.
+int nbi_nest_json(const char* spec_json, const char* dsl, char** out_json) {
+  try {
+    nestopt::ConvSpec s = nestopt::conv_spec_from_json(nlohmann::json::parse(spec_json));
+    nestopt::LoopNest n = nestopt::conv_nest(s);
+    if (dsl && *dsl) n = nestopt::apply(n, nestopt::parse_sequence(dsl));
+    *out_json = dup(nest_to_json(n).dump());
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return NB_ERR_GENERIC;

@@ -92,6 +92,31 @@ class NestStmtC(C.Structure):
                 ("naccess", C.c_int32), ("access", C.POINTER(NestAccessC))]
 
 
+class LegalAccessC(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("mode", C.c_int32), ("rank", C.c_int32),
+                ("idx", C.POINTER(NestExprC)), ("lo", C.POINTER(C.c_int64)),
+                ("hi", C.POINTER(C.c_int64))]
+
+
+class LegalStmtC(C.Structure):
+    _fields_ = [("sid", C.c_int32), ("gid", C.c_int32), ("depth", C.c_int32),
+                ("extents", C.POINTER(C.c_int64)), ("rank_base", C.c_int64),
+                ("rank_stride", C.POINTER(C.c_int64)), ("ndomain", C.c_int32),
+                ("coord", C.POINTER(NestExprC)), ("lo", C.POINTER(C.c_int64)),
+                ("hi", C.POINTER(C.c_int64)), ("naccess", C.c_int32),
+                ("access", C.POINTER(LegalAccessC))]
+
+
+class LegalNestC(C.Structure):
+    _fields_ = [("num_stmts", C.c_int64), ("stmts", C.POINTER(LegalStmtC))]
+
+
+class LegalOutC(C.Structure):
+    _fields_ = [("verdict", C.c_int32), ("src_inst", C.c_int64), ("dst_inst", C.c_int64),
+                ("src_stmt", C.c_int32), ("dst_stmt", C.c_int32),
+                ("src_coord", C.c_int64 * 8), ("dst_coord", C.c_int64 * 8), ("pairs", C.c_int64)]
+
+
 class NestC(C.Structure):
     _fields_ = [("num_stmts", C.c_int64), ("stmts", C.POINTER(NestStmtC)),
                 ("out_shape", C.c_int64 * 4), ("in_shape", C.c_int64 * 4),
@@ -124,6 +149,8 @@ SIGNATURES = {
     "nb_conv_forward": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int32, C.c_int]),
     "nb_conv_dgrad": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int]),
     "nb_nest_execute": (C.c_int, [vp, P(NestC), C.c_int32, vp, vp, vp]),
+    "nb_semantic_legality": (C.c_int, [vp, P(LegalNestC), P(LegalNestC), P(LegalOutC)]),
+    "nb_ctx_device": (C.c_int, [vp]),
     "nb_forward": (C.c_int, [vp, P(NetworkC), P(WeightsC), P(BatchC), C.c_int, dp, dp, dp]),
     "nb_activation_gradients": (C.c_int, [vp, P(NetworkC), P(WeightsC), P(BatchC), C.c_int,
                                           dp, dp]),

@@ -1009,6 +1009,8 @@ nb_status nb_ctx_create(int device, nb_ctx** out) {
   });
 }
 
+int nb_ctx_device(const nb_ctx* ctx) { return ctx ? ctx->device : -1; }
+
 nb_status nb_ctx_destroy(nb_ctx* ctx) {
   return guard([&] {
     if (!ctx) return;

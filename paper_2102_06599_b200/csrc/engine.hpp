@@ -124,6 +124,7 @@ struct nb_ctx {
   cudaStream_t stream = nullptr;
   std::recursive_mutex mu;
   nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws, tilecnt, trace;
+  nb::DevBuf legal;  // semantic-legality workspace (legality.cu)
   int num_sms = 148;
   nb::PinnedBuf host_io, host_out;
   // device copies of z streams keyed by (seed, stream index)

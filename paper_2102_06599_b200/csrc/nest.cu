@@ -8,11 +8,14 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "nest_expr.cuh"
 
 namespace nb {
 namespace {
 
-constexpr int kMaxDomain = 8, kMaxRank = 4, kMaxAcc = 4, kMaxDepth = 16, kStack = 16;
+constexpr int kMaxDomain = 8, kMaxRank = 4, kMaxAcc = 4, kMaxDepth = 16;
+using nexpr::kStack;
+using nexpr::run;
 
 struct DevAccess {
   int tensor, zero_pad, rank;
@@ -27,38 +30,6 @@ struct DevStmt {
   int naccess;
   DevAccess acc[kMaxAcc];
 };
-
-__device__ __forceinline__ int64_t floor_div(int64_t a, int64_t b) {
-  int64_t q = a / b;
-  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
-  return q;
-}
-
-__device__ int64_t run(const int64_t* __restrict__ code, int off, const int64_t* vals) {
-  int64_t st[kStack];
-  int sp = 0;
-  const int64_t* c = code + 2 * off;
-  // program length is stored as the op count in the first pair: (nops, 0)
-  const int nops = int(c[0]);
-  c += 2;
-  for (int i = 0; i < nops; ++i) {
-    const int64_t op = c[2 * i], arg = c[2 * i + 1];
-    switch (op) {
-      case 0: st[sp++] = arg; break;
-      case 1: st[sp++] = vals[arg]; break;
-      case 2: {
-        int64_t s = 0;
-        for (int k = 0; k < arg; ++k) s += st[--sp];
-        st[sp++] = s;
-        break;
-      }
-      case 3: st[sp - 1] *= arg; break;
-      case 4: st[sp - 1] = floor_div(st[sp - 1], arg); break;
-      default: st[sp - 1] = st[sp - 1] - floor_div(st[sp - 1], arg) * arg; break;
-    }
-  }
-  return st[sp - 1];
-}
 
 template <typename T>
 __global__ void k_nest_exec(DevStmt s, int64_t count, const int64_t* __restrict__ code,

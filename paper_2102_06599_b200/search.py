@@ -38,7 +38,15 @@ def load() -> C.CDLL:
         lib.nbi_execute.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p,
                                     C.c_void_p]
         lib.nbi_gate_candidates.restype = C.c_int
-        lib.nbi_gate_candidates.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.nbi_gate_candidates.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        lib.nbi_legality_nests.restype = C.c_int
+        lib.nbi_legality_nests.argtypes = [C.c_char_p, C.c_char_p, C.c_longlong, C.c_int,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
+        lib.nbi_nest_json.restype = C.c_int
+        lib.nbi_nest_json.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.nbi_legality.restype = C.c_int
+        lib.nbi_legality.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_longlong, C.c_int,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
         _lib = lib
     return _lib
 
@@ -60,19 +68,71 @@ def run_search_gpu(cfg: dict, devices: str = "0", precision: int = Precision.FP3
         lib.nbi_free(p)
 
 
-def gate_candidates(cfg: dict) -> list:
-    """The host half of a search, no GPU needed: the reference's
-    draw_candidates and evaluate_candidate's gates (I/search.hpp:187-293).
-    Returns one dict per candidate: status ("fisher" = a neural candidate
-    that needs a Fisher score, else the reference's final status), reason,
-    macs, and the repaired network JSON of "fisher" candidates."""
+def gate_candidates(cfg: dict, legal_device: int = -1) -> list:
+    """The host half of a search: the reference's draw_candidates and
+    evaluate_candidate's gates (I/search.hpp:187-293).  legal_device >= 0
+    checks semantic runs on that GPU (nb_semantic_legality), -1 (no GPU
+    needed) with the reference's host check.  Returns one dict per
+    candidate: status ("fisher" = a neural candidate that needs a Fisher
+    score, else the reference's final status), reason, macs, and the
+    repaired network JSON of "fisher" candidates."""
     lib = load()
     p = C.c_void_p()
-    rc = lib.nbi_gate_candidates(json.dumps(cfg).encode(), C.byref(p))
+    rc = lib.nbi_gate_candidates(json.dumps(cfg).encode(), int(legal_device), C.byref(p))
     if rc != 0:
         raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
     try:
         return json.loads(C.cast(p, C.c_char_p).value.decode())["candidates"]
+    finally:
+        lib.nbi_free(p)
+
+
+def legality(spec, seq: str, pre: str = "", cap: int = 1_000_000, device: int = -1):
+    """check_semantic_legality (I/transforms.hpp:598-663) of the semantic run
+    `seq` applied to conv_nest(spec) rewritten by `pre`: device -1 = the
+    reference's host function, else the GPU check on that device.  Returns
+    ({"verdict", "reason"} or {"error": "CapExceeded", "what"}, elapsed ms)."""
+    lib = load()
+    p = C.c_void_p()
+    ms = C.c_double()
+    sj = spec if isinstance(spec, dict) else spec.to_json()
+    rc = lib.nbi_legality(json.dumps(sj).encode(), pre.encode(), seq.encode(), int(cap),
+                          int(device), C.byref(ms), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode()), ms.value
+    finally:
+        lib.nbi_free(p)
+
+
+def legality_nests(original: dict, transformed: dict, cap: int = 1_000_000, device: int = -1):
+    """check_semantic_legality of two explicit nests (nest JSON of
+    nbi_nest_json: {"parts": [{"spine": [[name, extent, unroll, kernel]],
+    "stmts": [...]}]}), e.g. the reference tests' hand-injected rewrites."""
+    lib = load()
+    p = C.c_void_p()
+    ms = C.c_double()
+    rc = lib.nbi_legality_nests(json.dumps(original).encode(), json.dumps(transformed).encode(),
+                                int(cap), int(device), C.byref(ms), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode()), ms.value
+    finally:
+        lib.nbi_free(p)
+
+
+def nest_json(spec, dsl: str = "") -> dict:
+    """conv_nest(spec) (I/ir.hpp:427-470) rewritten by `dsl`, as nest JSON."""
+    lib = load()
+    p = C.c_void_p()
+    sj = spec if isinstance(spec, dict) else spec.to_json()
+    rc = lib.nbi_nest_json(json.dumps(sj).encode(), dsl.encode(), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode())
     finally:
         lib.nbi_free(p)
 
