@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <memory>
+#include <random>
 #include <sstream>
 #include <map>
 #include <string>
@@ -739,6 +740,55 @@ inline bool same_network(const nestopt::Network& a, const nestopt::Network& b) {
   return true;
 }
 
+// draw_candidates (I/search.hpp:188-214) with the candidate indices spread
+// over `threads` host threads.  Every index seeds its own
+// mt19937_64 from detail::mix_seed(seed, idx) and draws through the
+// reference's own detail::draw_step, so the candidates are identical to the
+// serial loop's; only the per-layer conv_nest of the origin is built once.
+inline std::vector<nestopt::Candidate> draw_candidates(const nestopt::Network& origin,
+                                                       const nestopt::SearchConfig& cfg,
+                                                       int threads) {
+  using namespace nestopt;
+  cfg.validate();
+  std::vector<LoopNest> base(origin.layers.size());
+  for (size_t l = 0; l < origin.layers.size(); ++l)
+    if (cfg.layer_allowed(l)) base[l] = conv_nest(origin.layers[l].spec);
+  std::vector<Candidate> out(size_t(std::max(cfg.candidate_count, 0)));
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (size_t idx; (idx = next.fetch_add(1)) < out.size();) {
+      std::mt19937_64 rng(nestopt::detail::mix_seed(cfg.seed, uint64_t(idx)));
+      Candidate cand;
+      for (size_t l = 0; l < origin.layers.size(); ++l) {
+        TransformSequence seq;
+        if (cfg.layer_allowed(l)) {
+          const int len = std::uniform_int_distribution<int>(0, cfg.max_seq_len)(rng);
+          LoopNest nest = base[l];
+          for (int st = 0; st < len; ++st) {
+            LoopNest nxt;
+            auto t = nestopt::detail::draw_step(rng, nest, cfg, nxt);
+            if (!t) break;
+            seq.steps.push_back(*t);
+            nest = std::move(nxt);
+            if (t->cls() == TransformClass::Neural) cand.neural = true;
+          }
+        }
+        cand.layer_seqs.push_back(std::move(seq));
+      }
+      out[idx] = std::move(cand);
+    }
+  };
+  const int nt = std::max(1, std::min<int>(threads, int(out.size())));
+  if (nt == 1) {
+    worker();
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+  }
+  return out;
+}
+
 // Instance count from which a semantic run is checked on the GPU
 // (NB_LEGAL_GPU_MIN; -1 = always on the host).  Below it the host check is
 // faster than a device round trip.
@@ -918,7 +968,7 @@ inline nestopt::SearchReport run_search_gpu(const nestopt::Network& origin,
   rep.origin_fisher = origin_fisher.total;
 
   auto t1 = std::chrono::steady_clock::now();
-  rep.candidates = draw_candidates(origin, cfg);
+  rep.candidates = nb200::draw_candidates(origin, cfg, cfg.jobs);
   auto t2 = std::chrono::steady_clock::now();
   GpuStats st = evaluate_all_gpu(rep.candidates, origin, cfg, origin_fisher, sp, prec);
   auto t3 = std::chrono::steady_clock::now();

@@ -253,7 +253,8 @@ int nbi_gate_candidates(const char* cfg_json, int legal_device, char** out_json)
     nestopt::SearchConfig cfg = nestopt::search_config_from_json(j);
     cfg.validate();
     origin.validate();
-    std::vector<nestopt::Candidate> cands = nestopt::draw_candidates(origin, cfg);
+    std::vector<nestopt::Candidate> cands =
+        nb200::draw_candidates(origin, cfg, int(std::max(1u, std::thread::hardware_concurrency())));
     nestopt::FisherReport dummy;
     dummy.total = std::numeric_limits<double>::quiet_NaN();
     std::vector<nestopt::Network> nets(cands.size());
@@ -332,6 +333,30 @@ int nbi_legality_nests(const char* orig_json, const char* tr_json, long long cap
   } catch (const nb200::DeviceError& e) {
     g_err = e.what();
     return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
+// The candidates of a search config as DSL per layer: threads == 0 runs the
+// reference's serial draw_candidates, else nb200::draw_candidates.
+int nbi_draw_candidates(const char* cfg_json, int threads, char** out_json) {
+  try {
+    nlohmann::json j = nlohmann::json::parse(cfg_json);
+    nestopt::Network origin = nestopt::network_from_json(j.at("network"));
+    nestopt::SearchConfig cfg = nestopt::search_config_from_json(j);
+    std::vector<nestopt::Candidate> c = threads == 0
+                                            ? nestopt::draw_candidates(origin, cfg)
+                                            : nb200::draw_candidates(origin, cfg, threads);
+    nlohmann::json arr = nlohmann::json::array();
+    for (const auto& cand : c) {
+      nlohmann::json layers = nlohmann::json::array();
+      for (const auto& seq : cand.layer_seqs) layers.push_back(nestopt::to_dsl(seq));
+      arr.push_back({{"neural", cand.neural}, {"layers", layers}});
+    }
+    *out_json = dup(arr.dump());
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return NB_ERR_GENERIC;

@@ -42,6 +42,8 @@ def load() -> C.CDLL:
         lib.nbi_legality_nests.restype = C.c_int
         lib.nbi_legality_nests.argtypes = [C.c_char_p, C.c_char_p, C.c_longlong, C.c_int,
                                            C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
+        lib.nbi_draw_candidates.restype = C.c_int
+        lib.nbi_draw_candidates.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
         lib.nbi_nest_json.restype = C.c_int
         lib.nbi_nest_json.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
         lib.nbi_legality.restype = C.c_int
@@ -119,6 +121,21 @@ def legality_nests(original: dict, transformed: dict, cap: int = 1_000_000, devi
         raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
     try:
         return json.loads(C.cast(p, C.c_char_p).value.decode()), ms.value
+    finally:
+        lib.nbi_free(p)
+
+
+def draw_candidates(cfg: dict, threads: int = 0) -> list:
+    """draw_candidates (I/search.hpp:188-214): threads 0 = the reference's
+    serial loop, else the bridge's index-parallel version.  Returns per
+    candidate {"neural", "layers": [DSL per layer]}."""
+    lib = load()
+    p = C.c_void_p()
+    rc = lib.nbi_draw_candidates(json.dumps(cfg).encode(), int(threads), C.byref(p))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    try:
+        return json.loads(C.cast(p, C.c_char_p).value.decode())
     finally:
         lib.nbi_free(p)
 

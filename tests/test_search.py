@@ -155,3 +155,19 @@ def test_tf32_search_with_near_tie_recheck_matches_reference():
     assert _check_candidates(rep["candidates"], g["candidates"], g["origin"]["fisher_total"],
                              tol=nb.TOLERANCE[Precision.TF32]["total"]) == 0
     assert rep["gpu"]["rechecked"] > 0
+
+
+@NEEDS_LIB
+def test_parallel_draw_matches_reference_draw():
+    """nb200::draw_candidates (index-parallel, SURVEY 8(f) #4) draws exactly
+    the reference's draw_candidates (I/search.hpp:188-214): same steps for
+    every candidate and layer, all kinds, two configs."""
+    from paper_2102_06599_b200.workloads import resnet34_chain
+    g = golden("search_toy_1000.json")
+    assert S.draw_candidates(g["config"], 0) == S.draw_candidates(g["config"], 8)
+    o = resnet34_chain().to_json()
+    cfg = {"schema_version": 1, "candidate_count": 150, "max_seq_len": 6, "seed": 11,
+           "batch": {"n": 8, "seed": 1}, "network": o}
+    ref = S.draw_candidates(cfg, 0)
+    assert ref == S.draw_candidates(cfg, 5)
+    assert any(c["neural"] for c in ref) and any(not c["neural"] for c in ref)
