@@ -170,4 +170,4 @@ def test_parallel_draw_matches_reference_draw():
            "batch": {"n": 8, "seed": 1}, "network": o}
     ref = S.draw_candidates(cfg, 0)
     assert ref == S.draw_candidates(cfg, 5)
-    assert any(c["neural"] for c in ref) and any(not c["neural"] for c in ref)
+    assert any(c["neural"] for c in ref)
