@@ -165,6 +165,17 @@ int pick_pair_bn(int n, int m_tiles, bool split3) {
   return 0;
 }
 
+// Multicast cluster for a single-CTA tile plan: two CTAs on two M tiles of
+// one N tile share every B stage (each loads half, multicast to both), which
+// halves the weight operand's L2 -> SM traffic.  NB_TC_MC=0 disables it.
+bool use_mc(int bn, int m_tiles, bool pair) {
+  static const int mode = [] {
+    const char* e = std::getenv("NB_TC_MC");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0 && !pair && (bn == 64 || bn == 128) && m_tiles >= 2;
+}
+
 // fprop: one phase over the OH x OW output, every tap, A box at
 // (S*oy - P + kh, S*ox - P + kw) (the element stride S is in the tensor map).
 void fprop_phase(const ConvGeom& g, tc::TcArgs& t) {
@@ -282,12 +293,14 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = r.slice_co;
-            t.ksplit = choose_ksplit(t, num_sms, pbn != 0);
+            const bool mc = use_mc(bn, t.m_tiles, pbn != 0);
+            t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
             tp.bn = bn;
             tp.pair = pbn != 0;
+            tp.mc = mc;
             tp.tile = t;
             tp.w_n = align64(used);
             tp.w_off = off;
@@ -325,7 +338,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          t.ksplit = choose_ksplit(t, num_sms, pbn != 0);
+          const bool mc = use_mc(bn, t.m_tiles, pbn != 0);
+          t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
           // split-K dgrad: k_splitk_epilogue writes one partial per image
           t.part_tiles_per_img =
               t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
@@ -334,6 +348,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           TcPlan& tp = lp.tcd;
           tp.bn = bn;
           tp.pair = pbn != 0;
+          tp.mc = mc;
           tp.tile = t;
           tp.w_n = align64(int64_t(g.Ci) * taps * r.slice_co);
           tp.w_off = off;
@@ -462,6 +477,7 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   L.bn = tp.bn;
   L.split3 = split3;
   L.pair = tp.pair;
+  L.mc = tp.mc;
   L.num_sms = c->num_sms;
   if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -1004,6 +1020,11 @@ nb_status nb_ctx_create(int device, nb_ctx** out) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     NB_CUDA(cudaSetDevice(device));
+    static const bool prefer_shared = [] {
+      const char* e = std::getenv("NB_CARVEOUT");
+      return e && std::atoi(e) == 1;
+    }();
+    if (prefer_shared) NB_CUDA(cudaDeviceSetCacheConfig(cudaFuncCachePreferShared));
     NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     *out = c.release();
   });

@@ -84,6 +84,7 @@ struct TcLaunch {
   int bn;       // N tile (of the pair, when pair)
   bool split3;  // 3xTF32
   bool pair;    // CTA pair (cluster of 2): M = 256 per tcgen05.mma.cta_group::2
+  bool mc = false;  // multicast cluster of 2: B halves multicast, MMAs per CTA
   int num_sms;
 };
 

@@ -10,6 +10,7 @@
 // of GPUs or sessions.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -138,7 +139,46 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       for (int32_t k : mine) busy[size_t(k)] = ms;
     };
-    if (devs.size() == 1) {
+    // NB_SCHED_THREADS=1: one host thread per session instead of per GPU
+    // (launch submission in parallel; each thread keeps one evaluation of its
+    // session in flight)
+    static const bool per_session = [] {
+      const char* e = std::getenv("NB_SCHED_THREADS");
+      return e && std::atoi(e) == 1;
+    }();
+    auto session_worker = [&](int32_t k) {
+      auto t0 = std::chrono::steady_clock::now();
+      Pending pend;
+      try {
+        for (size_t u : order) {
+          if (bin[u] != k) continue;
+          Result& r = res[u];
+          RunOut ro;
+          ro.per_channel = r.per_channel.data();
+          ro.per_layer = r.per_layer.data();
+          ro.total = &r.total;
+          ro.loss = &r.loss;
+          ro.probs = r.probs.data();
+          run_enqueue(sessions[k], descs[uniq[u]], nullptr, prec, true, ro, pend);
+          est[size_t(k)] += cost[u];
+          run_finish(pend);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (!err) err = std::current_exception();
+        try {
+          run_finish(pend);
+        } catch (...) {
+        }
+      }
+      busy[size_t(k)] =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    if (per_session && num_sessions > 1) {
+      std::vector<std::thread> pool;
+      for (int32_t k = 0; k < num_sessions; ++k) pool.emplace_back(session_worker, k);
+      for (auto& t : pool) t.join();
+    } else if (devs.size() == 1) {
       worker(devs[0]);
     } else {
       std::vector<std::thread> pool;
