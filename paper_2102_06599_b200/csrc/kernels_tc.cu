@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
   //   3xTF32 (16 warps): physical 0-7 converters, 8-11 epilogue, 12 TMEM
   //   allocator, 13 relay, 14 TMA producer, 15 MMA;
   //   1xTF32 (8 warps): physical 5 MMA, 1 epilogue quarter 1, rest as logical.
-  const int hw = int(threadIdx.x / 32), lane = int(threadIdx.x % 32);
+  // (the warp index is shuffled from lane 0 so the compiler can prove it
+  // warp-uniform: role branches are then uniform and the MMA warp's
+  // descriptor arithmetic runs on the uniform datapath)
+  const int hw = __shfl_sync(0xffffffffu, int(threadIdx.x / 32), 0), lane = int(threadIdx.x % 32);
   const int warp = SPLIT3 ? (hw < 8 ? hw + 8 : hw < 12 ? hw - 4 : hw == 12 ? 2 : hw == 13 ? 3
                                                                  : hw == 14 ? 0 : 1)
                           : (hw == 5 ? 1 : hw == 1 ? 5 : hw);
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
     __syncthreads();
   }
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   // Programmatic dependent launch: the next kernel on the stream may start
   // its own prologue on SMs this grid leaves free; everything above (barrier
   // init, TMEM allocation, descriptor prefetch) overlapped the previous
