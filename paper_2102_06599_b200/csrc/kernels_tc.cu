@@ -135,6 +135,17 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
 }
 
+// The converter's 3xTF32 split of a finite fp32 activation: hi = x rounded
+// to tf32 (nearest, ties away -- cvt.rna.tf32.f32 without its inf/nan
+// guard, which finite activations never need), lo = x - hi exactly in fp32
+// and handed to the tensor core as is (kind::tf32 reads its top 19 bits, so
+// lo is truncated where cvt.rna would round: a 2^-22 |x| difference, below
+// the dropped lo*lo term).  3 ALU ops per value instead of ~10.
+__device__ __forceinline__ void split_tf32_fast(uint32_t x, uint32_t& hi, uint32_t& lo) {
+  hi = (x + 0x1000u) & 0xffffe000u;
+  lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));
+}
+
 // 32 consecutive TMEM columns of this thread's lane <- v[0..31]
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -759,10 +770,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
                        : "r"(row + uint32_t((c ^ (ct & 7)) << 4)));
-          split_tf32(x.x, hi[4 * c], lo[4 * c]);
-          split_tf32(x.y, hi[4 * c + 1], lo[4 * c + 1]);
-          split_tf32(x.z, hi[4 * c + 2], lo[4 * c + 2]);
-          split_tf32(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+          split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
+          split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+          split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+          split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
         }
         // (debug 256: converters store to stage 0's columns only; experiments)
         const uint32_t ta =
