@@ -470,8 +470,8 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   static int tc_launch_no = 0;
   const bool tracing = trace_at >= 0 && tc_launch_no++ == trace_at;
   if (tracing) {
-    c->trace.ensure(5 * tc::kTraceStages * 8);
-    NB_CUDA(cudaMemsetAsync(c->trace.p, 0, 5 * tc::kTraceStages * 8, st));
+    c->trace.ensure((5 * tc::kTraceStages + 4 * 1024) * 8);
+    NB_CUDA(cudaMemsetAsync(c->trace.p, 0, (5 * tc::kTraceStages + 4 * 1024) * 8, st));
     L.args.trace = c->trace.as<long long>();
   }
   L.bn = tp.bn;
@@ -484,7 +484,7 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   NB_CUDA(tc::launch(L, st));
   c->launches++;
   if (tracing) {
-    std::vector<long long> h(5 * tc::kTraceStages);
+    std::vector<long long> h(5 * tc::kTraceStages + 4 * 1024);
     NB_CUDA(cudaMemcpyAsync(h.data(), c->trace.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
     NB_CUDA(cudaStreamSynchronize(st));
     FILE* f = std::fopen("nb_tc_trace.txt", "w");
@@ -496,6 +496,15 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
                      h[2 * tc::kTraceStages + i], h[3 * tc::kTraceStages + i],
                      h[4 * tc::kTraceStages + i]);
       std::fclose(f);
+    }
+    // per CTA: entry, after the grid dependency, MMA issue done, epilogue done (ns)
+    FILE* g = std::fopen("nb_tc_ctas.txt", "w");
+    if (g) {
+      for (int i = 0; i < 1024; ++i) {
+        const long long* e = &h[5 * tc::kTraceStages + 4 * i];
+        if (e[0]) std::fprintf(g, "%d %lld %lld %lld %lld\n", i, e[0], e[1], e[2], e[3]);
+      }
+      std::fclose(g);
     }
   }
 }

@@ -289,7 +289,10 @@ struct Cfg {
                                  : (kAcc * BN) <= 32 ? 32 : (kAcc * BN) <= 64 ? 64
                                  : (kAcc * BN) <= 128 ? 128 : (kAcc * BN) <= 256 ? 256 : 512;
   static constexpr int kAcol0 = kAcc * BN;  // first TMEM column of the A stages
-  static constexpr int kRedBytes = 128 * 17 * 4;
+  // epilogue scratch: partial-sum reduction (128 x 17 floats) + a 32 x 20
+  // float transpose tile per epilogue warp (coalesced A_prev / dpre rows)
+  static constexpr int kXposeBytes = 4 * 32 * 20 * 4;
+  static constexpr int kRedBytes = 128 * 17 * 4 + kXposeBytes;
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
 };
 
@@ -365,6 +368,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
   // (the warp index is shuffled from lane 0 so the compiler can prove it
   // warp-uniform: role branches are then uniform and the MMA warp's
   // descriptor arithmetic runs on the uniform datapath)
+  if (a.trace && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[5 * kTraceStages + 4 * blockIdx.x] = t;
+  }
   const int hw = __shfl_sync(0xffffffffu, int(threadIdx.x / 32), 0), lane = int(threadIdx.x % 32);
   const int warp = SPLIT3 ? (hw < 8 ? hw + 8 : hw < 12 ? hw - 4 : hw == 12 ? 2 : hw == 13 ? 3
                                                                  : hw == 14 ? 0 : 1)
@@ -414,6 +422,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
   // kernel's tail.  Every global read and write below waits for that kernel.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // trace: per-CTA %globaltimer at start (after the grid dependency) and at
+  // the end, slots [5*kTraceStages + 4*cta + {0: launch, 1: start, 2: mma done, 3: end}]
+  if (a.trace && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[5 * kTraceStages + 4 * blockIdx.x + 1] = t;
+  }
   // the barriers the other CTA's threads signal live in the MMA CTA (rank 0)
   const uint32_t ready_remote = PAIR ? mapa(ready, 0) : 0;
   const uint32_t tempty_remote = PAIR ? mapa(tempty, 0) : 0;
@@ -598,8 +613,135 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+      // Fused dgrad epilogue of the Fisher pipeline (each warp's 32 rows in one
+      // image): the next chunk's A_prev is loaded while this one is processed,
+      // a 31-shuffle reduce-scatter leaves lane l with the warp's sum of column
+      // l of the chunk, and the image's warps are combined once per tile.
+      const bool fast_dgrad = a.mode == 1 && a.ksplit == 1 && a.partial && a.a_prev &&
+                              rows_per_img % 32 == 0 && !(a.debug & 16);
+      if (fast_dgrad) {
+        const int64_t rbase = pix * a.out_ld + col0;
+        // A_prev in / dpre out through a per-warp transpose tile: lane l moves
+        // 16 B of row 8k + l/4 (column quad l%4) -- 8 rows x 64 B per warp
+        // instruction instead of 32 rows x 16 B
+        float* xp = red + 128 * 17 + q * (32 * 20);
+        const float* aprev = a.a_prev;
+        auto row_ptr = [&](int k) {  // this lane's transposed row k: base offset, valid
+          const int src = 8 * k + (lane >> 2);
+          const long long b = __shfl_sync(0xffffffffu, (long long)rbase, src);
+          const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
+          return ok ? b + 4 * (lane & 3) : -1ll;
+        };
+        long long rp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rp[k] = row_ptr(k);
+        float4 apn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          apn[k] = rp[k] >= 0 ? *reinterpret_cast<const float4*>(aprev + rp[k])
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
-      for (int c = 0; c < ((a.debug & 16) ? 0 : BN); c += 16) {  // experiment: no epilogue
+        for (int c = 0; c < BN; c += 16) {
+          // transpose this chunk's A_prev rows into registers (own row)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3)) = apn[k];
+          __syncwarp();
+          float av[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 t = *reinterpret_cast<const float4*>(xp + lane * 20 + 4 * i);
+            av[4 * i] = t.x;
+            av[4 * i + 1] = t.y;
+            av[4 * i + 2] = t.z;
+            av[4 * i + 3] = t.w;
+          }
+          __syncwarp();
+          if (c + 16 < BN && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
+          }
+          float v[16];
+          tmem_ld16(trow + uint32_t(c), v);
+          float x[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (empty_phase) v[i] = 0.f;
+            x[i] = valid ? av[i] * v[i] : 0.f;
+          }
+          if (a.g_out && valid) {
+            float4* go = reinterpret_cast<float4*>(a.g_out + rbase + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              go[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+          if (a.dpre_out && !(a.debug & 8192)) {  // (debug 8192: no dpre stores)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4 o;
+              o.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
+              o.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
+              o.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
+              o.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+              *reinterpret_cast<float4*>(xp + lane * 20 + 4 * i) = o;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (rp[k] >= 0)
+                *reinterpret_cast<float4*>(a.dpre_out + rp[k] + c) =
+                    *reinterpret_cast<const float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3));
+            __syncwarp();
+          }
+          if (a.debug & 4096) {  // experiment: no reduction
+            if (lane < 16) red[q * BN + c + lane] = x[lane & 15];
+            continue;
+          }
+          // reduce-scatter over the warp: 16 + 8 + 4 + 2 + 1 shuffles
+#pragma unroll
+          for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
+          const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+          float y[8], z[4], w2[2];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float send = b3 ? x[i] : x[i + 8], keep = b3 ? x[i + 8] : x[i];
+            y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float send = b2 ? y[i] : y[i + 4], keep = b2 ? y[i + 4] : y[i];
+            z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const float send = b1 ? z[i] : z[i + 2], keep = b1 ? z[i + 2] : z[i];
+            w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+          {
+            const float send = b0 ? w2[0] : w2[1], keep = b0 ? w2[1] : w2[0];
+            const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            if (lane < 16) red[q * BN + c + lane] = tot;  // column c + (lane & 15)
+          }
+        }
+        named_bar(1, 128);
+        if (tile_real) {
+          const int wpi = rows_per_img / 32;
+          for (int idx = r; idx < a.BNI * BN; idx += 128) {
+            const int img = idx / BN, j = idx % BN;
+            const int nimg = nb * a.BNI + img;
+            if (nimg < a.nimg) {
+              float sum = 0.f;
+              for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red[w * BN + j];
+              a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld + col0 +
+                        j] = double(sum);
+            }
+          }
+        }
+        named_bar(1, 128);
+      }
+#pragma unroll 1
+      for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
         float v[16];
         tmem_ld16(trow + uint32_t(c), v);
         if (empty_phase) {
@@ -798,6 +940,16 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
         }
       }
     }
+  }
+  if (a.trace && warp == 1 && lane == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[5 * kTraceStages + 4 * blockIdx.x + 2] = t;  // MMA warp done issuing
+  }
+  if (a.trace && warp == 4 && lane == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[5 * kTraceStages + 4 * blockIdx.x + 3] = t;  // epilogue done
   }
   tc_fence_before();
   if (CLUSTER) {
