@@ -708,6 +708,68 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
   }
 }
 
+// k_splitk_epilogue with float4 channel quads (C, ld, c0 multiples of 4):
+// thread (tx, ty) of block (cq, n) owns channels 4*(32*cq + tx) .. +3 and the
+// pixels ty, ty + 8, ...; same fixed summation orders as the scalar kernel.
+__global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
+  __shared__ float red[8][129];
+  const int c = (blockIdx.x * 32 + threadIdx.x) * 4;
+  const int64_t n = blockIdx.y;
+  float contrib[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c < e.C) {
+    for (int p = threadIdx.y; p < e.HW; p += 8) {
+      const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < e.ksplit; ++k) {
+        const float4 w = *reinterpret_cast<const float4*>(e.ws + k * e.ws_stride + idx);
+        v.x += w.x;
+        v.y += w.y;
+        v.z += w.z;
+        v.w += w.w;
+      }
+      if (e.mode == 0) {
+        if (e.relu) {
+          v.x = v.x > 0.f ? v.x : 0.f;
+          v.y = v.y > 0.f ? v.y : 0.f;
+          v.z = v.z > 0.f ? v.z : 0.f;
+          v.w = v.w > 0.f ? v.w : 0.f;
+        }
+        *reinterpret_cast<float4*>(e.out + idx) = v;
+      } else {
+        if (e.g_out) *reinterpret_cast<float4*>(e.g_out + idx) = v;
+        if (e.a_prev) {
+          const float4 a = *reinterpret_cast<const float4*>(e.a_prev + idx);
+          contrib[0] = fmaf(a.x, v.x, contrib[0]);
+          contrib[1] = fmaf(a.y, v.y, contrib[1]);
+          contrib[2] = fmaf(a.z, v.z, contrib[2]);
+          contrib[3] = fmaf(a.w, v.w, contrib[3]);
+          if (e.dpre_out) {
+            float4 d;
+            d.x = (e.relu_prev && !(a.x > 0.f)) ? 0.f : v.x;
+            d.y = (e.relu_prev && !(a.y > 0.f)) ? 0.f : v.y;
+            d.z = (e.relu_prev && !(a.z > 0.f)) ? 0.f : v.z;
+            d.w = (e.relu_prev && !(a.w > 0.f)) ? 0.f : v.w;
+            *reinterpret_cast<float4*>(e.dpre_out + idx) = d;
+          }
+        } else if (e.dpre_out) {
+          *reinterpret_cast<float4*>(e.dpre_out + idx) = v;
+        }
+      }
+    }
+  }
+  if (e.mode == 0 || !e.partial) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) red[threadIdx.y][4 * threadIdx.x + i] = contrib[i];
+  __syncthreads();
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  if (t < 128 && blockIdx.x * 128 + t < e.C) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][t];
+    e.partial[n * e.ld + e.c0 + blockIdx.x * 128 + t] = double(s);
+  }
+}
+
 int grid_for(int64_t total, int block) {
   int64_t g = (total + block - 1) / block;
   const int64_t cap = 148 * 32;
@@ -871,6 +933,11 @@ void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbas
 }
 
 void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st) {
+  if (e.C % 4 == 0 && e.ld % 4 == 0 && e.c0 % 4 == 0) {
+    dim3 grid((e.C + 127) / 128, e.N);
+    k_splitk_epilogue4<<<grid, dim3(32, 8), 0, st>>>(e);
+    return;
+  }
   dim3 grid((e.C + 31) / 32, e.N);
   k_splitk_epilogue<<<grid, dim3(32, 8), 0, st>>>(e);
 }
