@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
   constexpr bool PAIR = CL == 1, MC = CL == 2, CLUSTER = CL != 0;
   using C = Cfg<BN, SPLIT3, PAIR>;
   // ring depth: the configured stage count, or fewer for experiments
-  const int S = (a.debug >> 4) > 0 && (a.debug >> 4) < C::kStages ? (a.debug >> 4) : C::kStages;
+  const int dcap = (a.debug >> 16) & 0xf;
+  const int S = dcap > 0 && dcap < C::kStages ? dcap : C::kStages;
   constexpr int NACC = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =

@@ -69,8 +69,11 @@ struct TcArgs {
   int relu_prev, part_tiles_per_img, part_ld;
   // experiments only (NB_TC_DEBUG; every bit but the stage cap gives
   // garbage results): 2 = no MMAs, 4 = no A loads, 8 = no B loads, 16 = no
-  // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all; bits 4.. of
-  // (debug >> 4) also cap the ring depth (0 = the configured stage count)
+  // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all, 128 / 256 =
+  // MMAs read / converters write stage 0's TMEM columns only, 512 = no TMEM
+  // stores, 1024 = no split, 2048 = no A_prev loads, 4096 = no Fisher
+  // reduction, 8192 = no dpre stores; bits 16..19 cap the ring depth
+  // (0 = the configured stage count)
   int debug;
   // experiments only (NB_TC_TRACE): CTA 0 records clock64() stamps of its
   // first kTraceStages K blocks here (see kernels_tc.cu)
