@@ -141,11 +141,39 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
       }
     }
   }
-  if (!valid) return;
-  float* yo = y + pix * g.Co + r.b + grp * r.slice_co + co0;
+  // stage the block's 128 pixels x CO_T outputs in ws (row p rotated by p so
+  // the per-thread writes are bank-conflict free), then store them with
+  // consecutive threads on consecutive 16-byte pieces of each pixel's run
+  __syncthreads();
+  if (valid) {
 #pragma unroll
-  for (int t = 0; t < CO_T; ++t)
-    if (t < nco) yo[t] = (relu && !(acc[t] > 0.f)) ? 0.f : acc[t];  // I/nnet.hpp:138-139
+    for (int t = 0; t < CO_T; ++t)
+      ws[threadIdx.x][(t + threadIdx.x) & (CO_T - 1)] =
+          (relu && !(acc[t] > 0.f)) ? 0.f : acc[t];  // I/nnet.hpp:138-139
+  }
+  __syncthreads();
+  const int64_t pix0 = int64_t(blockIdx.x) * kFpPix;
+  const int cbase = r.b + grp * r.slice_co + co0;
+  const bool vec = (cbase % 4 == 0) && (g.Co % 4 == 0) && (nco % 4 == 0);
+  if (vec) {
+    const int quads = nco / 4;
+    for (int e = threadIdx.x; e < kFpPix * quads; e += kFpPix) {
+      const int p = e / quads, qd = e - p * quads;
+      if (pix0 + p >= npix) break;
+      float4 o;
+      o.x = ws[p][(4 * qd + p) & (CO_T - 1)];
+      o.y = ws[p][(4 * qd + 1 + p) & (CO_T - 1)];
+      o.z = ws[p][(4 * qd + 2 + p) & (CO_T - 1)];
+      o.w = ws[p][(4 * qd + 3 + p) & (CO_T - 1)];
+      *reinterpret_cast<float4*>(y + (pix0 + p) * g.Co + cbase + 4 * qd) = o;
+    }
+  } else {
+    for (int e = threadIdx.x; e < kFpPix * nco; e += kFpPix) {
+      const int p = e / nco, t = e - p * nco;
+      if (pix0 + p >= npix) break;
+      y[(pix0 + p) * g.Co + cbase + t] = ws[p][(t + p) & (CO_T - 1)];
+    }
+  }
 }
 
 // Grouped / depthwise fprop with a shared-memory halo tile (ranges whose
@@ -602,10 +630,18 @@ __global__ void k_head(HeadArgs a) {
     pooled[i] = s / double(a.HW);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < a.C; ++i) s += (a.head_src[int64_t(k) * a.C + i] * a.head_scale) * pooled[i];
-    z[k] = s;
+  // logits: one warp per class, lanes stride the channels, fixed-order
+  // xor-butterfly (fp64) -- the class loop no longer runs serially
+  {
+    const int wid = threadIdx.x / 32, ln = threadIdx.x % 32, nw = blockDim.x / 32;
+    for (int k = wid; k < a.K; k += nw) {
+      double s = 0.0;
+      for (int i = ln; i < a.C; i += 32)
+        s += (a.head_src[int64_t(k) * a.C + i] * a.head_scale) * pooled[i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (ln == 0) z[k] = s;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -285,6 +285,8 @@ void run_pair(int ctas) {
 }
 
 int main() {
+  run_pair<64, true, 0>(148);
+  run_pair<64, false, 0>(148);
   run_pair<128, true, 0>(148);
   run_pair<256, true, 0>(148);
   run_pair<128, false, 0>(148);
