@@ -176,6 +176,26 @@ bool use_mc(int bn, int m_tiles, bool pair) {
   return mode != 0 && !pair && (bn == 64 || bn == 128) && m_tiles >= 2;
 }
 
+// kw-fused plan (Cfg KWF in kernels_tc.cu) for a 64-wide single-group GEMM
+// over 32-pixel rows: 3-wide, stride 1, pad 1 -- the R34 CIFAR stage-1
+// layers.  NB_TC_KWF=0 disables it.
+bool use_kwf(const ConvGeom& g, int width, int rows_w) {
+  static const int mode = [] {
+    const char* e = std::getenv("NB_TC_KWF");
+    return e ? std::atoi(e) : 1;
+  }();
+  return mode != 0 && width == 64 && g.KW == 3 && g.S == 1 && g.P == 1 && rows_w == 32 &&
+         g.W == 32 && g.OW == 32;
+}
+
+// the kh taps of a kw-fused plan: A shifted in h only, B K chunk kh
+void kwf_taps(const ConvGeom& g, tc::TcArgs& t, int sgn) {
+  t.ntaps[0] = g.KH;
+  for (int kh = 0; kh < g.KH; ++kh)
+    t.taps[0][kh] = tc::pack_tap(kh, sgn > 0 ? kh - g.P : g.P - kh, 0);
+  t.kwf_sgn = sgn;
+}
+
 // fprop: one phase over the OH x OW output, every tap, A box at
 // (S*oy - P + kh, S*ox - P + kw) (the element stride S is in the tensor map).
 void fprop_phase(const ConvGeom& g, tc::TcArgs& t) {
@@ -276,7 +296,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
-          const int pbn = pick_pair_bn(r.slice_co, t.m_tiles, P.split3);
+          const bool kwf = r.groups == 1 && use_kwf(g, r.slice_co, t.BW);
+          const int pbn = kwf ? 0 : pick_pair_bn(r.slice_co, t.m_tiles, P.split3);
           const int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
           if (bn) {
             t.mode = 0;
@@ -284,6 +305,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.n_tiles = r.groups * t.n_tiles_per_group;
             t.S = g.S;
             fprop_phase(g, t);
+            if (kwf) kwf_taps(g, t, +1);
             t.a_cblocks = r.slice_ci / 32;
             t.a_c_base = 0;
             t.a_c_per_group = r.slice_ci;
@@ -293,7 +315,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = r.slice_co;
-            const bool mc = use_mc(bn, t.m_tiles, pbn != 0);
+            const bool mc = !kwf && use_mc(bn, t.m_tiles, pbn != 0);
             t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
@@ -301,11 +323,12 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             tp.bn = bn;
             tp.pair = pbn != 0;
             tp.mc = mc;
+            tp.kwf = kwf;
             tp.tile = t;
             tp.w_n = align64(used);
             tp.w_off = off;
-            tp.b_rows = r.len;
-            tp.b_k = taps * r.slice_ci;
+            tp.b_rows = kwf ? g.KW * r.len : r.len;
+            tp.b_k = kwf ? g.KH * r.slice_ci : taps * r.slice_ci;
             off += 2 * tp.w_n;
             lp.family[i] = Family::TensorCore;
           }
@@ -320,7 +343,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
-        const int pbn = pick_pair_bn(r.slice_ci, t.m_tiles * t.nphase, P.split3);
+        const bool kwf = r.groups == 1 && use_kwf(g, r.slice_ci, t.BW);
+        const int pbn = kwf ? 0 : pick_pair_bn(r.slice_ci, t.m_tiles * t.nphase, P.split3);
         const int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
         if (bn) {
           t.mode = 1;
@@ -328,6 +352,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.n_tiles = r.groups * t.n_tiles_per_group;
           t.S = 1;
           dgrad_phases(g, t);
+          if (kwf) kwf_taps(g, t, -1);
           t.a_cblocks = r.slice_co / 32;
           t.a_c_base = r.b;
           t.a_c_per_group = r.slice_co;
@@ -338,7 +363,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          const bool mc = use_mc(bn, t.m_tiles, pbn != 0);
+          const bool mc = !kwf && use_mc(bn, t.m_tiles, pbn != 0);
           t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
           // split-K dgrad: k_splitk_epilogue writes one partial per image
           t.part_tiles_per_img =
@@ -349,11 +374,12 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           tp.bn = bn;
           tp.pair = pbn != 0;
           tp.mc = mc;
+          tp.kwf = kwf;
           tp.tile = t;
           tp.w_n = align64(int64_t(g.Ci) * taps * r.slice_co);
           tp.w_off = off;
-          tp.b_rows = g.Ci;
-          tp.b_k = taps * r.slice_co;
+          tp.b_rows = kwf ? g.KW * g.Ci : g.Ci;
+          tp.b_k = kwf ? g.KH * r.slice_co : taps * r.slice_co;
           off += 2 * tp.w_n;
           lp.dgrad_family = Family::TensorCore;
         }
@@ -424,10 +450,12 @@ std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) 
          "," + std::to_string(d.wf_off) + "," + std::to_string(d.wd_off) + "," +
          std::to_string(int(lp.family[r]));
     if (lp.family[r] == Family::TensorCore)
-      k += "," + std::to_string(lp.tcf[r].w_off) + "," + std::to_string(lp.tcf[r].w_n);
+      k += "," + std::to_string(lp.tcf[r].w_off) + "," + std::to_string(lp.tcf[r].w_n) +
+           (lp.tcf[r].kwf ? "k" : "");
   }
   if (lp.dgrad_family == Family::TensorCore)
-    k += "|d" + std::to_string(lp.tcd.w_off) + "," + std::to_string(lp.tcd.w_n);
+    k += "|d" + std::to_string(lp.tcd.w_off) + "," + std::to_string(lp.tcd.w_n) +
+         (lp.tcd.kwf ? "k" : "");
   return k;
 }
 
@@ -438,13 +466,16 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
   float* base = lp.wbase;
   for (int r = 0; r < lp.geom.nranges; ++r) {
     PackDst d{base, base, nullptr, nullptr, nullptr, nullptr};
+    d.KW = lp.geom.KW;
     if (lp.family[r] == Family::TensorCore) {
       d.tcf_hi = base + lp.tcf[r].w_off;
       d.tcf_lo = d.tcf_hi + lp.tcf[r].w_n;
+      d.kwf_f = lp.tcf[r].kwf ? 1 : 0;
     }
     if (r == 0 && lp.dgrad_family == Family::TensorCore) {
       d.tcd_hi = base + lp.tcd.w_off;
       d.tcd_lo = d.tcd_hi + lp.tcd.w_n;
+      d.kwf_d = lp.tcd.kwf ? 1 : 0;
     }
     launch_pack_weights(src, scale, lp.geom, r, d, st);
     c->launches++;
@@ -478,6 +509,14 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   L.split3 = split3;
   L.pair = tp.pair;
   L.mc = tp.mc;
+  L.kwf = tp.kwf;
+  // NB_TC_CONVH: 1 (default) = both converter groups split every stage by
+  // channel halves, 0 = groups alternate stages, 2 = halves for kw-fused only
+  static const int convh = [] {
+    const char* e = std::getenv("NB_TC_CONVH");
+    return e ? std::atoi(e) : 1;
+  }();
+  L.args.conv_halves = convh == 1 || (convh == 2 && tp.kwf) ? 1 : 0;
   L.num_sms = c->num_sms;
   if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");

@@ -47,6 +47,7 @@ struct TcPlan {
   int bn = 0;
   bool pair = false;   // CTA-pair (cta_group::2) launch, bn = the pair's N tile
   bool mc = false;     // multicast cluster of 2 (B stage shared, cta_group::1 MMAs)
+  bool kwf = false;    // kw-fused 64-channel plan (B rows kw*64 + c, K = kh x channels)
   tc::TcArgs tile{};   // M/N tiling and operand bases (pointers filled at launch)
   int64_t w_off = 0;   // hi at w_off, lo at w_off + w_n (floats, layer-relative)
   int64_t w_n = 0;

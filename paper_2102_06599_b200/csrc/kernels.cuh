@@ -56,6 +56,8 @@ struct PackDst {
   float* tcf_lo;
   float* tcd_hi;
   float* tcd_lo;
+  // kw-fused tensor-core layouts (rows kw*width + c, K = kh x channels)
+  int kwf_f = 0, kwf_d = 0, KW = 1;
 };
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
                          const PackDst& d, cudaStream_t st);

@@ -71,13 +71,16 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     uint32_t hb, lb;
     split_tf32(__float_as_uint(v), hb, lb);
     const float hi = __uint_as_float(hb), lo = __uint_as_float(lb);
+    const int kh = tap / d.KW, kw = tap - kh * d.KW, KH = taps / d.KW;
     if (d.tcf_hi) {
-      const int64_t i = (int64_t(co_local) * taps + tap) * r.slice_ci + j;
+      const int64_t i = d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
+                                : (int64_t(co_local) * taps + tap) * r.slice_ci + j;
       d.tcf_hi[i] = hi;
       d.tcf_lo[i] = lo;
     }
     if (d.tcd_hi) {
-      const int64_t i = (int64_t(ci) * taps + tap) * r.slice_co + t;
+      const int64_t i = d.kwf_d ? ((int64_t(kw) * Ci + ci) * KH + kh) * r.slice_co + t
+                                : (int64_t(ci) * taps + tap) * r.slice_co + t;
       d.tcd_hi[i] = hi;
       d.tcd_lo[i] = lo;
     }

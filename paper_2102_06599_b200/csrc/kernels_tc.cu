@@ -146,6 +146,17 @@ __device__ __forceinline__ void split_tf32_fast(uint32_t x, uint32_t& hi, uint32
   lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));
 }
 
+// 16 consecutive TMEM columns of this thread's lane <- v[0..15]
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+
 // 32 consecutive TMEM columns of this thread's lane <- v[0..31]
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -271,24 +282,31 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
 // Kernel configuration.  PAIR = a CTA pair (cluster of 2) runs one
 // M=256 x N=BN MMA (tcgen05 cta_group::2): each CTA stages its own 128 A
 // rows and BN/2 of the B rows, and the pair's tensor cores share both.
-template <int BN, bool SPLIT3, bool PAIR>
+// KWF (kw-fused, 64-channel 3-wide stride-1 layers): the MMA's N holds the
+// three kw taps side by side (N = 3*BN: column kw*BN + c), K runs over
+// (kh, channel) only, and the epilogue adds D_kw of the pixel kw - P to the
+// left/right (one warp = one 32-pixel image row, so the neighbour is a lane
+// shuffle).  Same MACs; N=192 runs at the full tcgen05 rate where N=64 hits
+// the ~46-cycle instruction floor.
+template <int BN, bool SPLIT3, bool PAIR, bool KWF = false>
 struct Cfg {
-  static constexpr int kBRows = PAIR ? BN / 2 : BN;  // B rows staged per CTA
+  static constexpr int kNM = KWF ? 3 * BN : BN;      // MMA N / accumulator columns
+  static constexpr int kBRows = PAIR ? kNM / 2 : kNM;  // B rows staged per CTA
   static constexpr int kBBytes = kBRows * 128;
   // accumulator buffers: two (epilogue overlaps the next tile) unless the
   // 3xTF32 A stages would not fit next to them in TMEM
-  static constexpr int kAcc = (SPLIT3 && BN >= 256) ? 1 : 2;
+  static constexpr int kAcc = (SPLIT3 && kNM >= 256) ? 1 : 2;
   // smem stage: [A fp32 (TMA) | B_hi | B_lo?]; in 3xTF32 the split A halves
   // live in TMEM (64 columns per stage, after the accumulators)
   static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
   static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
-  static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * BN) / 64 : 99;
+  static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * kNM) / 64 : 99;
   static constexpr int kStages = kSmemStages < kTmemStages ? kSmemStages : kTmemStages;
   static constexpr int kThreads = SPLIT3 ? 512 : 256;  // 3xTF32: two converter groups
   static constexpr int kTmemCols = SPLIT3 ? 512
-                                 : (kAcc * BN) <= 32 ? 32 : (kAcc * BN) <= 64 ? 64
-                                 : (kAcc * BN) <= 128 ? 128 : (kAcc * BN) <= 256 ? 256 : 512;
-  static constexpr int kAcol0 = kAcc * BN;  // first TMEM column of the A stages
+                                 : (kAcc * kNM) <= 32 ? 32 : (kAcc * kNM) <= 64 ? 64
+                                 : (kAcc * kNM) <= 128 ? 128 : (kAcc * kNM) <= 256 ? 256 : 512;
+  static constexpr int kAcol0 = kAcc * kNM;  // first TMEM column of the A stages
   // epilogue scratch: partial-sum reduction (128 x 17 floats) + a 32 x 20
   // float transpose tile per epilogue warp (coalesced A_prev / dpre rows)
   static constexpr int kXposeBytes = 4 * 32 * 20 * 4;
@@ -331,12 +349,13 @@ __device__ __forceinline__ Tile decode(const TcArgs& a, int u, int rank) {
 // 2 = multicast cluster (MC): two CTAs on two M tiles of the same N tile,
 // each TMA-loading half of the B stage multicast into both, so the weight
 // operand crosses L2 -> SM once per cluster; MMAs stay cta_group::1.
-template <int BN, bool SPLIT3, int CL>
-__global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
+template <int BN, bool SPLIT3, int CL, bool KWF = false>
+__global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
               const __grid_constant__ CUtensorMap mapBl, const TcArgs a) {
   constexpr bool PAIR = CL == 1, MC = CL == 2, CLUSTER = CL != 0;
-  using C = Cfg<BN, SPLIT3, PAIR>;
+  using C = Cfg<BN, SPLIT3, PAIR, KWF>;
+  constexpr int NM = C::kNM;
   // ring depth: the configured stage count, or fewer for experiments
   const int dcap = (a.debug >> 16) & 0xf;
   const int S = dcap > 0 && dcap < C::kStages ? dcap : C::kStages;
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], kCtas);
+      mbar_init(&ready[s], kCtas * (a.conv_halves ? 2 : 1));
       mbar_init(&empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs read the stage's B
     }
     for (int i = 0; i < 2; ++i) {
@@ -487,7 +506,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
       // The whole warp runs the loop (descriptors stay warp-uniform, in
       // uniform registers); each tcgen05.mma / commit is issued by one
       // elect.sync-chosen lane inside its asm block.
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NM >> 3) << 17) |
                                  (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
       int stage = 0, mit = 0;
       uint32_t phase = 0;
@@ -503,7 +522,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
           mbar_wait(&tempty[acc], aphase ^ 1);
         }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * NM);
         for (int kb = 0; kb < kblocks; ++kb) {
           if (PAIR) {
             mbar_wait_cluster(&ready[stage], phase);
@@ -613,7 +632,30 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
       const bool tile_real = m < a.m_tiles;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+      const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * NM);
+      // accumulator chunk [c, c+16) of the layer's output channels; KWF adds
+      // the kw = 0 / 2 column blocks of the pixels kwf_sgn*(kw - 1) away
+      auto acc_ld16 = [&](int c, float* v) {
+        if (!KWF) {
+          tmem_ld16(trow + uint32_t(c), v);
+        } else {
+          float l[16], rr[16];
+          tmem_ld16(trow + uint32_t(c), l);
+          tmem_ld16(trow + uint32_t(BN + c), v);
+          tmem_ld16(trow + uint32_t(2 * BN + c), rr);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            // fprop (sgn +1): out(w) += D0(w-1) + D2(w+1); dgrad (-1): D0(w+1) + D2(w-1)
+            const float up0 = __shfl_up_sync(0xffffffffu, l[i], 1);
+            const float dn0 = __shfl_down_sync(0xffffffffu, l[i], 1);
+            const float up2 = __shfl_up_sync(0xffffffffu, rr[i], 1);
+            const float dn2 = __shfl_down_sync(0xffffffffu, rr[i], 1);
+            const float from_left = a.kwf_sgn > 0 ? up0 : up2;   // D(w-1) term
+            const float from_right = a.kwf_sgn > 0 ? dn2 : dn0;  // D(w+1) term
+            v[i] += (lane > 0 ? from_left : 0.f) + (lane < 31 ? from_right : 0.f);
+          }
+        }
+      };
       // Fused dgrad epilogue of the Fisher pipeline (each warp's 32 rows in one
       // image): the next chunk's A_prev is loaded while this one is processed,
       // a 31-shuffle reduce-scatter leaves lane l with the warp's sum of column
@@ -664,7 +706,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
               if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
           }
           float v[16];
-          tmem_ld16(trow + uint32_t(c), v);
+          acc_ld16(c, v);
           float x[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -744,7 +786,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
         float v[16];
-        tmem_ld16(trow + uint32_t(c), v);
+        acc_ld16(c, v);
         if (empty_phase) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -888,7 +930,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
     for (int u = unit0; u < num_units; u += ustep) {
       const Tile d = decode<CLUSTER>(a, u, int(rank));
       for (int kb = d.kb0; kb < d.kb1; ++kb, ++it) {
-        if ((it & 1) != cg) continue;
+        // conv_halves: both groups convert every stage, group cg channels
+        // [16cg, 16cg+16) -- half the per-stage latency; else alternate stages
+        if (!a.conv_halves && (it & 1) != cg) continue;
         const int stage = it % S;
         const uint32_t phase = uint32_t(it / S) & 1u;
         mbar_wait(&full[stage], phase);
@@ -902,6 +946,35 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1>::kThreads, 1)
           continue;
         }
         const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
+        if (a.conv_halves) {
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 x;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                         : "r"(row + uint32_t(((4 * cg + c) ^ (ct & 7)) << 4)));
+            split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
+            split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+            split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+            split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+          }
+          const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + stage * 64 + 16 * cg);
+          tmem_st16(ta, hi);
+          tmem_st16(ta + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          named_bar(2 + cg, 128);
+          if (ct == 0) trace(a, 2, it);
+          if (ct == 0) {
+            if (PAIR) {
+              mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+            } else {
+              mbar_arrive(&ready[stage]);
+            }
+          }
+          continue;
+        }
         uint32_t hi[32], lo[32];
         if (a.debug & 1024) {  // experiment: no smem reads / splits (store garbage)
 #pragma unroll
@@ -1007,12 +1080,12 @@ bool make_map_2d(CUtensorMap* m, const float* base, int K, int rows, int box_row
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool SPLIT3, int CL>
+template <int BN, bool SPLIT3, int CL, bool KWF = false>
 cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
-  using C = Cfg<BN, SPLIT3, CL == 1>;
+  using C = Cfg<BN, SPLIT3, CL == 1, KWF>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3, CL>,
+    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3, CL, KWF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -1036,7 +1109,7 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = CL ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL>, L.mapA, L.mapBh, L.mapBl, a);
+  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL, KWF>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
 }  // namespace
@@ -1063,13 +1136,17 @@ bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, cons
   const TcArgs& a = L.args;
   if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
   // a pair stages half of B per CTA; a multicast cluster loads half per CTA
-  const int box_rows = (L.pair || L.mc) ? L.bn / 2 : L.bn;
+  const int box_rows = L.kwf ? 3 * L.bn : (L.pair || L.mc) ? L.bn / 2 : L.bn;
   if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, box_rows)) return false;
   if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, box_rows)) return false;
   return true;
 }
 
 cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
+  if (L.kwf) {
+    if (L.bn != 64 || L.pair || L.mc) return cudaErrorInvalidValue;
+    return L.split3 ? launch_t<64, true, 0, true>(L, st) : launch_t<64, false, 0, true>(L, st);
+  }
   if (L.pair) {
     if (L.split3) {
       switch (L.bn) {

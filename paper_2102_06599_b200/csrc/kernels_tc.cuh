@@ -67,6 +67,11 @@ struct TcArgs {
   float* g_out;
   double* partial;
   int relu_prev, part_tiles_per_img, part_ld;
+  // kw-fused plan (KWF): +1 fprop, -1 dgrad, 0 off -- see Cfg in kernels_tc.cu
+  int kwf_sgn;
+  // 3xTF32 converters: both groups split every stage (channel halves) rather
+  // than alternating stages (lower per-stage latency for shallow rings)
+  int conv_halves;
   // experiments only (NB_TC_DEBUG; every bit but the stage cap gives
   // garbage results): 2 = no MMAs, 4 = no A loads, 8 = no B loads, 16 = no
   // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all, 128 / 256 =
@@ -88,6 +93,7 @@ struct TcLaunch {
   bool split3;  // 3xTF32
   bool pair;    // CTA pair (cluster of 2): M = 256 per tcgen05.mma.cta_group::2
   bool mc = false;  // multicast cluster of 2: B halves multicast, MMAs per CTA
+  bool kwf = false;  // kw-fused 64-channel plan (MMA N = 192)
   int num_sms;
 };
 
