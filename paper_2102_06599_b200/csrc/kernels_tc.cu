@@ -301,7 +301,12 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
   static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
   static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * kNM) / 64 : 99;
-  static constexpr int kStages = kSmemStages < kTmemStages ? kSmemStages : kTmemStages;
+  // the shared-memory ring (TMA stages) and, in 3xTF32, the TMEM ring of
+  // split A stages are separate: a stage's TMEM slot is reused as soon as
+  // its MMAs completed, so a wide accumulator (kw-fused N=192) that leaves
+  // room for only two A slots still gets a three-deep TMA ring
+  static constexpr int kStages = kSmemStages;
+  static constexpr int kTStages = kTmemStages < kSmemStages ? kTmemStages : kSmemStages;
   static constexpr int kThreads = SPLIT3 ? 512 : 256;  // 3xTF32: two converter groups
   static constexpr int kTmemCols = SPLIT3 ? 512
                                  : (kAcc * kNM) <= 32 ? 32 : (kAcc * kNM) <= 64 ? 64
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   // ring depth: the configured stage count, or fewer for experiments
   const int dcap = (a.debug >> 16) & 0xf;
   const int S = dcap > 0 && dcap < C::kStages ? dcap : C::kStages;
+  const int ST = SPLIT3 ? (S < C::kTStages ? S : C::kTStages) : S;  // TMEM A slots
   constexpr int NACC = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =
@@ -370,12 +376,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   float* red = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kRedBytes);
   uint64_t* full = bars;            // S: this CTA's TMA bytes landed
-  uint64_t* ready = bars + S;       // S: stage ready for the MMA (split A in TMEM /
-                                    //    both CTAs' data landed) -- MMA CTA's copy
-  uint64_t* empty = bars + 2 * S;   // S: the MMAs reading the stage are done
-  uint64_t* tfull = bars + 3 * S;   // 2: accumulator complete
-  uint64_t* tempty = bars + 3 * S + 2;  // 2: accumulator drained (MMA CTA's copy)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* ready = bars + S;       // ST: TMEM A slot ready for the MMA (split A in TMEM /
+                                    //     both CTAs' data landed) -- MMA CTA's copy
+  uint64_t* empty = bars + S + ST;  // S: the MMAs reading the smem stage are done
+  uint64_t* tfull = bars + 2 * S + ST;       // 2: accumulator complete
+  uint64_t* tempty = bars + 2 * S + ST + 2;  // 2: accumulator drained (MMA CTA's copy)
+  uint64_t* tfree = bars + 2 * S + ST + 4;   // ST: the MMAs reading the TMEM A slot are done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * ST + 4);
 
   // Role of each warp.  An SM sub-partition issues from its eligible warps
   // highest-warp-id first, so the single MMA-issuing thread sits in the
@@ -400,9 +407,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   const uint32_t rank = CLUSTER ? cluster_rank() : 0;
   constexpr int kCtas = PAIR ? 2 : 1;
   if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&ready[s], kCtas * (a.conv_halves ? 2 : 1));
+      mbar_init(&tfree[s], 1);
+    }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], kCtas * (a.conv_halves ? 2 : 1));
       mbar_init(&empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs read the stage's B
     }
     for (int i = 0; i < 2; ++i) {
@@ -485,7 +495,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
           if (MC) {
             // this CTA's half of the B rows, into both CTAs' stage buffers
-            const int half = int(rank) * (BN / 2);
+            const int half = int(rank) * (NM / 2);
             if (ld_b) tma_load_2d_mc(b_hi(stage) + half * 128, &mapBh, &full[stage], kcoord, row + half, 3);
             if (SPLIT3 && ld_b)
               tma_load_2d_mc(b_lo(stage) + half * 128, &mapBl, &full[stage], kcoord, row + half, 3);
@@ -508,8 +518,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       // elect.sync-chosen lane inside its asm block.
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NM >> 3) << 17) |
                                  (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
-      int stage = 0, mit = 0;
-      uint32_t phase = 0;
+      int stage = 0, mit = 0, tslot = 0;
+      uint32_t phase = 0, tph = 0;
       int local = 0;
       for (int u = unit0; u < num_units; u += ustep, ++local) {
         const Tile d = decode<CLUSTER>(a, u, 0);
@@ -525,9 +535,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         const uint32_t d_tmem = tmem_base + uint32_t(acc * NM);
         for (int kb = 0; kb < kblocks; ++kb) {
           if (PAIR) {
-            mbar_wait_cluster(&ready[stage], phase);
+            mbar_wait_cluster(SPLIT3 ? &ready[tslot] : &ready[stage], SPLIT3 ? tph : phase);
+          } else if (SPLIT3) {
+            mbar_wait(&ready[tslot], tph);
           } else {
-            mbar_wait(SPLIT3 ? &ready[stage] : &full[stage], phase);
+            mbar_wait(&full[stage], phase);
           }
           trace(a, 3, mit);
           tc_fence_after();
@@ -539,7 +551,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
             // (debug 128: every stage's MMAs read stage 0's columns -- no
             // dependency on the columns just converted; experiments)
             const uint32_t a_t =
-                tmem_base + uint32_t(C::kAcol0 + ((a.debug & 128) ? 0 : stage) * 64);
+                tmem_base + uint32_t(C::kAcol0 + ((a.debug & 128) ? 0 : tslot) * 64);
             const uint64_t dbl = sw128_desc(smem_u32(b_lo(stage)));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -570,15 +582,22 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           }
           if (PAIR) {
             mma2_commit_both(&empty[stage]);
+            if (SPLIT3) mma2_commit_both(&tfree[tslot]);
           } else if (MC) {
             mma_commit_mc(&empty[stage]);
+            if (SPLIT3) mma_commit(&tfree[tslot]);
           } else {
             mma_commit(&empty[stage]);
+            if (SPLIT3) mma_commit(&tfree[tslot]);
           }
           trace(a, 4, mit++);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
+          }
+          if (++tslot == ST) {
+            tslot = 0;
+            tph ^= 1;
           }
         }
         // with no taps (empty phase) this arrives at once
@@ -935,13 +954,20 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         if (!a.conv_halves && (it & 1) != cg) continue;
         const int stage = it % S;
         const uint32_t phase = uint32_t(it / S) & 1u;
+        const int tslot = it % ST;
+        const uint32_t tph = uint32_t(it / ST) & 1u;
         mbar_wait(&full[stage], phase);
+        if (PAIR) {
+          mbar_wait_cluster(&tfree[tslot], tph ^ 1);  // the slot's previous MMAs are done
+        } else {
+          mbar_wait(&tfree[tslot], tph ^ 1);
+        }
         trace(a, 1, it);
         if (a.debug & 32) {  // experiment: no conversion work
           named_bar(2 + cg, 128);
           if (ct == 0) {
-            if (PAIR) mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
-            else mbar_arrive(&ready[stage]);
+            if (PAIR) mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
+            else mbar_arrive(&ready[tslot]);
           }
           continue;
         }
@@ -959,7 +985,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
             split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
             split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
           }
-          const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + stage * 64 + 16 * cg);
+          const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + tslot * 64 + 16 * cg);
           tmem_st16(ta, hi);
           tmem_st16(ta + 32, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -968,9 +994,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           if (ct == 0) trace(a, 2, it);
           if (ct == 0) {
             if (PAIR) {
-              mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+              mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
             } else {
-              mbar_arrive(&ready[stage]);
+              mbar_arrive(&ready[tslot]);
             }
           }
           continue;
@@ -993,7 +1019,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         }
         // (debug 256: converters store to stage 0's columns only; experiments)
         const uint32_t ta =
-            tmem_base + lane_base + uint32_t(C::kAcol0 + ((a.debug & 256) ? 0 : stage) * 64);
+            tmem_base + lane_base + uint32_t(C::kAcol0 + ((a.debug & 256) ? 0 : tslot) * 64);
         if (a.debug & 512) {  // experiment: no TMEM stores
           asm volatile("" ::"r"(hi[0] ^ lo[31] ^ hi[17] ^ lo[5]));
         } else {
@@ -1007,9 +1033,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         if (ct == 0) trace(a, 2, it);
         if (ct == 0) {
           if (PAIR) {
-            mbar_arrive_remote(ready_remote + uint32_t(stage * 8));
+            mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
           } else {
-            mbar_arrive(&ready[stage]);
+            mbar_arrive(&ready[tslot]);
           }
         }
       }
@@ -1136,7 +1162,8 @@ bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, cons
   const TcArgs& a = L.args;
   if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
   // a pair stages half of B per CTA; a multicast cluster loads half per CTA
-  const int box_rows = L.kwf ? 3 * L.bn : (L.pair || L.mc) ? L.bn / 2 : L.bn;
+  const int nm = L.kwf ? 3 * L.bn : L.bn;  // MMA N (B rows of a stage)
+  const int box_rows = (L.pair || L.mc) ? nm / 2 : nm;
   if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, box_rows)) return false;
   if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, box_rows)) return false;
   return true;
@@ -1144,7 +1171,9 @@ bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, cons
 
 cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
   if (L.kwf) {
-    if (L.bn != 64 || L.pair || L.mc) return cudaErrorInvalidValue;
+    if (L.bn != 64 || L.pair) return cudaErrorInvalidValue;
+    if (L.mc)
+      return L.split3 ? launch_t<64, true, 2, true>(L, st) : launch_t<64, false, 2, true>(L, st);
     return L.split3 ? launch_t<64, true, 0, true>(L, st) : launch_t<64, false, 0, true>(L, st);
   }
   if (L.pair) {
