@@ -201,6 +201,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld of 16 columns without the wait (the caller waits once for
+// several loads with tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -658,20 +673,21 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         if (!KWF) {
           tmem_ld16(trow + uint32_t(c), v);
         } else {
-          float l[16], rr[16];
-          tmem_ld16(trow + uint32_t(c), l);
-          tmem_ld16(trow + uint32_t(BN + c), v);
-          tmem_ld16(trow + uint32_t(2 * BN + c), rr);
+          uint32_t l[16], m[16], rr[16];
+          tmem_ld16_nw(trow + uint32_t(c), l);
+          tmem_ld16_nw(trow + uint32_t(BN + c), m);
+          tmem_ld16_nw(trow + uint32_t(2 * BN + c), rr);
+          tmem_wait_ld();
+          // fprop (sgn +1): out(w) = D0(w-1) + D1(w) + D2(w+1); dgrad: D0(w+1) + D1(w) + D2(w-1)
+          const bool fwd = a.kwf_sgn > 0;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            // fprop (sgn +1): out(w) += D0(w-1) + D2(w+1); dgrad (-1): D0(w+1) + D2(w-1)
-            const float up0 = __shfl_up_sync(0xffffffffu, l[i], 1);
-            const float dn0 = __shfl_down_sync(0xffffffffu, l[i], 1);
-            const float up2 = __shfl_up_sync(0xffffffffu, rr[i], 1);
-            const float dn2 = __shfl_down_sync(0xffffffffu, rr[i], 1);
-            const float from_left = a.kwf_sgn > 0 ? up0 : up2;   // D(w-1) term
-            const float from_right = a.kwf_sgn > 0 ? dn2 : dn0;  // D(w+1) term
-            v[i] += (lane > 0 ? from_left : 0.f) + (lane < 31 ? from_right : 0.f);
+            const float left_src = __uint_as_float(fwd ? l[i] : rr[i]);
+            const float right_src = __uint_as_float(fwd ? rr[i] : l[i]);
+            const float from_left = __shfl_up_sync(0xffffffffu, left_src, 1);
+            const float from_right = __shfl_down_sync(0xffffffffu, right_src, 1);
+            v[i] = __uint_as_float(m[i]) + (lane > 0 ? from_left : 0.f) +
+                   (lane < 31 ? from_right : 0.f);
           }
         }
       };
