@@ -256,6 +256,9 @@ TC_SPECS = [
     ConvSpec(64, 64, 9, 9, 3, 3, 2, 1),                        # stride 2, odd input
     ConvSpec(32, 64, 16, 16, 3, 3, 2, 1, spatial_div_h=2),     # stride 2 + crop
     ConvSpec(64, 64, 8, 8, 1, 1, 2, 0),                        # 1x1 s2: empty dgrad phases
+    ConvSpec(64, 64, 32, 32, 3, 3, 1, 1),                      # kw-fused fprop + dgrad (N=192)
+    ConvSpec(128, 64, 32, 32, 3, 3, 1, 1),                     # kw-fused fprop, K = 3 x 128
+    ConvSpec(64, 64, 12, 32, 3, 3, 1, 1, spatial_div_h=2),     # kw-fused, short rows + crop
 ]
 
 
