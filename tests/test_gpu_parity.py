@@ -339,3 +339,27 @@ def test_tc_chain_gradients_match_oracle(ctx, oracle):
         np.testing.assert_allclose(a.ravel(), ra, rtol=0, atol=1e-4 * np.abs(ra).max())
         np.testing.assert_allclose(g.ravel(), rg, rtol=0, atol=1e-3 * np.abs(rg).max())
         off += k
+
+
+STEM_SPECS = [
+    ConvSpec(3, 64, 32, 32, 3, 3, 1, 1),     # the R34 stem (k_fprop_blocked<64>)
+    ConvSpec(4, 64, 9, 9, 3, 3, 2, 1),       # stride 2, partial last block
+    ConvSpec(14, 64, 5, 5, 3, 3, 1, 1),      # K = 126 <= 128
+    ConvSpec(3, 64, 7, 7, 3, 3, 1, 1, spatial_div_h=7),  # crop
+]
+
+
+@pytest.mark.parametrize("prec", [Precision.FP32, Precision.SIMT])
+@pytest.mark.parametrize("spec", STEM_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}")
+def test_stem_fprop_integer_exact(ctx, oracle, spec, prec):
+    """The direct fprop of stem-shaped layers (k_fprop_blocked, outputs staged
+    through shared memory) against reference_conv<int64>, small integers so
+    fp32 sums are exact."""
+    rng = np.random.default_rng(spec.ci * 3 + spec.h)
+    n = 3
+    x = rng.integers(-3, 4, size=(n, spec.ci, spec.h, spec.w)).astype(np.float64)
+    w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(np.float64)
+    y = nb.reference_conv(spec, x, w, precision=prec, ctx=ctx)
+    for i in range(n):
+        want = oracle.conv(spec, x[i].astype(np.int64), w.astype(np.int64))
+        assert np.array_equal(y[i], want.astype(np.float64)), i
