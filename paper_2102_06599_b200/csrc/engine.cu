@@ -132,6 +132,11 @@ int pick_bn(int n_per_group, bool split3) {
 // one wave of SMs, divide the K blocks (taps x 32-channel chunks, at least 4
 // per split) so that tiles x splits still fits in one wave.
 int choose_ksplit(const tc::TcArgs& t, int num_sms, bool pair) {
+  static const int mode = [] {  // NB_TC_KSPLIT=0: never split K (experiments)
+    const char* e = std::getenv("NB_TC_KSPLIT");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!mode) return 1;
   const int tiles = t.nphase * (pair ? (t.m_tiles + 1) / 2 : t.m_tiles) * t.n_tiles;
   if (pair) num_sms /= 2;
   int mink = 1 << 30;
