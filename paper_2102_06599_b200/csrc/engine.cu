@@ -469,7 +469,10 @@ std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) 
   return k;
 }
 
-constexpr size_t kWCacheCap = size_t(2) << 30;  // packed-weight slab bytes per context
+// packed-weight slab bytes per context: a search's distinct layers of one
+// pool stay resident (a full slab is reset between runs, repacking every
+// layer of the next candidates), at a few GB of the 180 GB per GPU
+constexpr size_t kWCacheCap = size_t(6) << 30;
 
 void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
                 cudaStream_t st) {
