@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
 #pragma unroll
   for (int t = 0; t < CO_T; ++t) acc[t] = 0.f;
   const int K = r.slice_ci * g.KH * g.KW;
+  // float4 input path: a tap's slice_ci channels are contiguous and aligned,
+  // and K chunks hold whole taps (summation order per output unchanged)
+  const bool vec4 = r.slice_ci % 4 == 0 && kFpKChunk % r.slice_ci == 0 && g.Ci % 4 == 0;
   for (int k0 = 0; k0 < K; k0 += kFpKChunk) {
     const int kn = min(kFpKChunk, K - k0);
     __syncthreads();
@@ -130,7 +133,29 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
       ws[kk][t] = t < nco ? wf[int64_t(k0 + kk) * r.len + grp * r.slice_co + co0 + t] : 0.f;
     }
     __syncthreads();
-    if (valid) {
+    if (valid && vec4) {
+      // whole taps of the chunk, the tap's slice_ci inputs as float4s
+      for (int kk = 0; kk < kn; kk += r.slice_ci) {
+        const int tap = (k0 + kk) / r.slice_ci;
+        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+        const int ih = g.S * oh - g.P + kh, iw = g.S * ow - g.P + kw;
+        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
+        const float4* xp = reinterpret_cast<const float4*>(
+            x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci);
+        for (int j4 = 0; j4 < r.slice_ci / 4; ++j4) {
+          const float4 xv = __ldg(xp + j4);
+          const int b = kk + 4 * j4;
+#pragma unroll
+          for (int t = 0; t < CO_T; ++t) {
+            float a = acc[t];
+            a = fmaf(xv.x, ws[b][t], a);
+            a = fmaf(xv.y, ws[b + 1][t], a);
+            a = fmaf(xv.z, ws[b + 2][t], a);
+            acc[t] = fmaf(xv.w, ws[b + 3][t], a);
+          }
+        }
+      }
+    } else if (valid) {
       for (int kk = 0; kk < kn; ++kk) {
         const int k = k0 + kk;
         const int tap = k / r.slice_ci, j = k - tap * r.slice_ci;

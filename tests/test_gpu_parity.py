@@ -346,6 +346,9 @@ STEM_SPECS = [
     ConvSpec(4, 64, 9, 9, 3, 3, 2, 1),       # stride 2, partial last block
     ConvSpec(14, 64, 5, 5, 3, 3, 1, 1),      # K = 126 <= 128
     ConvSpec(3, 64, 7, 7, 3, 3, 1, 1, spatial_div_h=7),  # crop
+    ConvSpec(64, 128, 16, 16, 3, 3, 2, 1, groups=8),     # grouped s2, slice_ci 8 (float4 path)
+    ConvSpec(96, 96, 6, 6, 3, 3, 2, 1, groups=12),       # grouped s2, slice 8
+    ConvSpec(36, 72, 5, 5, 3, 3, 2, 1, groups=3),        # slice_ci 12 (float4, K = 108)
 ]
 
 
