@@ -331,7 +331,7 @@ struct Cfg {
   // float transpose tile per epilogue warp (coalesced A_prev / dpre rows)
   static constexpr int kXposeBytes = 4 * 32 * 20 * 4;
   static constexpr int kRedBytes = 128 * 17 * 4 + kXposeBytes;
-  static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 256;
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 512;
 };
 
 // Trace slots (CTA 0, first kTraceStages K blocks): [role][it]
@@ -397,7 +397,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   uint64_t* tfull = bars + 2 * S + ST;       // 2: accumulator complete
   uint64_t* tempty = bars + 2 * S + ST + 2;  // 2: accumulator drained (MMA CTA's copy)
   uint64_t* tfree = bars + 2 * S + ST + 4;   // ST: the MMAs reading the TMEM A slot are done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * ST + 4);
+  // 3xTF32 single-CTA: the A box lands on its own barrier, so the
+  // converters start while the (3x larger) B stage is still in flight;
+  // `full` then covers B only
+  uint64_t* fulla = bars + 2 * S + 2 * ST + 4;  // S
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2 * ST + 4);
+  constexpr bool kSplitA = SPLIT3 && !PAIR;
 
   // Role of each warp.  An SM sub-partition issues from its eligible warps
   // highest-warp-id first, so the single MMA-issuing thread sits in the
@@ -428,6 +433,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
     }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&fulla[s], 1);
       mbar_init(&empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs read the stage's B
     }
     for (int i = 0; i < 2; ++i) {
@@ -504,9 +510,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           trace(a, 0, pit++);
           const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
-          mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
-                                           (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
-          if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+          if (kSplitA) {
+            mbar_expect_tx(&fulla[stage], ld_a ? a_box_bytes : 0u);
+            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &fulla[stage], c_base + cb * 32, aw, ah, n0);
+            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
+          } else {
+            mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
+                                             (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
+            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+          }
           const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
           if (MC) {
             // this CTA's half of the B rows, into both CTAs' stage buffers
@@ -552,7 +564,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           if (PAIR) {
             mbar_wait_cluster(SPLIT3 ? &ready[tslot] : &ready[stage], SPLIT3 ? tph : phase);
           } else if (SPLIT3) {
-            mbar_wait(&ready[tslot], tph);
+            mbar_wait(&ready[tslot], tph);  // A converted (kSplitA: A landed before)
+            mbar_wait(&full[stage], phase);  // B landed
           } else {
             mbar_wait(&full[stage], phase);
           }
@@ -972,7 +985,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
         const uint32_t phase = uint32_t(it / S) & 1u;
         const int tslot = it % ST;
         const uint32_t tph = uint32_t(it / ST) & 1u;
-        mbar_wait(&full[stage], phase);
+        mbar_wait(kSplitA ? &fulla[stage] : &full[stage], phase);
         if (PAIR) {
           mbar_wait_cluster(&tfree[tslot], tph ^ 1);  // the slot's previous MMAs are done
         } else {
