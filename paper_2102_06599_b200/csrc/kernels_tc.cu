@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -1155,15 +1156,27 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
+  // NB_TC_PDL=0: launch without programmatic dependent launch (experiments)
+  static const bool pdl = [] {
+    const char* e = std::getenv("NB_TC_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
   cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = CL ? 2 : 1;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CL) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = CL ? 2 : 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL, KWF>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
