@@ -146,19 +146,6 @@ int choose_ksplit(const tc::TcArgs& t, int num_sms, bool pair) {
   return ks >= 2 ? ks : 1;
 }
 
-// Fused split-K (TcArgs::ksplit_fused): the last split of each tile runs the
-// epilogue instead of a separate k_splitk_epilogue launch.  NB_TC_SKFUSE:
-// 0 (default) off, 1 every split-K launch.  Measured slower (438 vs 487
-// candidates/s): the last arrivals run whole-tile epilogues serially at the
-// end of the grid, where the separate kernel spreads them over every SM.
-bool use_skfuse(int ksplit) {
-  static const int mode = [] {
-    const char* e = std::getenv("NB_TC_SKFUSE");
-    return e ? std::atoi(e) : 0;
-  }();
-  return ksplit > 1 && mode != 0;
-}
-
 // CTA-pair N tile for a range whose per-group width is n: the pair runs
 // M = 256 and each CTA stages half of B, halving the weight-operand traffic
 // per SM.  Measured slower than single-CTA tiles on the R34 layers (fprop
@@ -340,7 +327,6 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.out_c_per_group = r.slice_co;
             const bool mc = use_mc(bn, t.m_tiles, pbn != 0, kwf);
             t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
-            t.ksplit_fused = use_skfuse(t.ksplit) ? 1 : 0;
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
@@ -389,12 +375,9 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.part_ld = g.Ci;
           const bool mc = use_mc(bn, t.m_tiles, pbn != 0, kwf);
           t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
-          t.ksplit_fused = use_skfuse(t.ksplit) ? 1 : 0;
           // split-K dgrad: k_splitk_epilogue writes one partial per image
-          // (fused split-K: the kernel's own per-tile partials)
-          t.part_tiles_per_img = t.ksplit > 1 && !t.ksplit_fused
-                                     ? 1
-                                     : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
+          t.part_tiles_per_img =
+              t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
           if (t.ksplit > 1)
             P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
@@ -535,13 +518,6 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
     NB_CUDA(cudaMemsetAsync(c->trace.p, 0, (5 * tc::kTraceStages + 4 * 1024) * 8, st));
     L.args.trace = c->trace.as<long long>();
   }
-  if (L.args.ksplit > 1 && L.args.ksplit_fused) {
-    const size_t cb = size_t(L.args.nphase) * L.args.m_tiles * L.args.n_tiles * 4;
-    const size_t had = c->tilecnt.bytes;
-    c->tilecnt.ensure(cb);
-    if (c->tilecnt.bytes != had) NB_CUDA(cudaMemsetAsync(c->tilecnt.p, 0, c->tilecnt.bytes, st));
-    L.args.tile_cnt = c->tilecnt.as<unsigned>();
-  }
   L.bn = tp.bn;
   L.split3 = split3;
   L.pair = tp.pair;
@@ -605,7 +581,7 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       a.ws = c->ws.as<float>();
       a.ws_stride = int64_t(g.N) * g.OH * g.OW * g.Co;
       launch_tc(c, lp.tcf[r], a, P.split3, x, g.Ci, g.W, g.H, g.N, base + lp.tcf[r].w_off, st);
-      if (a.ksplit > 1 && !a.ksplit_fused) {
+      if (a.ksplit > 1) {
         SplitEpi e{};
         e.ws = a.ws;
         e.ws_stride = a.ws_stride;
@@ -652,7 +628,7 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
     a.ws = c->ws.as<float>();
     a.ws_stride = int64_t(g.N) * g.H * g.W * g.Ci;
     launch_tc(c, lp.tcd, a, P.split3, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
-    if (a.ksplit > 1 && !a.ksplit_fused) {
+    if (a.ksplit > 1) {
       SplitEpi e{};
       e.ws = a.ws;
       e.ws_stride = a.ws_stride;

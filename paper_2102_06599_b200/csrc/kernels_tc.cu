@@ -683,29 +683,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * NM);
       // accumulator chunk [c, c+16) of the layer's output channels; KWF adds
       // the kw = 0 / 2 column blocks of the pixels kwf_sgn*(kw - 1) away
-      // fused split-K fixup: the tile's last split re-reads every split's
-      // partial from ws (split order) instead of its TMEM accumulator
-      bool src_ws = false;
       auto acc_ld16 = [&](int c, float* v) {
-        if (src_ws) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          if (valid) {
-            for (int k = 0; k < a.ksplit; ++k) {
-              const float4* w4 = reinterpret_cast<const float4*>(
-                  a.ws + int64_t(k) * a.ws_stride + pix * a.out_ld + col0 + c);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float4 t = w4[i];
-                v[4 * i] += t.x;
-                v[4 * i + 1] += t.y;
-                v[4 * i + 2] += t.z;
-                v[4 * i + 3] += t.w;
-              }
-            }
-          }
-          return;
-        }
         if (!KWF) {
           tmem_ld16(trow + uint32_t(c), v);
         } else {
@@ -731,279 +709,250 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       // image): the next chunk's A_prev is loaded while this one is processed,
       // a 31-shuffle reduce-scatter leaves lane l with the warp's sum of column
       // l of the chunk, and the image's warps are combined once per tile.
-      auto epilogue_body = [&](bool partials_only) {
-        const bool fast_dgrad = a.mode == 1 && !partials_only && a.partial && a.a_prev &&
-                                rows_per_img % 32 == 0 && !(a.debug & 16);
-        if (fast_dgrad) {
-          const int64_t rbase = pix * a.out_ld + col0;
-          // A_prev in / dpre out through a per-warp transpose tile: lane l moves
-          // 16 B of row 8k + l/4 (column quad l%4) -- 8 rows x 64 B per warp
-          // instruction instead of 32 rows x 16 B
-          float* xp = red + 128 * 17 + q * (32 * 20);
-          const float* aprev = a.a_prev;
-          auto row_ptr = [&](int k) {  // this lane's transposed row k: base offset, valid
-            const int src = 8 * k + (lane >> 2);
-            const long long b = __shfl_sync(0xffffffffu, (long long)rbase, src);
-            const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
-            return ok ? b + 4 * (lane & 3) : -1ll;
-          };
-          long long rp[4];
-  #pragma unroll
-          for (int k = 0; k < 4; ++k) rp[k] = row_ptr(k);
-          float4 apn[4];
-  #pragma unroll
+      const bool fast_dgrad = a.mode == 1 && a.ksplit == 1 && a.partial && a.a_prev &&
+                              rows_per_img % 32 == 0 && !(a.debug & 16);
+      if (fast_dgrad) {
+        const int64_t rbase = pix * a.out_ld + col0;
+        // A_prev in / dpre out through a per-warp transpose tile: lane l moves
+        // 16 B of row 8k + l/4 (column quad l%4) -- 8 rows x 64 B per warp
+        // instruction instead of 32 rows x 16 B
+        float* xp = red + 128 * 17 + q * (32 * 20);
+        const float* aprev = a.a_prev;
+        auto row_ptr = [&](int k) {  // this lane's transposed row k: base offset, valid
+          const int src = 8 * k + (lane >> 2);
+          const long long b = __shfl_sync(0xffffffffu, (long long)rbase, src);
+          const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
+          return ok ? b + 4 * (lane & 3) : -1ll;
+        };
+        long long rp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rp[k] = row_ptr(k);
+        float4 apn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          apn[k] = rp[k] >= 0 ? *reinterpret_cast<const float4*>(aprev + rp[k])
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+          // transpose this chunk's A_prev rows into registers (own row)
+#pragma unroll
           for (int k = 0; k < 4; ++k)
-            apn[k] = rp[k] >= 0 ? *reinterpret_cast<const float4*>(aprev + rp[k])
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-  #pragma unroll 1
-          for (int c = 0; c < BN; c += 16) {
-            // transpose this chunk's A_prev rows into registers (own row)
-  #pragma unroll
+            *reinterpret_cast<float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3)) = apn[k];
+          __syncwarp();
+          float av[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 t = *reinterpret_cast<const float4*>(xp + lane * 20 + 4 * i);
+            av[4 * i] = t.x;
+            av[4 * i + 1] = t.y;
+            av[4 * i + 2] = t.z;
+            av[4 * i + 3] = t.w;
+          }
+          __syncwarp();
+          if (c + 16 < BN && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
+#pragma unroll
             for (int k = 0; k < 4; ++k)
-              *reinterpret_cast<float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3)) = apn[k];
-            __syncwarp();
-            float av[16];
-  #pragma unroll
+              if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
+          }
+          float v[16];
+          acc_ld16(c, v);
+          float x[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (empty_phase) v[i] = 0.f;
+            x[i] = valid ? av[i] * v[i] : 0.f;
+          }
+          if (a.g_out && valid) {
+            float4* go = reinterpret_cast<float4*>(a.g_out + rbase + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              go[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+          if (a.dpre_out && !(a.debug & 8192)) {  // (debug 8192: no dpre stores)
+#pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float4 t = *reinterpret_cast<const float4*>(xp + lane * 20 + 4 * i);
-              av[4 * i] = t.x;
-              av[4 * i + 1] = t.y;
-              av[4 * i + 2] = t.z;
-              av[4 * i + 3] = t.w;
+              float4 o;
+              o.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
+              o.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
+              o.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
+              o.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+              *reinterpret_cast<float4*>(xp + lane * 20 + 4 * i) = o;
             }
             __syncwarp();
-            if (c + 16 < BN && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
-  #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (rp[k] >= 0)
+                *reinterpret_cast<float4*>(a.dpre_out + rp[k] + c) =
+                    *reinterpret_cast<const float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3));
+            __syncwarp();
+          }
+          if (a.debug & 4096) {  // experiment: no reduction
+            if (lane < 16) red[q * BN + c + lane] = x[lane & 15];
+            continue;
+          }
+          // reduce-scatter over the warp: 16 + 8 + 4 + 2 + 1 shuffles
+#pragma unroll
+          for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
+          const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+          float y[8], z[4], w2[2];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float send = b3 ? x[i] : x[i + 8], keep = b3 ? x[i + 8] : x[i];
+            y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float send = b2 ? y[i] : y[i + 4], keep = b2 ? y[i + 4] : y[i];
+            z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const float send = b1 ? z[i] : z[i + 2], keep = b1 ? z[i + 2] : z[i];
+            w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+          {
+            const float send = b0 ? w2[0] : w2[1], keep = b0 ? w2[1] : w2[0];
+            const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            if (lane < 16) red[q * BN + c + lane] = tot;  // column c + (lane & 15)
+          }
+        }
+        named_bar(1, 128);
+        if (tile_real) {
+          const int wpi = rows_per_img / 32;
+          for (int idx = r; idx < a.BNI * BN; idx += 128) {
+            const int img = idx / BN, j = idx % BN;
+            const int nimg = nb * a.BNI + img;
+            if (nimg < a.nimg) {
+              float sum = 0.f;
+              for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red[w * BN + j];
+              a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld + col0 +
+                        j] = double(sum);
             }
-            float v[16];
-            acc_ld16(c, v);
-            float x[16];
-  #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              if (empty_phase) v[i] = 0.f;
-              x[i] = valid ? av[i] * v[i] : 0.f;
+          }
+        }
+        named_bar(1, 128);
+      }
+#pragma unroll 1
+      for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
+        float v[16];
+        acc_ld16(c, v);
+        if (empty_phase) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (a.ksplit > 1) {
+          // split-K: raw partial sums into this split's copy of the output;
+          // k_splitk_epilogue adds the copies in order and runs the epilogue
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(a.ws + int64_t(d.ks) * a.ws_stride +
+                                                  pix * a.out_ld + col0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        } else if (a.mode == 0) {
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              if (a.relu) {
+                x.x = x.x > 0.f ? x.x : 0.f;
+                x.y = x.y > 0.f ? x.y : 0.f;
+                x.z = x.z > 0.f ? x.z : 0.f;
+                x.w = x.w > 0.f ? x.w : 0.f;
+              }
+              o[i] = x;
             }
-            if (a.g_out && valid) {
-              float4* go = reinterpret_cast<float4*>(a.g_out + rbase + c);
-  #pragma unroll
+          }
+        } else {
+          float contrib[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) contrib[i] = 0.f;
+          if (valid) {
+            const int64_t base = pix * a.out_ld + col0 + c;
+            if (a.g_out) {
+              float4* go = reinterpret_cast<float4*>(a.g_out + base);
+#pragma unroll
               for (int i = 0; i < 4; ++i)
                 go[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
-            if (a.dpre_out && !(a.debug & 8192)) {  // (debug 8192: no dpre stores)
-  #pragma unroll
+            if (a.a_prev) {
+              const float4* ap = reinterpret_cast<const float4*>(a.a_prev + base);
+              float av[16];
+#pragma unroll
               for (int i = 0; i < 4; ++i) {
-                float4 o;
-                o.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
-                o.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
-                o.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
-                o.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
-                *reinterpret_cast<float4*>(xp + lane * 20 + 4 * i) = o;
+                float4 x = ap[i];
+                av[4 * i] = x.x;
+                av[4 * i + 1] = x.y;
+                av[4 * i + 2] = x.z;
+                av[4 * i + 3] = x.w;
               }
-              __syncwarp();
-  #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                if (rp[k] >= 0)
-                  *reinterpret_cast<float4*>(a.dpre_out + rp[k] + c) =
-                      *reinterpret_cast<const float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3));
-              __syncwarp();
-            }
-            if (a.debug & 4096) {  // experiment: no reduction
-              if (lane < 16) red[q * BN + c + lane] = x[lane & 15];
-              continue;
-            }
-            // reduce-scatter over the warp: 16 + 8 + 4 + 2 + 1 shuffles
-  #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
-            const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
-            float y[8], z[4], w2[2];
-  #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float send = b3 ? x[i] : x[i + 8], keep = b3 ? x[i + 8] : x[i];
-              y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-            }
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float send = b2 ? y[i] : y[i + 4], keep = b2 ? y[i + 4] : y[i];
-              z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-            }
-  #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const float send = b1 ? z[i] : z[i + 2], keep = b1 ? z[i + 2] : z[i];
-              w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-            }
-            {
-              const float send = b0 ? w2[0] : w2[1], keep = b0 ? w2[1] : w2[0];
-              const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-              if (lane < 16) red[q * BN + c + lane] = tot;  // column c + (lane & 15)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) contrib[i] = av[i] * v[i];
+              if (a.dpre_out) {
+                float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float4 x;
+                  x.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
+                  x.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
+                  x.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
+                  x.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+                  dp[i] = x;
+                }
+              }
+            } else if (a.dpre_out) {
+              float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           }
-          named_bar(1, 128);
-          if (tile_real) {
+          if (a.partial && tile_real && rows_per_img % 32 == 0) {
+            // deterministic per-(image, channel) sums: each warp's 32 rows lie
+            // in one image -- xor-butterfly within the warp, then the image's
+            // warps in order
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+#pragma unroll
+              for (int o = 16; o; o >>= 1) contrib[i] += __shfl_xor_sync(0xffffffffu, contrib[i], o);
+            if (lane == 0) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) red[q * 17 + i] = contrib[i];
+            }
+            named_bar(1, 128);
             const int wpi = rows_per_img / 32;
-            for (int idx = r; idx < a.BNI * BN; idx += 128) {
-              const int img = idx / BN, j = idx % BN;
+            if (r < a.BNI * 16) {
+              const int img = r / 16, j = r % 16;
               const int nimg = nb * a.BNI + img;
               if (nimg < a.nimg) {
-                float sum = 0.f;
-                for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red[w * BN + j];
-                a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld + col0 +
-                          j] = double(sum);
+                float s = 0.f;
+                for (int w = img * wpi; w < (img + 1) * wpi; ++w) s += red[w * 17 + j];
+                a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
+                          col0 + c + j] = double(s);
               }
             }
-          }
-          named_bar(1, 128);
-        }
-  #pragma unroll 1
-        for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
-          float v[16];
-          acc_ld16(c, v);
-          if (empty_phase) {
-  #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          }
-          if (partials_only) {
-            // split-K: raw partial sums into this split's copy of the output;
-            // k_splitk_epilogue adds the copies in order and runs the epilogue
-            if (valid) {
-              float4* o = reinterpret_cast<float4*>(a.ws + int64_t(d.ks) * a.ws_stride +
-                                                    pix * a.out_ld + col0 + c);
-  #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-          } else if (a.mode == 0) {
-            if (valid) {
-              float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
-  #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                if (a.relu) {
-                  x.x = x.x > 0.f ? x.x : 0.f;
-                  x.y = x.y > 0.f ? x.y : 0.f;
-                  x.z = x.z > 0.f ? x.z : 0.f;
-                  x.w = x.w > 0.f ? x.w : 0.f;
-                }
-                o[i] = x;
+            named_bar(1, 128);
+          } else if (a.partial && tile_real) {
+            // small images (several per tile): serial sums over each image's rows
+#pragma unroll
+            for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
+            named_bar(1, 128);
+            for (int wi2 = r; wi2 < a.BNI * 16; wi2 += 128) {
+              const int img = wi2 / 16, j = wi2 % 16;
+              const int nimg = nb * a.BNI + img;
+              if (nimg < a.nimg) {
+                float s = 0.f;
+                for (int rr = img * rows_per_img; rr < (img + 1) * rows_per_img; ++rr)
+                  s += red[rr * 17 + j];
+                a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
+                          col0 + c + j] = double(s);
               }
             }
-          } else {
-            float contrib[16];
-  #pragma unroll
-            for (int i = 0; i < 16; ++i) contrib[i] = 0.f;
-            if (valid) {
-              const int64_t base = pix * a.out_ld + col0 + c;
-              if (a.g_out) {
-                float4* go = reinterpret_cast<float4*>(a.g_out + base);
-  #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  go[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-              }
-              if (a.a_prev) {
-                const float4* ap = reinterpret_cast<const float4*>(a.a_prev + base);
-                float av[16];
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float4 x = ap[i];
-                  av[4 * i] = x.x;
-                  av[4 * i + 1] = x.y;
-                  av[4 * i + 2] = x.z;
-                  av[4 * i + 3] = x.w;
-                }
-  #pragma unroll
-                for (int i = 0; i < 16; ++i) contrib[i] = av[i] * v[i];
-                if (a.dpre_out) {
-                  float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
-  #pragma unroll
-                  for (int i = 0; i < 4; ++i) {
-                    float4 x;
-                    x.x = (a.relu_prev && !(av[4 * i] > 0.f)) ? 0.f : v[4 * i];
-                    x.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
-                    x.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
-                    x.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
-                    dp[i] = x;
-                  }
-                }
-              } else if (a.dpre_out) {
-                float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
-  #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-              }
-            }
-            if (a.partial && tile_real && rows_per_img % 32 == 0) {
-              // deterministic per-(image, channel) sums: each warp's 32 rows lie
-              // in one image -- xor-butterfly within the warp, then the image's
-              // warps in order
-  #pragma unroll
-              for (int i = 0; i < 16; ++i)
-  #pragma unroll
-                for (int o = 16; o; o >>= 1) contrib[i] += __shfl_xor_sync(0xffffffffu, contrib[i], o);
-              if (lane == 0) {
-  #pragma unroll
-                for (int i = 0; i < 16; ++i) red[q * 17 + i] = contrib[i];
-              }
-              named_bar(1, 128);
-              const int wpi = rows_per_img / 32;
-              if (r < a.BNI * 16) {
-                const int img = r / 16, j = r % 16;
-                const int nimg = nb * a.BNI + img;
-                if (nimg < a.nimg) {
-                  float s = 0.f;
-                  for (int w = img * wpi; w < (img + 1) * wpi; ++w) s += red[w * 17 + j];
-                  a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
-                            col0 + c + j] = double(s);
-                }
-              }
-              named_bar(1, 128);
-            } else if (a.partial && tile_real) {
-              // small images (several per tile): serial sums over each image's rows
-  #pragma unroll
-              for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
-              named_bar(1, 128);
-              for (int wi2 = r; wi2 < a.BNI * 16; wi2 += 128) {
-                const int img = wi2 / 16, j = wi2 % 16;
-                const int nimg = nb * a.BNI + img;
-                if (nimg < a.nimg) {
-                  float s = 0.f;
-                  for (int rr = img * rows_per_img; rr < (img + 1) * rows_per_img; ++rr)
-                    s += red[rr * 17 + j];
-                  a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
-                            col0 + c + j] = double(s);
-                }
-              }
-              named_bar(1, 128);
-            }
+            named_bar(1, 128);
           }
         }
-      };
-      if (a.ksplit > 1) {
-        epilogue_body(true);  // this split's partial sums -> ws
-        if (a.ksplit_fused) {
-          // the tile's last split to arrive (counter) sums all splits in
-          // split order and runs the epilogue proper; it resets the counter
-          __shared__ int sk_last;
-          named_bar(1, 128);
-          if (r == 0) {
-            __threadfence();
-            const int64_t tid = (int64_t(d.ph) * a.m_tiles + m) * a.n_tiles + nt;
-            const unsigned old = atomicAdd(a.tile_cnt + tid, 1u);
-            const int last = old == unsigned(a.ksplit - 1);
-            if (last) {
-              a.tile_cnt[tid] = 0u;
-              __threadfence();
-            }
-            sk_last = last;
-          }
-          named_bar(1, 128);
-          if (sk_last) {
-            src_ws = true;
-            epilogue_body(false);
-          }
-        }
-      } else {
-        epilogue_body(false);
       }
       // all 128 rows drained -> one arrival per CTA on the MMA CTA's barrier
       tc_fence_before();

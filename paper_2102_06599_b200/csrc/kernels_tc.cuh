@@ -46,10 +46,6 @@ struct TcArgs {
   int ksplit;
   float* ws;
   int64_t ws_stride;
-  // fused split-K: no k_splitk_epilogue launch; the last split of each tile
-  // (per-tile arrival counter, reset by it) runs the epilogue from ws
-  int ksplit_fused;
-  unsigned* tile_cnt;
   int S;  // element stride of the A box (fprop stride; 1 for dgrad)
   // phases
   int nphase, PS;
