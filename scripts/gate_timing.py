@@ -15,6 +15,7 @@ L = len(o["layers"])
 cfg = {"schema_version": 1, "candidate_count": count, "max_seq_len": 6, "seed": 7,
        "batch": {"n": 128, "seed": 1}, "layer_mask": [l in mask for l in range(L)], "network": o}
 res = {}
+S.gate_candidates(dict(cfg, candidate_count=8), legal_device=0)  # CUDA context / module load
 for dev in (0, -1):
     t = time.perf_counter()
     g = S.gate_candidates(cfg, legal_device=dev)
