@@ -794,7 +794,7 @@ inline std::vector<nestopt::Candidate> draw_candidates(const nestopt::Network& o
 // faster than a device round trip.
 inline long long legal_gpu_min() {
   const char* e = std::getenv("NB_LEGAL_GPU_MIN");
-  return e && *e ? std::atoll(e) : 20000;
+  return e && *e ? std::atoll(e) : 1000;
 }
 
 // Scheduler statistics of one evaluate_all_gpu call.
