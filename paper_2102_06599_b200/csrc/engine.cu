@@ -478,7 +478,11 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
                 cudaStream_t st) {
   float* base = lp.wbase;
   for (int r = 0; r < lp.geom.nranges; ++r) {
-    PackDst d{base, base, nullptr, nullptr, nullptr, nullptr};
+    // the direct-kernel layouts only where a direct kernel reads them
+    const bool need_wf = lp.family[r] != Family::TensorCore;
+    const bool need_wd = lp.dgrad_family != Family::TensorCore;
+    PackDst d{need_wf ? base : nullptr, need_wd ? base : nullptr, nullptr, nullptr, nullptr,
+              nullptr};
     d.KW = lp.geom.KW;
     if (lp.family[r] == Family::TensorCore) {
       d.tcf_hi = base + lp.tcf[r].w_off;
