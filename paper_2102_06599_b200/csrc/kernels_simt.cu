@@ -96,12 +96,14 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
 constexpr int kFpPix = 128;
 constexpr int kFpKChunk = 128;
 
-template <int CO_T>
+template <int CO_T, int PX>
 __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
                                                           const float* __restrict__ x,
                                                           const float* __restrict__ wbase,
                                                           float* __restrict__ y, bool relu) {
-  __shared__ float ws[kFpKChunk][CO_T];
+  // PX pixels per thread (pixels threadIdx.x + 128 i): each shared-memory
+  // weight read feeds PX pixels
+  __shared__ float ws[kFpKChunk * PX][CO_T];
   const RangeDesc r = g.r[ri];
   const float* __restrict__ wf = wbase + r.wf_off;
   const int co_chunks = (r.slice_co + CO_T - 1) / CO_T;
@@ -109,18 +111,24 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
   const int co0 = (blockIdx.y % co_chunks) * CO_T;  // within the group
   const int nco = min(CO_T, r.slice_co - co0);
   const int64_t npix = int64_t(g.N) * g.OH * g.OW;
-  const int64_t pix = int64_t(blockIdx.x) * kFpPix + threadIdx.x;
-  const bool valid = pix < npix;
-  int ow = 0, oh = 0;
-  int64_t n = 0;
-  if (valid) {
-    ow = int(pix % g.OW);
-    oh = int((pix / g.OW) % g.OH);
-    n = pix / (int64_t(g.OW) * g.OH);
-  }
-  float acc[CO_T];
+  const int64_t pix0 = int64_t(blockIdx.x) * kFpPix * PX;
+  bool valid[PX];
+  int ow[PX], oh[PX];
+  int64_t n[PX];
 #pragma unroll
-  for (int t = 0; t < CO_T; ++t) acc[t] = 0.f;
+  for (int i = 0; i < PX; ++i) {
+    const int64_t pix = pix0 + threadIdx.x + i * kFpPix;
+    valid[i] = pix < npix;
+    const int64_t pp = valid[i] ? pix : 0;
+    ow[i] = int(pp % g.OW);
+    oh[i] = int((pp / g.OW) % g.OH);
+    n[i] = pp / (int64_t(g.OW) * g.OH);
+  }
+  float acc[PX][CO_T];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int t = 0; t < CO_T; ++t) acc[i][t] = 0.f;
   const int K = r.slice_ci * g.KH * g.KW;
   // float4 input path: a tap's slice_ci channels are contiguous and aligned,
   // and K chunks hold whole taps (summation order per output unchanged)
@@ -133,59 +141,76 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
       ws[kk][t] = t < nco ? wf[int64_t(k0 + kk) * r.len + grp * r.slice_co + co0 + t] : 0.f;
     }
     __syncthreads();
-    if (valid && vec4) {
+    if (vec4) {
       // whole taps of the chunk, the tap's slice_ci inputs as float4s
       for (int kk = 0; kk < kn; kk += r.slice_ci) {
         const int tap = (k0 + kk) / r.slice_ci;
         const int kh = tap / g.KW, kw = tap - kh * g.KW;
-        const int ih = g.S * oh - g.P + kh, iw = g.S * ow - g.P + kw;
-        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
-        const float4* xp = reinterpret_cast<const float4*>(
-            x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci);
+        const float4* xp[PX];
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+          const int ih = g.S * oh[i] - g.P + kh, iw = g.S * ow[i] - g.P + kw;
+          xp[i] = (valid[i] && ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+                      ? reinterpret_cast<const float4*>(x + ((n[i] * g.H + ih) * g.W + iw) * g.Ci +
+                                                        int64_t(grp) * r.slice_ci)
+                      : nullptr;  // padded taps add nothing (I/nnet.hpp:121-123)
+        }
         for (int j4 = 0; j4 < r.slice_ci / 4; ++j4) {
-          const float4 xv = __ldg(xp + j4);
+          float4 xv[PX];
+#pragma unroll
+          for (int i = 0; i < PX; ++i)
+            xv[i] = xp[i] ? __ldg(xp[i] + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
           const int b = kk + 4 * j4;
 #pragma unroll
           for (int t = 0; t < CO_T; ++t) {
-            float a = acc[t];
-            a = fmaf(xv.x, ws[b][t], a);
-            a = fmaf(xv.y, ws[b + 1][t], a);
-            a = fmaf(xv.z, ws[b + 2][t], a);
-            acc[t] = fmaf(xv.w, ws[b + 3][t], a);
+            const float w0 = ws[b][t], w1 = ws[b + 1][t], w2 = ws[b + 2][t], w3 = ws[b + 3][t];
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+              if (!xp[i]) continue;
+              float a = acc[i][t];
+              a = fmaf(xv[i].x, w0, a);
+              a = fmaf(xv[i].y, w1, a);
+              a = fmaf(xv[i].z, w2, a);
+              acc[i][t] = fmaf(xv[i].w, w3, a);
+            }
           }
         }
       }
-    } else if (valid) {
+    } else {
       for (int kk = 0; kk < kn; ++kk) {
         const int k = k0 + kk;
         const int tap = k / r.slice_ci, j = k - tap * r.slice_ci;
         const int kh = tap / g.KW, kw = tap - kh * g.KW;
-        const int ih = g.S * oh - g.P + kh, iw = g.S * ow - g.P + kw;
-        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
-        const float xv =
-            __ldg(x + ((n * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci + j);
 #pragma unroll
-        for (int t = 0; t < CO_T; ++t) acc[t] = fmaf(xv, ws[kk][t], acc[t]);
+        for (int i = 0; i < PX; ++i) {
+          const int ih = g.S * oh[i] - g.P + kh, iw = g.S * ow[i] - g.P + kw;
+          if (!valid[i] || ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
+          const float xv =
+              __ldg(x + ((n[i] * g.H + ih) * g.W + iw) * g.Ci + int64_t(grp) * r.slice_ci + j);
+#pragma unroll
+          for (int t = 0; t < CO_T; ++t) acc[i][t] = fmaf(xv, ws[kk][t], acc[i][t]);
+        }
       }
     }
   }
-  // stage the block's 128 pixels x CO_T outputs in ws (row p rotated by p so
-  // the per-thread writes are bank-conflict free), then store them with
+  // stage the block's pixels x CO_T outputs in ws (row p rotated by p so the
+  // per-thread writes are bank-conflict free), then store them with
   // consecutive threads on consecutive 16-byte pieces of each pixel's run
   __syncthreads();
-  if (valid) {
+#pragma unroll
+  for (int i = 0; i < PX; ++i) {
+    if (!valid[i]) continue;
+    const int p = threadIdx.x + i * kFpPix;
 #pragma unroll
     for (int t = 0; t < CO_T; ++t)
-      ws[threadIdx.x][(t + threadIdx.x) & (CO_T - 1)] =
-          (relu && !(acc[t] > 0.f)) ? 0.f : acc[t];  // I/nnet.hpp:138-139
+      ws[p][(t + p) & (CO_T - 1)] = (relu && !(acc[i][t] > 0.f)) ? 0.f : acc[i][t];  // I/nnet.hpp:138-139
   }
   __syncthreads();
-  const int64_t pix0 = int64_t(blockIdx.x) * kFpPix;
   const int cbase = r.b + grp * r.slice_co + co0;
   const bool vec = (cbase % 4 == 0) && (g.Co % 4 == 0) && (nco % 4 == 0);
   if (vec) {
     const int quads = nco / 4;
-    for (int e = threadIdx.x; e < kFpPix * quads; e += kFpPix) {
+    for (int e = threadIdx.x; e < kFpPix * PX * quads; e += kFpPix) {
       const int p = e / quads, qd = e - p * quads;
       if (pix0 + p >= npix) break;
       float4 o;
@@ -196,7 +221,7 @@ __global__ void __launch_bounds__(kFpPix) k_fprop_blocked(ConvGeom g, int ri,
       *reinterpret_cast<float4*>(y + (pix0 + p) * g.Co + cbase + 4 * qd) = o;
     }
   } else {
-    for (int e = threadIdx.x; e < kFpPix * nco; e += kFpPix) {
+    for (int e = threadIdx.x; e < kFpPix * PX * nco; e += kFpPix) {
       const int p = e / nco, t = e - p * nco;
       if (pix0 + p >= npix) break;
       y[(pix0 + p) * g.Co + cbase + t] = ws[p][(t + p) & (CO_T - 1)];
@@ -935,14 +960,15 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
   }
   const int64_t npix = int64_t(g.N) * g.OH * g.OW;
   const unsigned gx = unsigned((npix + kFpPix - 1) / kFpPix);
+  const unsigned gx2 = unsigned((npix + 2 * kFpPix - 1) / (2 * kFpPix));
   if (r.slice_co <= 16) {
-    k_fprop_blocked<16><<<dim3(gx, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
+    k_fprop_blocked<16, 2><<<dim3(gx2, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
   } else if (r.slice_co <= 32) {
-    k_fprop_blocked<32><<<dim3(gx, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
+    k_fprop_blocked<32, 2><<<dim3(gx2, r.groups), kFpPix, 0, st>>>(g, range, x, wbase, y, relu);
   } else {
     const int chunks = (r.slice_co + 63) / 64;
-    k_fprop_blocked<64><<<dim3(gx, r.groups * chunks), kFpPix, 0, st>>>(g, range, x, wbase, y,
-                                                                        relu);
+    k_fprop_blocked<64, 1><<<dim3(gx, r.groups * chunks), kFpPix, 0, st>>>(g, range, x, wbase,
+                                                                           y, relu);
   }
 }
 
