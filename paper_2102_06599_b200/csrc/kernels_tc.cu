@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   constexpr int kCtas = PAIR ? 2 : 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&ready[s], kCtas * (a.conv_halves ? 2 : 1));
+      mbar_init(&ready[s], kCtas * (SPLIT3 && a.conv_halves ? 2 : 1));  // (1xTF32: relay arrivals)
       mbar_init(&tfree[s], 1);
     }
     for (int s = 0; s < S; ++s) {
