@@ -7,6 +7,7 @@
 // output channels for fprop and across input channels for dgrad).
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -764,6 +765,10 @@ __global__ void __launch_bounds__(512) k_fisher_reduce(const FisherLayer* __rest
 // tiles, N); each thread walks pixels p = lane, lane+8, ... of one image.
 __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
   __shared__ float red[8][33];
+  // launched with programmatic stream serialization: let the next conv
+  // launch early, then wait for the split units this reduces
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int64_t n = blockIdx.y;
   float contrib = 0.f;
@@ -802,6 +807,10 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
 // pixels ty, ty + 8, ...; same fixed summation orders as the scalar kernel.
 __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
   __shared__ float red[8][129];
+  // launched with programmatic stream serialization: let the next conv
+  // launch early, then wait for the split units this reduces
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int c = (blockIdx.x * 32 + threadIdx.x) * 4;
   const int64_t n = blockIdx.y;
   float contrib[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1023,13 +1032,27 @@ void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbas
 }
 
 void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st) {
+  // programmatic dependent launch: its launch overlaps the conv's tail (the
+  // kernel waits on griddepcontrol before reading the partials)
+  static const bool pdl = [] {
+    const char* v = std::getenv("NB_TC_PDL");
+    return !v || std::atoi(v) != 0;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(32, 8);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (e.C % 4 == 0 && e.ld % 4 == 0 && e.c0 % 4 == 0) {
-    dim3 grid((e.C + 127) / 128, e.N);
-    k_splitk_epilogue4<<<grid, dim3(32, 8), 0, st>>>(e);
+    cfg.gridDim = dim3((e.C + 127) / 128, e.N);
+    cudaLaunchKernelEx(&cfg, k_splitk_epilogue4, e);
     return;
   }
-  dim3 grid((e.C + 31) / 32, e.N);
-  k_splitk_epilogue<<<grid, dim3(32, 8), 0, st>>>(e);
+  cfg.gridDim = dim3((e.C + 31) / 32, e.N);
+  cudaLaunchKernelEx(&cfg, k_splitk_epilogue, e);
 }
 
 void launch_head(const HeadArgs& a, cudaStream_t st) {
