@@ -194,8 +194,10 @@ bool use_kwf(const ConvGeom& g, int width, int rows_w) {
     const char* e = std::getenv("NB_TC_KWF");
     return e ? std::atoi(e) : 1;
   }();
-  return mode != 0 && width == 64 && g.KW == 3 && g.S == 1 && g.P == 1 && rows_w == 32 &&
-         g.W == 32 && g.OW == 32;
+  // image rows of 4..32 pixels that tile a warp exactly (tile rows = image
+  // rows: lane segments of rows_w lanes hold one image row each)
+  return mode != 0 && width == 64 && g.KW == 3 && g.S == 1 && g.P == 1 && rows_w == g.OW &&
+         g.W == g.OW && g.OW >= 4 && g.OW <= 32 && 32 % g.OW == 0;
 }
 
 // the kh taps of a kw-fused plan: A shifted in h only, B K chunk kh
@@ -204,6 +206,7 @@ void kwf_taps(const ConvGeom& g, tc::TcArgs& t, int sgn) {
   for (int kh = 0; kh < g.KH; ++kh)
     t.taps[0][kh] = tc::pack_tap(kh, sgn > 0 ? kh - g.P : g.P - kh, 0);
   t.kwf_sgn = sgn;
+  t.kwf_w = g.OW;
 }
 
 // fprop: one phase over the OH x OW output, every tap, A box at

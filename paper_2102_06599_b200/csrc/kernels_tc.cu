@@ -692,16 +692,18 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           tmem_ld16_nw(trow + uint32_t(BN + c), m);
           tmem_ld16_nw(trow + uint32_t(2 * BN + c), rr);
           tmem_wait_ld();
-          // fprop (sgn +1): out(w) = D0(w-1) + D1(w) + D2(w+1); dgrad: D0(w+1) + D1(w) + D2(w-1)
+          // fprop (sgn +1): out(w) = D0(w-1) + D1(w) + D2(w+1); dgrad: D0(w+1) + D1(w) + D2(w-1);
+          // w = the lane's position in its image-row segment of kwf_w lanes
           const bool fwd = a.kwf_sgn > 0;
+          const int kw_lane = lane & (a.kwf_w - 1);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float left_src = __uint_as_float(fwd ? l[i] : rr[i]);
             const float right_src = __uint_as_float(fwd ? rr[i] : l[i]);
-            const float from_left = __shfl_up_sync(0xffffffffu, left_src, 1);
-            const float from_right = __shfl_down_sync(0xffffffffu, right_src, 1);
-            v[i] = __uint_as_float(m[i]) + (lane > 0 ? from_left : 0.f) +
-                   (lane < 31 ? from_right : 0.f);
+            const float from_left = __shfl_up_sync(0xffffffffu, left_src, 1, a.kwf_w);
+            const float from_right = __shfl_down_sync(0xffffffffu, right_src, 1, a.kwf_w);
+            v[i] = __uint_as_float(m[i]) + (kw_lane > 0 ? from_left : 0.f) +
+                   (kw_lane < a.kwf_w - 1 ? from_right : 0.f);
           }
         }
       };

@@ -69,6 +69,7 @@ struct TcArgs {
   int relu_prev, part_tiles_per_img, part_ld;
   // kw-fused plan (KWF): +1 fprop, -1 dgrad, 0 off -- see Cfg in kernels_tc.cu
   int kwf_sgn;
+  int kwf_w;  // image row width of a kw-fused plan (a lane segment per row)
   // 3xTF32 converters: both groups split every stage (channel halves) rather
   // than alternating stages (lower per-stage latency for shallow rings)
   int conv_halves;

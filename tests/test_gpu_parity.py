@@ -259,6 +259,8 @@ TC_SPECS = [
     ConvSpec(64, 64, 32, 32, 3, 3, 1, 1),                      # kw-fused fprop + dgrad (N=192)
     ConvSpec(128, 64, 32, 32, 3, 3, 1, 1),                     # kw-fused fprop, K = 3 x 128
     ConvSpec(64, 64, 12, 32, 3, 3, 1, 1, spatial_div_h=2),     # kw-fused, short rows + crop
+    ConvSpec(64, 64, 8, 8, 3, 3, 1, 1),                        # kw-fused, 8-pixel rows (4 per warp)
+    ConvSpec(128, 64, 6, 16, 3, 3, 1, 1),                      # kw-fused, 16-pixel rows, partial tiles
 ]
 
 
