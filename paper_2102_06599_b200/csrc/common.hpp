@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "nb200.h"
@@ -81,6 +82,8 @@ struct NetDesc {
 // head is z_L[k] * (1/sqrt(C_last)).  libstdc++'s normal_distribution
 // returns z*stddev + mean, so scaling a cached prefix is bit-exact.
 const std::vector<double>& z_stream(uint64_t seed, int64_t stream, int64_t count);
+// Fills several (stream, count) z-streams in parallel host threads.
+void z_prefetch(uint64_t seed, const std::vector<std::pair<int64_t, int64_t>>& streams);
 
 void make_batch(const NetDesc& net, int64_t n, uint64_t seed, double* x, int32_t* labels);
 

@@ -975,6 +975,10 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
 }
 
 void warm_z(nb_ctx* c, const NetDesc& net) {
+  std::vector<std::pair<int64_t, int64_t>> want;
+  for (int64_t l = 0; l < net.L(); ++l) want.push_back({l, net.specs[l].weight_count()});
+  want.push_back({net.L(), net.num_classes * net.c_last()});
+  z_prefetch(net.seed, want);
   for (int64_t l = 0; l < net.L(); ++l) ensure_z(c, net.seed, l, net.specs[l].weight_count());
   ensure_z(c, net.seed, net.L(), net.num_classes * net.c_last());
 }

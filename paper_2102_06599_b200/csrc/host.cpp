@@ -2,6 +2,7 @@
 // MAC counts, shape repair, the z-stream weight cache, make_batch and the
 // LPT scheduler helper.  No device code here.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -9,6 +10,7 @@
 #include <mutex>
 #include <numeric>
 #include <random>
+#include <thread>
 
 #include "common.hpp"
 
@@ -179,19 +181,44 @@ std::map<ZKey, std::shared_ptr<std::vector<double>>> g_z;
 }  // namespace
 
 const std::vector<double>& z_stream(uint64_t seed, int64_t stream, int64_t count) {
+  {
+    std::lock_guard<std::mutex> lk(g_z_mu);
+    auto& slot = g_z[{seed, stream}];
+    if (slot && int64_t(slot->size()) >= count) return *slot;
+  }
+  // Generated outside the lock so z_prefetch can fill several layers'
+  // streams at once; a racing thread producing the same stream produces
+  // the same numbers, and the longer vector wins.
+  // Same engine seeding and draw sequence as I/nnet.hpp:64-68 / :72-75.
+  auto v = std::make_shared<std::vector<double>>(size_t(count));
+  std::mt19937_64 rng(seed * 0x9e3779b97f4a7c15ull + uint64_t(stream) + 1);
+  std::normal_distribution<double> dist(0.0, 1.0);
+  for (double& x : *v) x = dist(rng);
   std::lock_guard<std::mutex> lk(g_z_mu);
   auto& slot = g_z[{seed, stream}];
-  if (!slot || int64_t(slot->size()) < count) {
-    // Same engine seeding and draw sequence as I/nnet.hpp:64-68 / :72-75.
-    auto v = std::make_shared<std::vector<double>>(size_t(count));
-    std::mt19937_64 rng(seed * 0x9e3779b97f4a7c15ull + uint64_t(stream) + 1);
-    std::normal_distribution<double> dist(0.0, 1.0);
-    for (double& x : *v) x = dist(rng);
+  if (!slot || slot->size() < v->size()) {
     slot = v;  // older (shorter) vectors stay alive in holders' copies only
     static std::vector<std::shared_ptr<std::vector<double>>> keep;
     keep.push_back(v);  // references handed out must outlive extensions
   }
   return *slot;
+}
+
+void z_prefetch(uint64_t seed, const std::vector<std::pair<int64_t, int64_t>>& streams) {
+  // Longest first, so the 2.4M-draw layers do not start last.
+  std::vector<std::pair<int64_t, int64_t>> todo(streams);
+  std::sort(todo.begin(), todo.end(),
+            [](const auto& a, const auto& b) { return a.second > b.second; });
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>(todo.size(), std::min(hw, 16u));
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  for (size_t t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (size_t i; (i = next.fetch_add(1)) < todo.size();)
+        z_stream(seed, todo[i].first, todo[i].second);
+    });
+  for (auto& th : pool) th.join();
 }
 
 // make_batch, I/nnet.hpp:87-101: per example Ci*H*W normals, then one label.
@@ -294,6 +321,10 @@ nb_status nb_fisher_flops(const nb_network* net, int64_t n, double* flops) {
 nb_status nb_init_weights(const nb_network* net, double* weights, double* head) {
   return guard([&] {
     NetDesc d = NetDesc::from(net);
+    std::vector<std::pair<int64_t, int64_t>> want;
+    for (int64_t l = 0; l < d.L(); ++l) want.push_back({l, d.specs[l].weight_count()});
+    want.push_back({d.L(), d.num_classes * d.c_last()});
+    z_prefetch(d.seed, want);
     size_t off = 0;
     for (int64_t l = 0; l < d.L(); ++l) {
       const Spec& s = d.specs[l];
