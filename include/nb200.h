@@ -341,6 +341,19 @@ nb_ctx* nb_session_ctx(nb_session* s);
 nb_status nb_session_fisher(nb_session* s, const nb_network* net,
                             const nb_weights* w, nb_precision prec,
                             nb_fisher_out* out);
+/* fisher_potential (I/nnet.hpp:321-350) of one network with the batch split
+ * into example shards (the secondary axis for fewer networks
+ * than GPUs): shards[i] holds examples [n_0+..+n_{i-1}, +n_i) of one batch,
+ * normally one session per GPU, each on its own context.  Every shard
+ * divides dz by the whole batch's N and plans its launches for it; the
+ * per-example sums s_nc are gathered into shards[0]'s GPU (peer copies) and
+ * reduced there in the unsharded kernel's fixed order, so the report
+ * (per_channel, per_layer, total, loss, probs) is bitwise that of one
+ * session holding the whole batch.  NB_ERR_CONFIG for repeated contexts or
+ * shards of different batch seeds. */
+nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count,
+                            const nb_network* net, const nb_weights* w,
+                            nb_precision prec, nb_fisher_out* out);
 /* forward only (transformed-net inference): probs n x classes, loss. */
 nb_status nb_session_forward(nb_session* s, const nb_network* net,
                              const nb_weights* w, nb_precision prec,

@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     RECHECK_BAND, TOLERANCE, FisherReport, ForwardCache, InvalidSpec, Layer, Network, NoDevice, Precision, Session,
     ShapeMismatch, Unsupported, activation_gradients, conv_dgrad, count_macs,
     default_context, device_count, evaluate, fisher_accepts, fisher_flops, fisher_potential,
+    fisher_sharded, shard_batch,
     forward, layer_forward, legality_fisher, make_batch, network_macs, reference_conv,
     repair_network, schedule_lpt,
 )

@@ -162,6 +162,8 @@ SIGNATURES = {
     "nb_session_ctx": (vp, [vp]),
     "nb_session_fisher": (C.c_int, [vp, P(NetworkC), P(WeightsC), C.c_int, P(FisherOutC)]),
     "nb_session_forward": (C.c_int, [vp, P(NetworkC), P(WeightsC), C.c_int, dp, dp]),
+    "nb_fisher_sharded": (C.c_int, [P(vp), C.c_int32, P(NetworkC), P(WeightsC), C.c_int,
+                                    P(FisherOutC)]),
     "nb_evaluate": (C.c_int, [P(vp), C.c_int32, P(NetworkC), C.c_int64, C.c_int,
                               P(FisherOutC), P(EvalStatsC)]),
 }

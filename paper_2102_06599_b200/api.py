@@ -607,6 +607,31 @@ class Session:
         return probs, loss.value
 
 
+def shard_batch(batch: Batch, count: int) -> List[Batch]:
+    """Consecutive example slices of one batch (sizes differ by at most one),
+    for nb_fisher_sharded."""
+    n = len(batch)
+    if not 1 <= count <= n:
+        raise ConfigError(f"cannot split {n} examples into {count} shards")
+    cuts = [n * i // count for i in range(count + 1)]
+    return [Batch(batch.inputs[a:b], batch.labels[a:b], batch.seed)
+            for a, b in zip(cuts[:-1], cuts[1:])]
+
+
+def fisher_sharded(shards: Sequence[Session], net: Network,
+                   precision: int = Precision.FP32) -> FisherReport:
+    """fisher_potential (I/nnet.hpp:321-350) with the batch split over
+    ``shards`` (sessions on distinct contexts -- normally one per GPU --
+    holding consecutive slices of one batch, see shard_batch).  The report is
+    bitwise that of one session holding the whole batch."""
+    h = net.c_struct()
+    out, pc, pl, pr = _fisher_buffers(net, sum(s.n for s in shards))
+    sp = (C.c_void_p * len(shards))(*[s.ptr for s in shards])
+    _check(abi.load().nb_fisher_sharded(sp, len(shards), C.byref(h.c), h.wptr(), precision,
+                                        C.byref(out)))
+    return _report(net, out, pc, pl, pr)
+
+
 @dataclass
 class EvalStats:
     evaluated: int

@@ -128,16 +128,23 @@ int pick_bn(int n_per_group, bool split3) {
   return 0;
 }
 
+// M tiles of a tensor-core launch over `nimg` images (plan_tiles' count).
+int m_tiles_at(int OH, int OW, int64_t nimg, int S) {
+  tc::TcArgs t{};
+  tc::plan_tiles(OH, OW, int(nimg), S, t);
+  return t.m_tiles;
+}
+
 // Split-K factor of a tensor-core launch: when its output tiles cannot fill
 // one wave of SMs, divide the K blocks (taps x 32-channel chunks, at least 4
 // per split) so that tiles x splits still fits in one wave.
-int choose_ksplit(const tc::TcArgs& t, int num_sms, bool pair) {
+int choose_ksplit(const tc::TcArgs& t, int m_tiles, int num_sms, bool pair) {
   static const int mode = [] {  // NB_TC_KSPLIT=0: never split K (experiments)
     const char* e = std::getenv("NB_TC_KSPLIT");
     return e ? std::atoi(e) : 1;
   }();
   if (!mode) return 1;
-  const int tiles = t.nphase * (pair ? (t.m_tiles + 1) / 2 : t.m_tiles) * t.n_tiles;
+  const int tiles = t.nphase * (pair ? (m_tiles + 1) / 2 : m_tiles) * t.n_tiles;
   if (pair) num_sms /= 2;
   int mink = 1 << 30;
   for (int p = 0; p < t.nphase; ++p) mink = std::min(mink, t.ntaps[p] * t.a_cblocks);
@@ -266,7 +273,8 @@ void dgrad_phases(const ConvGeom& g, tc::TcArgs& t) {
 // tcgen05 implicit GEMM when the range is tensor-core shaped (32-channel K
 // chunks, 16-aligned N), the direct FFMA kernels otherwise -- plus packed-
 // weight, activation and Fisher-partial arena offsets.
-NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int64_t plan_n) {
+  if (plan_n <= 0) plan_n = n;
   NetPlan P;
   const bool tc_on = prec != NB_PREC_SIMT;
   P.split3 = prec == NB_PREC_FP32;
@@ -309,8 +317,12 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
+          // launch-shape decisions are made at the planning batch size, so an
+          // example shard runs the whole batch's kernels (same split-K, so
+          // the same summation order per output)
+          const int mt = m_tiles_at(g.OH, g.OW, plan_n, g.S);
           const bool kwf = r.groups == 1 && use_kwf(g, r.slice_co, t.BW);
-          const int pbn = kwf ? 0 : pick_pair_bn(r.slice_co, t.m_tiles, P.split3);
+          const int pbn = kwf ? 0 : pick_pair_bn(r.slice_co, mt, P.split3);
           const int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
           if (bn) {
             t.mode = 0;
@@ -328,8 +340,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = r.slice_co;
-            const bool mc = use_mc(bn, t.m_tiles, pbn != 0, kwf);
-            t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
+            const bool mc = use_mc(bn, mt, pbn != 0, kwf);
+            t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
@@ -356,8 +368,9 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
+        const int mt = m_tiles_at(gh, gw, plan_n, 1);
         const bool kwf = r.groups == 1 && use_kwf(g, r.slice_ci, t.BW);
-        const int pbn = kwf ? 0 : pick_pair_bn(r.slice_ci, t.m_tiles * t.nphase, P.split3);
+        const int pbn = kwf ? 0 : pick_pair_bn(r.slice_ci, mt * t.nphase, P.split3);
         const int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
         if (bn) {
           t.mode = 1;
@@ -376,8 +389,8 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms) {
           t.out_c_base = 0;
           t.out_c_per_group = r.slice_ci;
           t.part_ld = g.Ci;
-          const bool mc = use_mc(bn, t.m_tiles, pbn != 0, kwf);
-          t.ksplit = choose_ksplit(t, num_sms, pbn != 0 || mc);
+          const bool mc = use_mc(bn, mt, pbn != 0, kwf);
+          t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
           // split-K dgrad: k_splitk_epilogue writes one partial per image
           t.part_tiles_per_img =
               t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
@@ -685,7 +698,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     c->prof.host(name, std::chrono::duration<double, std::milli>(now - tp).count());
     tp = now;
   };
-  NetPlan P = lower(net, N, prec, c->num_sms);
+  NetPlan P = lower(net, N, prec, c->num_sms, out.grad_n > 0 ? out.grad_n : N);
   const bool want_grads = out.grads != nullptr;
   phase("host_lower");
 
@@ -787,6 +800,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   HeadArgs ha{};
   ha.act = act + last.act_off;
   ha.N = int(N);
+  ha.grad_n = double(out.grad_n > 0 ? out.grad_n : N);
   ha.HW = last.geom.OH * last.geom.OW;
   ha.C = last.geom.Co;
   ha.K = int(K);
@@ -824,14 +838,15 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     int max_c = 1;
     for (int64_t l = 0; l < L; ++l) {
       const LayerPlan& lp = P.layers[l];
-      ht[l] = FisherLayer{part + lp.part_off, lp.geom.Co, lp.tiles, off};
+      ht[l] = FisherLayer{part + lp.part_off, lp.geom.Co, lp.tiles, off,
+                          int64_t(lp.tiles) * lp.geom.Co};
       off += lp.geom.Co;
       max_c = std::max(max_c, lp.geom.Co);
     }
     NB_CUDA(cudaMemcpyAsync(d_ftab, ht, size_t(L) * sizeof(FisherLayer),
                             cudaMemcpyHostToDevice, st));
     c->prof.begin(st);
-    launch_fisher_reduce(d_ftab, int(L), max_c, int(N), d_perch, st);
+    launch_fisher_reduce(d_ftab, int(L), max_c, int(N), d_perch, out.s_dev, P.ch_total, st);
     c->prof.end(st, "fisher_reduce", 0.0, 8.0 * double(P.part_total));
     c->launches++;
   }
@@ -1214,6 +1229,117 @@ nb_status nb_session_fisher(nb_session* s, const nb_network* net, const nb_weigh
     ro.probs = out->probs;
     run_network(s, d, w, prec, true, ro);
     out->seed = s->seed;
+  });
+}
+
+// fisher_potential (I/nnet.hpp:321-350) of one network over a batch split
+// into consecutive example shards, one session (normally one GPU) each --
+// SURVEY 8(e)'s secondary axis, for when there are fewer networks than GPUs.
+// Every shard plans its launches for the whole batch and divides dz by the
+// whole batch's N, so its per-example sums s_nc are bitwise those of one
+// session holding the whole batch.  They are gathered into shards[0]'s GPU
+// (peer copies over NVLink) and reduced there by k_fisher_reduce in the same
+// fixed order; loss and probabilities are concatenated in example order.
+nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count, const nb_network* net,
+                            const nb_weights* w, nb_precision prec, nb_fisher_out* out) {
+  return guard([&] {
+    need(shards, "shards");
+    need(out, "output");
+    if (count < 1) fail(NB_ERR_CONFIG, "need at least one shard");
+    NetDesc d = NetDesc::from(net);
+    int64_t n_all = 0;
+    for (int32_t i = 0; i < count; ++i) {
+      need(shards[i], "shard session");
+      for (int32_t j = 0; j < i; ++j)
+        if (shards[j]->ctx == shards[i]->ctx)
+          fail(NB_ERR_CONFIG, "example shards must use distinct contexts");
+      if (shards[i]->seed != shards[0]->seed)
+        fail(NB_ERR_CONFIG, "example shards must hold slices of one batch (same seed)");
+      n_all += shards[i]->n;
+    }
+    const int64_t L = d.L(), K = d.num_classes;
+    int64_t ch_total = 0;
+    for (int64_t l = 0; l < L; ++l) ch_total += d.specs[l].co_eff();
+    nb_ctx* root = shards[0]->ctx;
+    {
+      std::lock_guard<std::recursive_mutex> lk(root->mu);
+      ctx_activate(root);
+      root->shard_s.ensure(size_t(n_all * ch_total) * 8);
+    }
+    std::vector<double> ex_loss(static_cast<size_t>(n_all));
+    std::vector<Pending> pend(static_cast<size_t>(count));
+    std::vector<int64_t> first(static_cast<size_t>(count));
+    int64_t n0 = 0;
+    for (int32_t i = 0; i < count; ++i) {
+      nb_session* sh = shards[i];
+      first[size_t(i)] = n0;
+      double* s_dev = root->shard_s.as<double>();
+      if (i > 0) {
+        std::lock_guard<std::recursive_mutex> lk(sh->ctx->mu);
+        ctx_activate(sh->ctx);
+        sh->ctx->shard_s.ensure(size_t(sh->n * ch_total) * 8);
+        s_dev = sh->ctx->shard_s.as<double>();
+      }
+      RunOut ro;
+      ro.probs = out->probs ? out->probs + n0 * K : nullptr;
+      ro.ex_loss = ex_loss.data() + n0;
+      ro.grad_n = n_all;
+      ro.s_dev = s_dev;
+      run_enqueue(sh, d, w, prec, true, ro, pend[size_t(i)]);
+      n0 += sh->n;
+    }
+    for (auto& p : pend) run_finish(p);
+    double lsum = 0.0;
+    for (double v : ex_loss) lsum += v;
+    out->loss = lsum / double(n_all);
+    out->seed = shards[0]->seed;
+
+    std::lock_guard<std::recursive_mutex> lk(root->mu);
+    ctx_activate(root);
+    cudaStream_t st = root->stream;
+    double* S = root->shard_s.as<double>();
+    for (int32_t i = 1; i < count; ++i) {
+      nb_ctx* c = shards[i]->ctx;
+      NB_CUDA(cudaMemcpyPeerAsync(S + first[size_t(i)] * ch_total, root->device, c->shard_s.p,
+                                  c->device, size_t(shards[i]->n * ch_total) * 8, st));
+    }
+    // the gathered s_nc as one-tile partials: s = 0 - (s_nc) per example,
+    // squared exactly as the unsharded reduction squares s_nc
+    root->shard_aux.ensure(size_t(L) * sizeof(FisherLayer) + size_t(ch_total) * 8);
+    root->host_io.ensure(size_t(L) * sizeof(FisherLayer) + size_t(ch_total) * 8);
+    FisherLayer* ht = root->host_io.as<FisherLayer>();
+    int64_t off = 0;
+    int max_c = 1;
+    std::vector<int64_t> co(static_cast<size_t>(L));
+    for (int64_t l = 0; l < L; ++l) {
+      const int c = int(d.specs[l].co_eff());
+      ht[l] = FisherLayer{S + off, c, 1, off, ch_total};
+      co[size_t(l)] = c;
+      off += c;
+      max_c = std::max(max_c, c);
+    }
+    FisherLayer* d_tab = root->shard_aux.as<FisherLayer>();
+    double* d_pc = reinterpret_cast<double*>(d_tab + L);
+    NB_CUDA(cudaMemcpyAsync(d_tab, ht, size_t(L) * sizeof(FisherLayer), cudaMemcpyHostToDevice,
+                            st));
+    launch_fisher_reduce(d_tab, int(L), max_c, int(n_all), d_pc, nullptr, 0, st);
+    root->launches++;
+    double* h_pc = reinterpret_cast<double*>(ht + L);
+    NB_CUDA(cudaMemcpyAsync(h_pc, d_pc, size_t(ch_total) * 8, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaGetLastError());
+    NB_CUDA(cudaStreamSynchronize(st));
+    // per_layer / total in the reference's order (I/nnet.hpp:345-349)
+    double tot = 0.0;
+    int64_t o = 0;
+    for (int64_t l = 0; l < L; ++l) {
+      double layer = 0.0;
+      for (int64_t ch = 0; ch < co[size_t(l)]; ++ch) layer += h_pc[o + ch];
+      if (out->per_layer) out->per_layer[l] = layer;
+      o += co[size_t(l)];
+      tot += layer;
+    }
+    if (out->per_channel) std::memcpy(out->per_channel, h_pc, size_t(ch_total) * 8);
+    out->total = tot;
   });
 }
 

@@ -79,7 +79,10 @@ struct NetPlan {
   bool split3 = false;    // 3xTF32 tensor-core numerics (NB_PREC_FP32)
 };
 
-NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms = 148);
+// plan_n: the batch size launch shapes are chosen for (0 = n; an example
+// shard passes the whole batch's size)
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms = 148,
+              int64_t plan_n = 0);
 
 struct KStat {
   int64_t launches = 0;
@@ -127,6 +130,7 @@ struct nb_ctx {
   std::recursive_mutex mu;
   nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws, tilecnt, trace;
   nb::DevBuf legal;  // semantic-legality workspace (legality.cu)
+  nb::DevBuf shard_s, shard_aux;  // example-sharded Fisher (nb_fisher_sharded)
   int num_sms = 148;
   nb::PinnedBuf host_io, host_out;
   // device copies of z streams keyed by (seed, stream index)
@@ -167,6 +171,11 @@ struct RunOut {
   double* loss = nullptr;
   double* acts = nullptr;   // reference layout, see nb_activation_gradients
   double* grads = nullptr;
+  // example sharding (nb_fisher_sharded): the whole batch's size, which dz is
+  // divided by and the lowering plans for (0 = this session's own N), and a
+  // device buffer receiving s_nc as [n][ch_total] doubles (nullable)
+  int64_t grad_n = 0;
+  double* s_dev = nullptr;
 };
 
 // An evaluation enqueued on its session's stream, not yet collected.

@@ -96,6 +96,7 @@ void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st);
 struct HeadArgs {
   const float* act;  // (N, HW, C) last layer output
   int N, HW, C, K;
+  double grad_n;  // the batch size dz is divided by (the global N when sharded)
   const double* head_src;  // K x C source (z-stream or explicit)
   double head_scale;
   const int32_t* labels;
@@ -110,11 +111,14 @@ struct HeadArgs {
 void launch_head(const HeadArgs& a, cudaStream_t st);
 // Fisher reduction: per (layer, channel) delta = sum_n (sum_tiles partial)^2 / (2N).
 struct FisherLayer {
-  const double* partial;
+  const double* partial;  // example n's tile partials at partial + n * nstride
   int C, tiles;
   int64_t out_off;
+  int64_t nstride;
 };
+// s_out (nullable): s_nc stored at s_out[n * s_ld + out_off + c], the
+// per-example sums an example-sharded evaluation gathers to its root.
 void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,
-                          double* per_channel, cudaStream_t st);
+                          double* per_channel, double* s_out, int64_t s_ld, cudaStream_t st);
 
 }  // namespace nb

@@ -708,7 +708,7 @@ __global__ void k_head(HeadArgs a) {
     a.ex_loss[n] = -log(fmax(dz[y], 1e-300));
     for (int k = 0; k < a.K; ++k) a.probs[int64_t(n) * a.K + k] = dz[k];
     dz[y] -= 1.0;
-    for (int k = 0; k < a.K; ++k) dz[k] /= double(a.N);
+    for (int k = 0; k < a.K; ++k) dz[k] /= a.grad_n;
   }
   __syncthreads();
   if (!a.backward) return;
@@ -737,7 +737,8 @@ __global__ void k_head(HeadArgs a) {
 // order), I/nnet.hpp:330-345.  Block = 32 channels x 16 example lanes; the
 // 16 lane sums are combined in a fixed order (deterministic, fp64).
 __global__ void __launch_bounds__(512) k_fisher_reduce(const FisherLayer* __restrict__ layers,
-                                                       int N, double* __restrict__ per_channel) {
+                                                       int N, double* __restrict__ per_channel,
+                                                       double* __restrict__ s_out, int64_t s_ld) {
   __shared__ double red[16][33];
   const FisherLayer L = layers[blockIdx.y];
   const int c = blockIdx.x * 32 + threadIdx.x;
@@ -745,9 +746,10 @@ __global__ void __launch_bounds__(512) k_fisher_reduce(const FisherLayer* __rest
   double acc = 0.0;
   if (c < L.C) {
     for (int n = threadIdx.y; n < N; n += 16) {
-      const double* p = L.partial + int64_t(n) * L.tiles * L.C + c;
+      const double* p = L.partial + int64_t(n) * L.nstride + c;
       double s = 0.0;
       for (int t = 0; t < L.tiles; ++t) s -= p[int64_t(t) * L.C];
+      if (s_out) s_out[int64_t(n) * s_ld + L.out_off + c] = s;
       acc += s * s;
     }
   }
@@ -1061,9 +1063,9 @@ void launch_head(const HeadArgs& a, cudaStream_t st) {
 }
 
 void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,
-                          double* per_channel, cudaStream_t st) {
+                          double* per_channel, double* s_out, int64_t s_ld, cudaStream_t st) {
   dim3 grid((max_c + 31) / 32, L);
-  k_fisher_reduce<<<grid, dim3(32, 16), 0, st>>>(layers_dev, N, per_channel);
+  k_fisher_reduce<<<grid, dim3(32, 16), 0, st>>>(layers_dev, N, per_channel, s_out, s_ld);
 }
 
 }  // namespace nb
