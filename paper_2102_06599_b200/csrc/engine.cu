@@ -128,6 +128,14 @@ int pick_bn(int n_per_group, bool split3) {
   return 0;
 }
 
+// N tile of a padded plan (one group, width a multiple of 16 that no tile
+// divides): the last tile's extra columns are zero weight rows (TMA
+// out-of-bounds fill) the epilogue does not store.
+int pick_bn_padded(int n, bool split3) {
+  if (n % 16) return 0;
+  return n <= 32 ? 32 : n <= 64 ? 64 : split3 ? 128 : (n <= 128 ? 128 : 256);
+}
+
 // M tiles of a tensor-core launch over `nimg` images (plan_tiles' count).
 int m_tiles_at(int OH, int OW, int64_t nimg, int S) {
   tc::TcArgs t{};
@@ -313,8 +321,11 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
       r.wd_off = off;
       off += align64(used);
       lp.family[i] = Family::Direct;
-      if (tc_on && (g.S == 1 || g.S == 2) && r.slice_ci % 32 == 0 && r.b % 16 == 0 &&
-          g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
+      // channel counts off the 32-channel K chunk (e.g. DenseNet's 48-wide
+      // growth) run as padded plans when the layer is one group
+      const bool pad_ok = r.groups == 1 && g.Ci % 4 == 0;
+      if (tc_on && (g.S == 1 || g.S == 2) && (r.slice_ci % 32 == 0 || pad_ok) &&
+          r.b % 16 == 0 && g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
           // launch-shape decisions are made at the planning batch size, so an
@@ -323,18 +334,20 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           const int mt = m_tiles_at(g.OH, g.OW, plan_n, g.S);
           const bool kwf = r.groups == 1 && use_kwf(g, r.slice_co, t.BW);
           const int pbn = kwf ? 0 : pick_pair_bn(r.slice_co, mt, P.split3);
-          const int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
+          int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
+          if (!bn && pad_ok) bn = pick_bn_padded(r.slice_co, P.split3);
+          const int kp = (r.slice_ci + 31) / 32 * 32;
           if (bn) {
             t.mode = 0;
-            t.n_tiles_per_group = r.slice_co / bn;
+            t.n_tiles_per_group = (r.slice_co + bn - 1) / bn;
             t.n_tiles = r.groups * t.n_tiles_per_group;
             t.S = g.S;
             fprop_phase(g, t);
             if (kwf) kwf_taps(g, t, +1);
-            t.a_cblocks = r.slice_ci / 32;
+            t.a_cblocks = kp / 32;
             t.a_c_base = 0;
             t.a_c_per_group = r.slice_ci;
-            t.b_k_per_tap = r.slice_ci;
+            t.b_k_per_tap = kp;
             t.b_row_base = 0;
             t.b_row_per_group = r.slice_co;
             t.out_ld = g.Co;
@@ -350,10 +363,11 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
             tp.mc = mc;
             tp.kwf = kwf;
             tp.tile = t;
-            tp.w_n = align64(used);
+            tp.kp = kp != r.slice_ci ? kp : 0;
+            tp.w_n = align64(int64_t(r.len) * taps * kp);
             tp.w_off = off;
             tp.b_rows = kwf ? g.KW * r.len : r.len;
-            tp.b_k = kwf ? g.KH * r.slice_ci : taps * r.slice_ci;
+            tp.b_k = kwf ? g.KH * r.slice_ci : taps * kp;
             off += 2 * tp.w_n;
             lp.family[i] = Family::TensorCore;
           }
@@ -362,8 +376,10 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
     }
     // dgrad on the tensor cores: stride 1 as one phase, stride 2 as the four
     // sub-pixel phases (a phase grid of ceil(H/2) x ceil(W/2)).
+    const bool dpad_ok = g.r[0].groups == 1 && g.Co % 4 == 0;
     if (l >= 1 && tc_on && g.nranges == 1 && (g.S == 1 || g.S == 2) &&
-        g.r[0].slice_co % 32 == 0 && g.Ci % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
+        (g.r[0].slice_co % 32 == 0 || dpad_ok) && g.Ci % 4 == 0 &&
+        taps <= tc::kMaxPhaseTaps) {
       const RangeDesc& r = g.r[0];
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
@@ -371,18 +387,20 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
         const int mt = m_tiles_at(gh, gw, plan_n, 1);
         const bool kwf = r.groups == 1 && use_kwf(g, r.slice_ci, t.BW);
         const int pbn = kwf ? 0 : pick_pair_bn(r.slice_ci, mt * t.nphase, P.split3);
-        const int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
+        int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
+        if (!bn && dpad_ok) bn = pick_bn_padded(r.slice_ci, P.split3);
+        const int kp = (r.slice_co + 31) / 32 * 32;
         if (bn) {
           t.mode = 1;
-          t.n_tiles_per_group = r.slice_ci / bn;
+          t.n_tiles_per_group = (r.slice_ci + bn - 1) / bn;
           t.n_tiles = r.groups * t.n_tiles_per_group;
           t.S = 1;
           dgrad_phases(g, t);
           if (kwf) kwf_taps(g, t, -1);
-          t.a_cblocks = r.slice_co / 32;
+          t.a_cblocks = kp / 32;
           t.a_c_base = r.b;
           t.a_c_per_group = r.slice_co;
-          t.b_k_per_tap = r.slice_co;
+          t.b_k_per_tap = kp;
           t.b_row_base = 0;
           t.b_row_per_group = r.slice_ci;
           t.out_ld = g.Ci;
@@ -402,10 +420,11 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           tp.mc = mc;
           tp.kwf = kwf;
           tp.tile = t;
-          tp.w_n = align64(int64_t(g.Ci) * taps * r.slice_co);
+          tp.kp = kp != r.slice_co ? kp : 0;
+          tp.w_n = align64(int64_t(g.Ci) * taps * kp);
           tp.w_off = off;
           tp.b_rows = kwf ? g.KW * g.Ci : g.Ci;
-          tp.b_k = kwf ? g.KH * r.slice_co : taps * r.slice_co;
+          tp.b_k = kwf ? g.KH * r.slice_co : taps * kp;
           off += 2 * tp.w_n;
           lp.dgrad_family = Family::TensorCore;
         }
@@ -504,11 +523,16 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
       d.tcf_hi = base + lp.tcf[r].w_off;
       d.tcf_lo = d.tcf_hi + lp.tcf[r].w_n;
       d.kwf_f = lp.tcf[r].kwf ? 1 : 0;
+      d.kpf = lp.tcf[r].kp;
+      if (d.kpf)  // the padded K columns stay zero
+        NB_CUDA(cudaMemsetAsync(d.tcf_hi, 0, size_t(2 * lp.tcf[r].w_n) * 4, st));
     }
     if (r == 0 && lp.dgrad_family == Family::TensorCore) {
       d.tcd_hi = base + lp.tcd.w_off;
       d.tcd_lo = d.tcd_hi + lp.tcd.w_n;
       d.kwf_d = lp.tcd.kwf ? 1 : 0;
+      d.kpd = lp.tcd.kp;
+      if (d.kpd) NB_CUDA(cudaMemsetAsync(d.tcd_hi, 0, size_t(2 * lp.tcd.w_n) * 4, st));
     }
     launch_pack_weights(src, scale, lp.geom, r, d, st);
     c->launches++;

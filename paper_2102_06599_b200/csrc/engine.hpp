@@ -52,6 +52,10 @@ struct TcPlan {
   int64_t w_off = 0;   // hi at w_off, lo at w_off + w_n (floats, layer-relative)
   int64_t w_n = 0;
   int b_rows = 0, b_k = 0;
+  // padded plan: K per tap rounded up to 32-channel chunks (0 = exact); the
+  // packed weights' extra K columns are zero, the activations' extra
+  // channels are TMA out-of-bounds zero fill
+  int kp = 0;
 };
 
 // Lowered layer: geometry + per-range family + packed-weight offsets.

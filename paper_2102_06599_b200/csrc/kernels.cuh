@@ -58,6 +58,8 @@ struct PackDst {
   float* tcd_lo;
   // kw-fused tensor-core layouts (rows kw*width + c, K = kh x channels)
   int kwf_f = 0, kwf_d = 0, KW = 1;
+  // padded K per tap of the fprop / dgrad tensor-core layouts (0 = exact)
+  int kpf = 0, kpd = 0;
 };
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
                          const PackDst& d, cudaStream_t st);

@@ -74,14 +74,16 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     const float hi = __uint_as_float(hb), lo = __uint_as_float(lb);
     const int kh = tap / d.KW, kw = tap - kh * d.KW, KH = taps / d.KW;
     if (d.tcf_hi) {
+      const int kpf = d.kpf ? d.kpf : r.slice_ci;
       const int64_t i = d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
-                                : (int64_t(co_local) * taps + tap) * r.slice_ci + j;
+                                : (int64_t(co_local) * taps + tap) * kpf + j;
       d.tcf_hi[i] = hi;
       d.tcf_lo[i] = lo;
     }
     if (d.tcd_hi) {
+      const int kpd = d.kpd ? d.kpd : r.slice_co;
       const int64_t i = d.kwf_d ? ((int64_t(kw) * Ci + ci) * KH + kh) * r.slice_co + t
-                                : (int64_t(ci) * taps + tap) * r.slice_co + t;
+                                : (int64_t(ci) * taps + tap) * kpd + t;
       d.tcd_hi[i] = hi;
       d.tcd_lo[i] = lo;
     }

@@ -675,6 +675,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       const int64_t pix =
           (int64_t(n) * a.OutH + oh * a.PS + a.py[ph]) * a.OutW + ow * a.PS + a.px[ph];
       const int col0 = a.out_c_base + g * a.out_c_per_group + nn * BN;
+      // columns of this N tile that exist (a padded plan's last tile is
+      // narrower than BN; 16-column granularity)
+      const int nlim = KWF ? BN : a.out_c_per_group - nn * BN;
       const bool empty_phase = a.ntaps[ph] == 0;
       const int tile_in_img = ph * part_per_phase + (a.BNI == 1 ? hb * a.tiles_w + wb : 0);
       const bool tile_real = m < a.m_tiles;
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
+          if (c >= nlim) break;
           // transpose this chunk's A_prev rows into registers (own row)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
             av[4 * i + 3] = t.w;
           }
           __syncwarp();
-          if (c + 16 < BN && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
+          if (c + 16 < BN && c + 16 < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
@@ -824,7 +828,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           for (int idx = r; idx < a.BNI * BN; idx += 128) {
             const int img = idx / BN, j = idx % BN;
             const int nimg = nb * a.BNI + img;
-            if (nimg < a.nimg) {
+            if (nimg < a.nimg && j < nlim) {
               float sum = 0.f;
               for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red[w * BN + j];
               a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld + col0 +
@@ -836,6 +840,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       }
 #pragma unroll 1
       for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
+        if (c >= nlim) break;
         float v[16];
         acc_ld16(c, v);
         if (empty_phase) {

@@ -262,6 +262,17 @@ TC_SPECS = [
     ConvSpec(64, 64, 8, 8, 3, 3, 1, 1),                        # kw-fused, 8-pixel rows (4 per warp)
     ConvSpec(128, 64, 6, 16, 3, 3, 1, 1),                      # kw-fused, 16-pixel rows, partial tiles
 ]
+# padded plans: K per tap rounded up to 32-channel chunks (TMA zero fill),
+# the last N tile narrower than BN (DenseNet's 48-channel growth)
+PAD_SPECS = [
+    ConvSpec(144, 192, 8, 8, 1, 1, 1, 0),                      # K 144 -> 160
+    ConvSpec(192, 48, 8, 8, 3, 3, 1, 1),                       # N 48 of 64; dgrad K 48 -> 64
+    ConvSpec(48, 80, 16, 16, 3, 3, 2, 1),                      # both padded, stride 2
+    ConvSpec(20, 16, 7, 7, 3, 3, 1, 1),                        # K 20 -> 32, N 16 of 32
+    ConvSpec(64, 48, 8, 8, 3, 3, 1, 1,
+             channel_splits=[ChannelSplit(0, 16, 1), ChannelSplit(16, 48, 1)]),  # padded range
+]
+TC_SPECS += PAD_SPECS
 
 
 @pytest.mark.parametrize("prec", [Precision.FP32, Precision.TF32])
@@ -277,6 +288,23 @@ def test_tc_conv_integer_exact(ctx, oracle, spec, prec):
     for i in range(n):
         want = oracle.conv(spec, x[i].astype(np.int64), w.astype(np.int64))
         assert np.array_equal(y[i], want.astype(np.float64)), i
+
+
+@pytest.mark.parametrize("spec", PAD_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}")
+def test_padded_specs_run_on_tensor_cores(spec):
+    """The padded shapes are lowered to the tcgen05 kernel, not the FFMA
+    fallback (fprop; dgrad too where Ci is a multiple of 16)."""
+    c = nb.Context(0)
+    net = Network([Layer(ConvSpec(spec.ci, spec.ci, spec.h, spec.w, 1, 1, 1, 0)), Layer(spec)],
+                  num_classes=10, seed=3)
+    s = nb.Session(net, nb.make_batch(net, 4, 1), ctx=c)
+    c.set_profiling(True)
+    s.fisher(net)
+    names = set(c.kernel_stats())
+    assert "conv_fprop_tc_3xtf32" in names, names
+    if spec.ci % 16 == 0 and not spec.channel_splits:
+        assert "conv_dgrad_tc_3xtf32_fisher" in names, names
+        assert "conv_dgrad_direct_fisher" not in names, names
 
 
 @pytest.mark.parametrize("spec", TC_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}g{s.groups}")
