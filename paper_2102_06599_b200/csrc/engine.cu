@@ -136,6 +136,22 @@ int pick_bn_padded(int n, bool split3) {
   return n <= 32 ? 32 : n <= 64 ? 64 : split3 ? 128 : (n <= 128 ? 128 : 256);
 }
 
+// A grouped range whose slices miss the 32-channel K chunk runs as one dense
+// GEMM over block-diagonal weights when it has at most 8 groups (NB_TC_DENSE
+// sets the cap; 0 = never): G x the MACs on the tensor pipe still beat the
+// FFMA kernels' 5-15 TFLOP/s.
+int dense_cap() {
+  static const int cap = [] {
+    const char* e = std::getenv("NB_TC_DENSE");
+    return e ? std::atoi(e) : 8;
+  }();
+  return cap;
+}
+bool use_dense(const RangeDesc& r, int64_t Ci) {
+  return r.groups > 1 && r.groups <= dense_cap() && r.slice_ci % 32 != 0 && Ci % 4 == 0 &&
+         r.len % 16 == 0;
+}
+
 // M tiles of a tensor-core launch over `nimg` images (plan_tiles' count).
 int m_tiles_at(int OH, int OW, int64_t nimg, int S) {
   tc::TcArgs t{};
@@ -322,9 +338,15 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
       off += align64(used);
       lp.family[i] = Family::Direct;
       // channel counts off the 32-channel K chunk (e.g. DenseNet's 48-wide
-      // growth) run as padded plans when the layer is one group
-      const bool pad_ok = r.groups == 1 && g.Ci % 4 == 0;
-      if (tc_on && (g.S == 1 || g.S == 2) && (r.slice_ci % 32 == 0 || pad_ok) &&
+      // growth) run as padded plans when the layer is one group; a few groups
+      // of narrow slices run as one dense GEMM over block-diagonal weights
+      // (G x the MACs, on the tensor pipe instead of FFMA)
+      const bool dense = use_dense(r, g.Ci);
+      const int G = dense ? 1 : r.groups;
+      const int sci = dense ? int(g.Ci) : r.slice_ci;
+      const int sco = dense ? r.len : r.slice_co;
+      const bool pad_ok = G == 1 && g.Ci % 4 == 0;
+      if (tc_on && (g.S == 1 || g.S == 2) && (sci % 32 == 0 || pad_ok) &&
           r.b % 16 == 0 && g.Co % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
         tc::TcArgs t{};
         if (tc::plan_tiles(g.OH, g.OW, g.N, g.S, t)) {
@@ -332,27 +354,27 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           // example shard runs the whole batch's kernels (same split-K, so
           // the same summation order per output)
           const int mt = m_tiles_at(g.OH, g.OW, plan_n, g.S);
-          const bool kwf = r.groups == 1 && use_kwf(g, r.slice_co, t.BW);
-          const int pbn = kwf ? 0 : pick_pair_bn(r.slice_co, mt, P.split3);
-          int bn = pbn ? pbn : pick_bn(r.slice_co, P.split3);
-          if (!bn && pad_ok) bn = pick_bn_padded(r.slice_co, P.split3);
-          const int kp = (r.slice_ci + 31) / 32 * 32;
+          const bool kwf = G == 1 && !dense && use_kwf(g, sco, t.BW);
+          const int pbn = kwf ? 0 : pick_pair_bn(sco, mt, P.split3);
+          int bn = pbn ? pbn : pick_bn(sco, P.split3);
+          if (!bn && pad_ok) bn = pick_bn_padded(sco, P.split3);
+          const int kp = (sci + 31) / 32 * 32;
           if (bn) {
             t.mode = 0;
-            t.n_tiles_per_group = (r.slice_co + bn - 1) / bn;
-            t.n_tiles = r.groups * t.n_tiles_per_group;
+            t.n_tiles_per_group = (sco + bn - 1) / bn;
+            t.n_tiles = G * t.n_tiles_per_group;
             t.S = g.S;
             fprop_phase(g, t);
             if (kwf) kwf_taps(g, t, +1);
             t.a_cblocks = kp / 32;
             t.a_c_base = 0;
-            t.a_c_per_group = r.slice_ci;
+            t.a_c_per_group = sci;
             t.b_k_per_tap = kp;
             t.b_row_base = 0;
-            t.b_row_per_group = r.slice_co;
+            t.b_row_per_group = sco;
             t.out_ld = g.Co;
             t.out_c_base = r.b;
-            t.out_c_per_group = r.slice_co;
+            t.out_c_per_group = sco;
             const bool mc = use_mc(bn, mt, pbn != 0, kwf);
             t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
             if (t.ksplit > 1)
@@ -363,11 +385,13 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
             tp.mc = mc;
             tp.kwf = kwf;
             tp.tile = t;
-            tp.kp = kp != r.slice_ci ? kp : 0;
+            tp.kp = kp != sci ? kp : 0;
+            tp.dense = dense ? r.groups : 0;
+            tp.hw_chunks = t.ksplit > 1 ? splitk_hw_chunks(plan_n, g.OH * g.OW, r.len) : 1;
             tp.w_n = align64(int64_t(r.len) * taps * kp);
             tp.w_off = off;
             tp.b_rows = kwf ? g.KW * r.len : r.len;
-            tp.b_k = kwf ? g.KH * r.slice_ci : taps * kp;
+            tp.b_k = kwf ? g.KH * sci : taps * kp;
             off += 2 * tp.w_n;
             lp.family[i] = Family::TensorCore;
           }
@@ -376,42 +400,50 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
     }
     // dgrad on the tensor cores: stride 1 as one phase, stride 2 as the four
     // sub-pixel phases (a phase grid of ceil(H/2) x ceil(W/2)).
-    const bool dpad_ok = g.r[0].groups == 1 && g.Co % 4 == 0;
+    // (a grouped layer whose slices do not tile the GEMM densifies as in fprop)
+    const RangeDesc& r0 = g.r[0];
+    const bool ddense = g.nranges == 1 && r0.groups > 1 && r0.groups <= dense_cap() &&
+                        (r0.slice_co % 32 != 0 || !pick_bn(r0.slice_ci, P.split3)) &&
+                        g.Co % 4 == 0 && g.Ci % 16 == 0;
+    const int DG = ddense ? 1 : r0.groups;
+    const int dsci = ddense ? int(g.Ci) : r0.slice_ci;
+    const int dsco = ddense ? r0.len : r0.slice_co;
+    const bool dpad_ok = DG == 1 && g.Co % 4 == 0;
     if (l >= 1 && tc_on && g.nranges == 1 && (g.S == 1 || g.S == 2) &&
-        (g.r[0].slice_co % 32 == 0 || dpad_ok) && g.Ci % 4 == 0 &&
-        taps <= tc::kMaxPhaseTaps) {
+        (dsco % 32 == 0 || dpad_ok) && g.Ci % 4 == 0 && taps <= tc::kMaxPhaseTaps) {
       const RangeDesc& r = g.r[0];
       tc::TcArgs t{};
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
         const int mt = m_tiles_at(gh, gw, plan_n, 1);
-        const bool kwf = r.groups == 1 && use_kwf(g, r.slice_ci, t.BW);
-        const int pbn = kwf ? 0 : pick_pair_bn(r.slice_ci, mt * t.nphase, P.split3);
-        int bn = pbn ? pbn : pick_bn(r.slice_ci, P.split3);
-        if (!bn && dpad_ok) bn = pick_bn_padded(r.slice_ci, P.split3);
-        const int kp = (r.slice_co + 31) / 32 * 32;
+        const bool kwf = DG == 1 && !ddense && use_kwf(g, dsci, t.BW);
+        const int pbn = kwf ? 0 : pick_pair_bn(dsci, mt * t.nphase, P.split3);
+        int bn = pbn ? pbn : pick_bn(dsci, P.split3);
+        if (!bn && dpad_ok) bn = pick_bn_padded(dsci, P.split3);
+        const int kp = (dsco + 31) / 32 * 32;
         if (bn) {
           t.mode = 1;
-          t.n_tiles_per_group = (r.slice_ci + bn - 1) / bn;
-          t.n_tiles = r.groups * t.n_tiles_per_group;
+          t.n_tiles_per_group = (dsci + bn - 1) / bn;
+          t.n_tiles = DG * t.n_tiles_per_group;
           t.S = 1;
           dgrad_phases(g, t);
           if (kwf) kwf_taps(g, t, -1);
           t.a_cblocks = kp / 32;
           t.a_c_base = r.b;
-          t.a_c_per_group = r.slice_co;
+          t.a_c_per_group = dsco;
           t.b_k_per_tap = kp;
           t.b_row_base = 0;
-          t.b_row_per_group = r.slice_ci;
+          t.b_row_per_group = dsci;
           t.out_ld = g.Ci;
           t.out_c_base = 0;
-          t.out_c_per_group = r.slice_ci;
+          t.out_c_per_group = dsci;
           t.part_ld = g.Ci;
           const bool mc = use_mc(bn, mt, pbn != 0, kwf);
           t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
-          // split-K dgrad: k_splitk_epilogue writes one partial per image
+          // split-K dgrad: k_splitk_epilogue writes one partial per (image, pixel chunk)
+          const int hw_chunks = t.ksplit > 1 ? splitk_hw_chunks(plan_n, g.H * g.W, g.Ci) : 1;
           t.part_tiles_per_img =
-              t.ksplit > 1 ? 1 : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
+              t.ksplit > 1 ? hw_chunks : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
           if (t.ksplit > 1)
             P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
@@ -420,11 +452,13 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           tp.mc = mc;
           tp.kwf = kwf;
           tp.tile = t;
-          tp.kp = kp != r.slice_co ? kp : 0;
+          tp.kp = kp != dsco ? kp : 0;
+          tp.dense = ddense ? r.groups : 0;
+          tp.hw_chunks = hw_chunks;
           tp.w_n = align64(int64_t(g.Ci) * taps * kp);
           tp.w_off = off;
           tp.b_rows = kwf ? g.KW * g.Ci : g.Ci;
-          tp.b_k = kwf ? g.KH * r.slice_co : taps * kp;
+          tp.b_k = kwf ? g.KH * dsco : taps * kp;
           off += 2 * tp.w_n;
           lp.dgrad_family = Family::TensorCore;
         }
@@ -496,11 +530,12 @@ std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) 
          std::to_string(int(lp.family[r]));
     if (lp.family[r] == Family::TensorCore)
       k += "," + std::to_string(lp.tcf[r].w_off) + "," + std::to_string(lp.tcf[r].w_n) +
-           (lp.tcf[r].kwf ? "k" : "");
+           (lp.tcf[r].kwf ? "k" : "") + (lp.tcf[r].dense ? "D" : "") +
+           (lp.tcf[r].kp ? "p" : "");
   }
   if (lp.dgrad_family == Family::TensorCore)
     k += "|d" + std::to_string(lp.tcd.w_off) + "," + std::to_string(lp.tcd.w_n) +
-         (lp.tcd.kwf ? "k" : "");
+         (lp.tcd.kwf ? "k" : "") + (lp.tcd.dense ? "D" : "") + (lp.tcd.kp ? "p" : "");
   return k;
 }
 
@@ -523,16 +558,18 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
       d.tcf_hi = base + lp.tcf[r].w_off;
       d.tcf_lo = d.tcf_hi + lp.tcf[r].w_n;
       d.kwf_f = lp.tcf[r].kwf ? 1 : 0;
-      d.kpf = lp.tcf[r].kp;
-      if (d.kpf)  // the padded K columns stay zero
+      d.kpf = lp.tcf[r].tile.b_k_per_tap;  // K per tap of the layout (padded / dense)
+      d.dense_f = lp.tcf[r].dense ? 1 : 0;
+      if (d.kpf || d.dense_f)  // the padded K columns / off-diagonal blocks stay zero
         NB_CUDA(cudaMemsetAsync(d.tcf_hi, 0, size_t(2 * lp.tcf[r].w_n) * 4, st));
     }
     if (r == 0 && lp.dgrad_family == Family::TensorCore) {
       d.tcd_hi = base + lp.tcd.w_off;
       d.tcd_lo = d.tcd_hi + lp.tcd.w_n;
       d.kwf_d = lp.tcd.kwf ? 1 : 0;
-      d.kpd = lp.tcd.kp;
-      if (d.kpd) NB_CUDA(cudaMemsetAsync(d.tcd_hi, 0, size_t(2 * lp.tcd.w_n) * 4, st));
+      d.kpd = lp.tcd.tile.b_k_per_tap;
+      d.dense_d = lp.tcd.dense ? 1 : 0;
+      if (d.kpd || d.dense_d) NB_CUDA(cudaMemsetAsync(d.tcd_hi, 0, size_t(2 * lp.tcd.w_n) * 4, st));
     }
     launch_pack_weights(src, scale, lp.geom, r, d, st);
     c->launches++;
@@ -638,6 +675,7 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
         e.C = rd.len;
         e.out = y;
         e.relu = relu ? 1 : 0;
+        e.hw_chunks = lp.tcf[r].hw_chunks;
         launch_splitk_epilogue(e, st);
         c->launches++;
       }
@@ -688,6 +726,7 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       e.g_out = g_out;
       e.partial = partial;
       e.relu_prev = relu_prev ? 1 : 0;
+      e.hw_chunks = lp.tcd.hw_chunks;
       launch_splitk_epilogue(e, st);
       c->launches++;
     }

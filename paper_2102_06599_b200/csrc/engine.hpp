@@ -56,6 +56,11 @@ struct TcPlan {
   // packed weights' extra K columns are zero, the activations' extra
   // channels are TMA out-of-bounds zero fill
   int kp = 0;
+  // densified grouped range: the original group count (0 = not densified);
+  // the packed weights are block-diagonal over the full channel range
+  int dense = 0;
+  // split-K epilogue pixel chunks (splitk_hw_chunks at the planning batch)
+  int hw_chunks = 1;
 };
 
 // Lowered layer: geometry + per-range family + packed-weight offsets.

@@ -60,6 +60,9 @@ struct PackDst {
   int kwf_f = 0, kwf_d = 0, KW = 1;
   // padded K per tap of the fprop / dgrad tensor-core layouts (0 = exact)
   int kpf = 0, kpd = 0;
+  // densified grouped layouts: K indexed by the full input (fprop) / range
+  // output (dgrad) channel instead of the slice-local one
+  int dense_f = 0, dense_d = 0;
 };
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
                          const PackDst& d, cudaStream_t st);
@@ -90,8 +93,14 @@ struct SplitEpi {
   float* g_out;
   double* partial;
   int relu_prev;
+  // pixel chunks per image (grid z): enough blocks for small batches; a
+  // dgrad writes one Fisher partial per (image, chunk)
+  int hw_chunks = 1;
 };
 void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st);
+// Pixel chunks of a split-K epilogue over n images of HW pixels x C channels
+// (a function of the shape only, so plans and launches agree).
+int splitk_hw_chunks(int64_t n, int HW, int C);
 
 // GAP + linear head + softmax-CE (+ backward, + last-layer Fisher partial,
 // + the masked head gradient dpre of the last layer).

@@ -76,14 +76,14 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     if (d.tcf_hi) {
       const int kpf = d.kpf ? d.kpf : r.slice_ci;
       const int64_t i = d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
-                                : (int64_t(co_local) * taps + tap) * kpf + j;
+                                : (int64_t(co_local) * taps + tap) * kpf + (d.dense_f ? ci : j);
       d.tcf_hi[i] = hi;
       d.tcf_lo[i] = lo;
     }
     if (d.tcd_hi) {
       const int kpd = d.kpd ? d.kpd : r.slice_co;
       const int64_t i = d.kwf_d ? ((int64_t(kw) * Ci + ci) * KH + kh) * r.slice_co + t
-                                : (int64_t(ci) * taps + tap) * kpd + t;
+                                : (int64_t(ci) * taps + tap) * kpd + (d.dense_d ? co_local : t);
       d.tcd_hi[i] = hi;
       d.tcd_lo[i] = lo;
     }
@@ -672,18 +672,37 @@ __global__ void __launch_bounds__(256) k_dgrad_direct(
 
 // One block per example; fp64 throughout (head_logits/softmax/CE,
 // I/nnet.hpp:152-194; dz/dpool/g[L-1], I/nnet.hpp:209-224).
-__global__ void k_head(HeadArgs a) {
+__global__ void __launch_bounds__(512) k_head(HeadArgs a) {
   extern __shared__ double sm[];
   double* pooled = sm;            // C
   double* dpool = sm + a.C;       // C
   double* z = sm + 2 * a.C;       // K
   double* dz = z + a.K;           // K
+  double* rsum = dz + a.K;        // blockDim: per-(row group, channel) partial sums
   const int n = blockIdx.x;
   const float* act = a.act + int64_t(n) * a.HW * a.C;
-  for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < a.HW; ++j) s += double(act[int64_t(j) * a.C + i]);
-    pooled[i] = s / double(a.HW);
+  // narrow layers (C < blockDim): R row groups per channel, combined in
+  // group order, so a small batch still keeps every thread busy
+  const int R = a.C < int(blockDim.x) ? int(blockDim.x) / a.C : 1;
+  const int rg = int(threadIdx.x) / a.C, rc = int(threadIdx.x) % a.C;
+  if (R > 1) {
+    if (rg < R) {
+      double s = 0.0;
+      for (int j = rg; j < a.HW; j += R) s += double(act[int64_t(j) * a.C + rc]);
+      rsum[rg * a.C + rc] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+      double s = 0.0;
+      for (int q = 0; q < R; ++q) s += rsum[q * a.C + i];
+      pooled[i] = s / double(a.HW);
+    }
+  } else {
+    for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < a.HW; ++j) s += double(act[int64_t(j) * a.C + i]);
+      pooled[i] = s / double(a.HW);
+    }
   }
   __syncthreads();
   // logits: one warp per class, lanes stride the channels, fixed-order
@@ -720,6 +739,29 @@ __global__ void k_head(HeadArgs a) {
     dpool[i] = s;
   }
   __syncthreads();
+  if (R > 1) {
+    if (rg < R) {
+      const double gv = dpool[rc] / double(a.HW);
+      const float gf = float(gv);
+      double s = 0.0;
+      for (int j = rg; j < a.HW; j += R) {
+        const int64_t idx = (int64_t(n) * a.HW + j) * a.C + rc;
+        const float av = a.act[idx];
+        s += double(av) * gv;
+        if (a.dpre) a.dpre[idx] = (a.relu_last && !(av > 0.f)) ? 0.f : gf;
+        if (a.g_out) a.g_out[idx] = gf;
+      }
+      rsum[rg * a.C + rc] = s;
+    }
+    __syncthreads();
+    if (a.partial)
+      for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < R; ++q) s += rsum[q * a.C + i];
+        a.partial[int64_t(n) * a.C + i] = s;
+      }
+    return;
+  }
   for (int i = threadIdx.x; i < a.C; i += blockDim.x) {
     const double gv = dpool[i] / double(a.HW);
     const float gf = float(gv);
@@ -775,9 +817,10 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int64_t n = blockIdx.y;
+  const int cs = (e.HW + e.hw_chunks - 1) / e.hw_chunks, pend = min(e.HW, int(blockIdx.z + 1) * cs);
   float contrib = 0.f;
   if (c < e.C) {
-    for (int p = threadIdx.y; p < e.HW; p += 8) {
+    for (int p = int(blockIdx.z) * cs + threadIdx.y; p < pend; p += 8) {
       const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
       float v = 0.f;
       for (int k = 0; k < e.ksplit; ++k) v += e.ws[k * e.ws_stride + idx];
@@ -802,7 +845,7 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
-    e.partial[n * e.ld + e.c0 + c] = double(s);
+    e.partial[(n * e.hw_chunks + blockIdx.z) * e.ld + e.c0 + c] = double(s);
   }
 }
 
@@ -817,9 +860,10 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int c = (blockIdx.x * 32 + threadIdx.x) * 4;
   const int64_t n = blockIdx.y;
+  const int cs = (e.HW + e.hw_chunks - 1) / e.hw_chunks, pend = min(e.HW, int(blockIdx.z + 1) * cs);
   float contrib[4] = {0.f, 0.f, 0.f, 0.f};
   if (c < e.C) {
-    for (int p = threadIdx.y; p < e.HW; p += 8) {
+    for (int p = int(blockIdx.z) * cs + threadIdx.y; p < pend; p += 8) {
       const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int k = 0; k < e.ksplit; ++k) {
@@ -868,7 +912,7 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += red[k][t];
-    e.partial[n * e.ld + e.c0 + blockIdx.x * 128 + t] = double(s);
+    e.partial[(n * e.hw_chunks + blockIdx.z) * e.ld + e.c0 + blockIdx.x * 128 + t] = double(s);
   }
 }
 
@@ -1051,17 +1095,26 @@ void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st) {
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   if (e.C % 4 == 0 && e.ld % 4 == 0 && e.c0 % 4 == 0) {
-    cfg.gridDim = dim3((e.C + 127) / 128, e.N);
+    cfg.gridDim = dim3((e.C + 127) / 128, e.N, e.hw_chunks);
     cudaLaunchKernelEx(&cfg, k_splitk_epilogue4, e);
     return;
   }
-  cfg.gridDim = dim3((e.C + 31) / 32, e.N);
+  cfg.gridDim = dim3((e.C + 31) / 32, e.N, e.hw_chunks);
   cudaLaunchKernelEx(&cfg, k_splitk_epilogue, e);
 }
 
+int splitk_hw_chunks(int64_t n, int HW, int C) {
+  // about two blocks per SM, at least 64 pixels per chunk
+  const int64_t base = int64_t((C + 127) / 128) * n;
+  int64_t ch = (2 * 148 + base - 1) / base;
+  const int64_t cap = HW / 64 > 1 ? HW / 64 : 1;
+  return int(ch < 1 ? 1 : (ch > cap ? cap : ch));
+}
+
 void launch_head(const HeadArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (2 * size_t(a.C) + 2 * size_t(a.K));
-  k_head<<<a.N, 256, smem, st>>>(a);
+  constexpr int kThreads = 512;
+  const size_t smem = sizeof(double) * (2 * size_t(a.C) + 2 * size_t(a.K) + kThreads);
+  k_head<<<a.N, kThreads, smem, st>>>(a);
 }
 
 void launch_fisher_reduce(const FisherLayer* layers_dev, int L, int max_c, int N,

@@ -272,7 +272,15 @@ PAD_SPECS = [
     ConvSpec(64, 48, 8, 8, 3, 3, 1, 1,
              channel_splits=[ChannelSplit(0, 16, 1), ChannelSplit(16, 48, 1)]),  # padded range
 ]
-TC_SPECS += PAD_SPECS
+# densified grouped ranges: a few groups of slices off the 32-channel chunk
+# run as one GEMM over block-diagonal weights
+DENSE_SPECS = [
+    ConvSpec(64, 64, 8, 8, 3, 3, 1, 1, groups=4),              # slices of 16
+    ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, groups=8),            # slices of 8
+    ConvSpec(32, 48, 8, 8, 3, 3, 2, 1, groups=2),              # 16 -> 24 per group, stride 2
+    ConvSpec(128, 128, 4, 4, 3, 3, 1, 1, groups=8, bottleneck_out=2),  # 16 -> 8 per group
+]
+TC_SPECS += PAD_SPECS + DENSE_SPECS
 
 
 @pytest.mark.parametrize("prec", [Precision.FP32, Precision.TF32])
@@ -290,10 +298,11 @@ def test_tc_conv_integer_exact(ctx, oracle, spec, prec):
         assert np.array_equal(y[i], want.astype(np.float64)), i
 
 
-@pytest.mark.parametrize("spec", PAD_SPECS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}")
+@pytest.mark.parametrize("spec", PAD_SPECS + DENSE_SPECS,
+                         ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}g{s.groups}")
 def test_padded_specs_run_on_tensor_cores(spec):
-    """The padded shapes are lowered to the tcgen05 kernel, not the FFMA
-    fallback (fprop; dgrad too where Ci is a multiple of 16)."""
+    """The padded and densified shapes are lowered to the tcgen05 kernel, not
+    the FFMA fallback (fprop; dgrad too where Ci is a multiple of 16)."""
     c = nb.Context(0)
     net = Network([Layer(ConvSpec(spec.ci, spec.ci, spec.h, spec.w, 1, 1, 1, 0)), Layer(spec)],
                   num_classes=10, seed=3)
