@@ -128,11 +128,12 @@ int pick_bn(int n_per_group, bool split3) {
   return 0;
 }
 
-// N tile of a padded plan (one group, width a multiple of 16 that no tile
-// divides): the last tile's extra columns are zero weight rows (TMA
-// out-of-bounds fill) the epilogue does not store.
-int pick_bn_padded(int n, bool split3) {
-  if (n % 16) return 0;
+// N tile of a padded plan (one group, width a multiple of `gran` that no
+// tile divides): the last tile's extra columns are zero weight rows (TMA
+// out-of-bounds fill) the epilogue does not store -- fprop stores stop at 4
+// columns (gran 4), the fused dgrad epilogue at 16.
+int pick_bn_padded(int n, bool split3, int gran = 16) {
+  if (n % gran) return 0;
   return n <= 32 ? 32 : n <= 64 ? 64 : split3 ? 128 : (n <= 128 ? 128 : 256);
 }
 
@@ -297,7 +298,8 @@ void dgrad_phases(const ConvGeom& g, tc::TcArgs& t) {
 // tcgen05 implicit GEMM when the range is tensor-core shaped (32-channel K
 // chunks, 16-aligned N), the direct FFMA kernels otherwise -- plus packed-
 // weight, activation and Fisher-partial arena offsets.
-NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int64_t plan_n) {
+NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int64_t plan_n,
+              bool stem_col) {
   if (plan_n <= 0) plan_n = n;
   NetPlan P;
   const bool tc_on = prec != NB_PREC_SIMT;
@@ -357,7 +359,11 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           const bool kwf = G == 1 && !dense && use_kwf(g, sco, t.BW);
           const int pbn = kwf ? 0 : pick_pair_bn(sco, mt, P.split3);
           int bn = pbn ? pbn : pick_bn(sco, P.split3);
-          if (!bn && pad_ok) bn = pick_bn_padded(sco, P.split3);
+          static const int gran = [] {  // NB_TC_PADG: fprop padded-width granularity
+            const char* e = std::getenv("NB_TC_PADG");
+            return e ? std::atoi(e) : 4;
+          }();
+          if (!bn && pad_ok) bn = pick_bn_padded(sco, P.split3, gran);
           const int kp = (sci + 31) / 32 * 32;
           if (bn) {
             t.mode = 0;
@@ -395,6 +401,57 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
             off += 2 * tp.w_n;
             lp.family[i] = Family::TensorCore;
           }
+        }
+      }
+      // a narrow stem (Ci*KH*KW <= 32, e.g. the 3-channel 3x3 input layer)
+      // reading the session batch: a 1x1 GEMM over its im2col copy, K = 32
+      static const bool col_on = [] {  // NB_TC_COL=0: FFMA stem (experiments)
+        const char* e = std::getenv("NB_TC_COL");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (lp.family[i] == Family::Direct && stem_col && col_on && l == 0 && g.nranges == 1 &&
+          r.groups == 1 && tc_on && g.Ci * taps <= 32 && r.len % 4 == 0 && g.Co % 4 == 0) {
+        ConvGeom g1 = g;
+        g1.H = g.OH;
+        g1.W = g.OW;
+        g1.Ci = 32;
+        g1.KH = g1.KW = 1;
+        g1.S = 1;
+        g1.P = 0;
+        tc::TcArgs t{};
+        int bn = pick_bn(r.len, P.split3);
+        if (!bn) bn = pick_bn_padded(r.len, P.split3, 4);
+        if (bn && tc::plan_tiles(g.OH, g.OW, g.N, 1, t)) {
+          const int mt = m_tiles_at(g.OH, g.OW, plan_n, 1);
+          t.mode = 0;
+          t.n_tiles_per_group = (r.len + bn - 1) / bn;
+          t.n_tiles = t.n_tiles_per_group;
+          t.S = 1;
+          fprop_phase(g1, t);
+          t.a_cblocks = 1;
+          t.a_c_base = 0;
+          t.a_c_per_group = 32;
+          t.b_k_per_tap = 32;
+          t.b_row_base = 0;
+          t.b_row_per_group = r.len;
+          t.out_ld = g.Co;
+          t.out_c_base = r.b;
+          t.out_c_per_group = r.len;
+          t.ksplit = choose_ksplit(t, mt, num_sms, false);
+          TcPlan& tp = lp.tcf[i];
+          tp.bn = bn;
+          tp.tile = t;
+          tp.kp = 32;
+          tp.col = true;
+          tp.hw_chunks = t.ksplit > 1 ? splitk_hw_chunks(plan_n, g.OH * g.OW, r.len) : 1;
+          if (t.ksplit > 1)
+            P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
+          tp.w_n = align64(int64_t(r.len) * 32);
+          tp.w_off = off;
+          tp.b_rows = r.len;
+          tp.b_k = 32;
+          off += 2 * tp.w_n;
+          lp.family[i] = Family::TensorCore;
         }
       }
     }
@@ -531,7 +588,7 @@ std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) 
     if (lp.family[r] == Family::TensorCore)
       k += "," + std::to_string(lp.tcf[r].w_off) + "," + std::to_string(lp.tcf[r].w_n) +
            (lp.tcf[r].kwf ? "k" : "") + (lp.tcf[r].dense ? "D" : "") +
-           (lp.tcf[r].kp ? "p" : "");
+           (lp.tcf[r].kp ? "p" : "") + (lp.tcf[r].col ? "c" : "");
   }
   if (lp.dgrad_family == Family::TensorCore)
     k += "|d" + std::to_string(lp.tcd.w_off) + "," + std::to_string(lp.tcd.w_n) +
@@ -560,6 +617,7 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
       d.kwf_f = lp.tcf[r].kwf ? 1 : 0;
       d.kpf = lp.tcf[r].tile.b_k_per_tap;  // K per tap of the layout (padded / dense)
       d.dense_f = lp.tcf[r].dense ? 1 : 0;
+      d.col_f = lp.tcf[r].col ? 1 : 0;
       if (d.kpf || d.dense_f)  // the padded K columns / off-diagonal blocks stay zero
         NB_CUDA(cudaMemsetAsync(d.tcf_hi, 0, size_t(2 * lp.tcf[r].w_n) * 4, st));
     }
@@ -661,7 +719,10 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       a.relu = relu ? 1 : 0;
       a.ws = c->ws.as<float>();
       a.ws_stride = int64_t(g.N) * g.OH * g.OW * g.Co;
-      launch_tc(c, lp.tcf[r], a, P.split3, x, g.Ci, g.W, g.H, g.N, base + lp.tcf[r].w_off, st);
+      // (a col stem reads the session's im2col copy: 32 columns per output pixel)
+      const bool col = lp.tcf[r].col;
+      launch_tc(c, lp.tcf[r], a, P.split3, x, col ? 32 : g.Ci, col ? g.OW : g.W,
+                col ? g.OH : g.H, g.N, base + lp.tcf[r].w_off, st);
       if (a.ksplit > 1) {
         SplitEpi e{};
         e.ws = a.ws;
@@ -741,6 +802,44 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
 
 }  // namespace
 
+// The smallest spare session buffer of the context that fits, else a new one
+// (no cudaMalloc per session once the context has served a few).
+std::unique_ptr<DevBuf> take_spare(nb_ctx* c, size_t bytes) {
+  auto best = c->spare.end();
+  for (auto it = c->spare.begin(); it != c->spare.end(); ++it)
+    if ((*it)->bytes >= bytes && (best == c->spare.end() || (*it)->bytes < (*best)->bytes))
+      best = it;
+  std::unique_ptr<DevBuf> buf;
+  if (best != c->spare.end()) {
+    buf = std::move(*best);
+    c->spare.erase(best);
+  } else {
+    buf = std::make_unique<DevBuf>();
+    buf->ensure(bytes);
+  }
+  return buf;
+}
+
+// The session batch's im2col copy for a col stem (built once per geometry;
+// stream-ordered before the stem launch that reads it).
+const float* session_xcol(nb_ctx* c, nb_session* s, const ConvGeom& g, cudaStream_t st) {
+  const std::string sig = std::to_string(g.KH) + "," + std::to_string(g.KW) + "," +
+                          std::to_string(g.S) + "," + std::to_string(g.P) + "," +
+                          std::to_string(g.OH) + "," + std::to_string(g.OW);
+  if (s->xcol_sig != sig) {
+    const size_t bytes = size_t(s->n) * g.OH * g.OW * 32 * 4;
+    if (!s->xcol || s->xcol->bytes < bytes) {
+      if (s->xcol) c->spare.push_back(std::move(s->xcol));
+      s->xcol = take_spare(c, bytes);
+    }
+    launch_im2col32(s->x->as<float>(), s->n, int(s->h), int(s->w), int(s->ci), g.KH, g.KW, g.S,
+                    g.P, g.OH, g.OW, s->xcol->as<float>(), st);
+    c->launches++;
+    s->xcol_sig = sig;
+  }
+  return s->xcol->as<float>();
+}
+
 void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
                  bool backward, const RunOut& out, Pending& pend) {
   nb_ctx* c = s->ctx;
@@ -761,7 +860,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     c->prof.host(name, std::chrono::duration<double, std::milli>(now - tp).count());
     tp = now;
   };
-  NetPlan P = lower(net, N, prec, c->num_sms, out.grad_n > 0 ? out.grad_n : N);
+  NetPlan P = lower(net, N, prec, c->num_sms, out.grad_n > 0 ? out.grad_n : N, true);
   const bool want_grads = out.grads != nullptr;
   phase("host_lower");
 
@@ -852,6 +951,8 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   phase("host_weights");
   // ---- forward (I/nnet.hpp:180-197)
   const float* x = s->x->as<float>();
+  if (P.layers[0].family[0] == Family::TensorCore && P.layers[0].tcf[0].col)
+    x = session_xcol(c, s, P.layers[0].geom, st);
   for (int64_t l = 0; l < L; ++l) {
     float* y = act + P.layers[l].act_off;
     fprop_layer(c, P, P.layers[l], x, y, net.relu[l], st);
@@ -1096,22 +1197,7 @@ nb_session* make_session(nb_ctx* c, const NetDesc& net, const nb_batch* b) {
   s->seed = b->seed;
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   ctx_activate(c);
-  auto take = [&](size_t bytes) {
-    // the smallest spare buffer that fits, else a new one
-    auto best = c->spare.end();
-    for (auto it = c->spare.begin(); it != c->spare.end(); ++it)
-      if ((*it)->bytes >= bytes && (best == c->spare.end() || (*it)->bytes < (*best)->bytes))
-        best = it;
-    std::unique_ptr<DevBuf> buf;
-    if (best != c->spare.end()) {
-      buf = std::move(*best);
-      c->spare.erase(best);
-    } else {
-      buf = std::make_unique<DevBuf>();
-      buf->ensure(bytes);
-    }
-    return buf;
-  };
+  auto take = [&](size_t bytes) { return take_spare(c, bytes); };
   s->x = take(size_t(b->n * per) * 4);
   s->labels = take(size_t(b->n) * 4);
   c->io.ensure(size_t(b->n * per) * 8);
@@ -1268,9 +1354,10 @@ nb_status nb_session_destroy(nb_session* s) {
     std::lock_guard<std::recursive_mutex> lk(s->ctx->mu);
     ctx_activate(s->ctx);
     // keep the batch buffers for the context's next session (bounded)
-    if (s->ctx->spare.size() < 8) {
+    if (s->ctx->spare.size() < 12) {
       s->ctx->spare.push_back(std::move(s->x));
       s->ctx->spare.push_back(std::move(s->labels));
+      if (s->xcol) s->ctx->spare.push_back(std::move(s->xcol));
     }
     delete s;
   });

@@ -61,6 +61,9 @@ struct TcPlan {
   int dense = 0;
   // split-K epilogue pixel chunks (splitk_hw_chunks at the planning batch)
   int hw_chunks = 1;
+  // stem on the session's im2col copy of the batch: A = (N, OH, OW, 32) with
+  // K = (tap, channel) in 32 columns, a 1x1 GEMM (session_xcol)
+  bool col = false;
 };
 
 // Lowered layer: geometry + per-range family + packed-weight offsets.
@@ -91,7 +94,7 @@ struct NetPlan {
 // plan_n: the batch size launch shapes are chosen for (0 = n; an example
 // shard passes the whole batch's size)
 NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms = 148,
-              int64_t plan_n = 0);
+              int64_t plan_n = 0, bool stem_col = false);
 
 struct KStat {
   int64_t launches = 0;
@@ -166,6 +169,10 @@ struct nb_session {
   uint64_t seed = 0;
   std::unique_ptr<nb::DevBuf> x;       // (N, H, W, Ci) fp32
   std::unique_ptr<nb::DevBuf> labels;  // N int32
+  // im2col copy of x for a narrow stem (N, OH, OW, 32), built once per stem
+  // geometry (xcol_sig) -- the batch is resident and fixed
+  std::unique_ptr<nb::DevBuf> xcol;
+  std::string xcol_sig;
 };
 
 namespace nb {

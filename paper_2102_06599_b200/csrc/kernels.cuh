@@ -63,7 +63,13 @@ struct PackDst {
   // densified grouped layouts: K indexed by the full input (fprop) / range
   // output (dgrad) channel instead of the slice-local one
   int dense_f = 0, dense_d = 0;
+  // im2col stem layout: row co, K = tap * Ci + ci in 32 columns
+  int col_f = 0;
 };
+// im2col of an NHWC fp32 batch for a stem with Ci*KH*KW <= 32:
+// out (N, OH, OW, 32), column tap*Ci + ci, zeros for padding taps and k >= Ci*KH*KW
+void launch_im2col32(const float* x, int64_t N, int H, int W, int Ci, int KH, int KW, int S,
+                     int P, int OH, int OW, float* out, cudaStream_t st);
 void launch_pack_weights(const double* src, double scale, const ConvGeom& g, int range,
                          const PackDst& d, cudaStream_t st);
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,

@@ -75,8 +75,9 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     const int kh = tap / d.KW, kw = tap - kh * d.KW, KH = taps / d.KW;
     if (d.tcf_hi) {
       const int kpf = d.kpf ? d.kpf : r.slice_ci;
-      const int64_t i = d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
-                                : (int64_t(co_local) * taps + tap) * kpf + (d.dense_f ? ci : j);
+      const int64_t i = d.col_f   ? int64_t(co_local) * 32 + tap * r.slice_ci + j
+                        : d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
+                                  : (int64_t(co_local) * taps + tap) * kpf + (d.dense_f ? ci : j);
       d.tcf_hi[i] = hi;
       d.tcf_lo[i] = lo;
     }
@@ -1101,6 +1102,32 @@ void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st) {
   }
   cfg.gridDim = dim3((e.C + 31) / 32, e.N, e.hw_chunks);
   cudaLaunchKernelEx(&cfg, k_splitk_epilogue, e);
+}
+
+__global__ void k_im2col32(const float* __restrict__ x, int64_t N, int H, int W, int Ci, int KH,
+                           int KW, int S, int P, int OH, int OW, float* __restrict__ out) {
+  const int64_t total = N * OH * OW * 32;
+  const int K = Ci * KH * KW;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int k = int(e % 32);
+    const int64_t pix = e / 32;
+    const int ow = int(pix % OW), oh = int((pix / OW) % OH);
+    const int64_t n = pix / (int64_t(OW) * OH);
+    float v = 0.f;
+    if (k < K) {
+      const int tap = k / Ci, c = k - tap * Ci;
+      const int ih = oh * S - P + tap / KW, iw = ow * S - P + tap % KW;
+      if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * H + ih) * W + iw) * Ci + c];
+    }
+    out[e] = v;
+  }
+}
+
+void launch_im2col32(const float* x, int64_t N, int H, int W, int Ci, int KH, int KW, int S,
+                     int P, int OH, int OW, float* out, cudaStream_t st) {
+  k_im2col32<<<grid_for(N * OH * OW * 32, 256), 256, 0, st>>>(x, N, H, W, Ci, KH, KW, S, P, OH,
+                                                             OW, out);
 }
 
 int splitk_hw_chunks(int64_t n, int HW, int C) {

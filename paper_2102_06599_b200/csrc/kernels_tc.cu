@@ -855,13 +855,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
                                                   pix * a.out_ld + col0 + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              if (KWF || c + 4 * i < nlim)  // (fprop widths down to 4 columns)
+                o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           }
         } else if (a.mode == 0) {
           if (valid) {
             float4* o = reinterpret_cast<float4*>(a.out + pix * a.out_ld + col0 + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
+              if (!KWF && c + 4 * i >= nlim) break;
               float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
               if (a.relu) {
                 x.x = x.x > 0.f ? x.x : 0.f;

@@ -405,3 +405,35 @@ def test_stem_fprop_integer_exact(ctx, oracle, spec, prec):
     for i in range(n):
         want = oracle.conv(spec, x[i].astype(np.int64), w.astype(np.int64))
         assert np.array_equal(y[i], want.astype(np.float64)), i
+
+
+# the session path lowers narrow stems (Ci*KH*KW <= 32) to a 1x1 tensor-core
+# GEMM over the resident batch's im2col copy
+COL_STEMS = [
+    ConvSpec(3, 64, 32, 32, 3, 3, 1, 1),                    # the R34 stem
+    ConvSpec(3, 32, 17, 17, 3, 3, 2, 1),                    # stride 2, odd size
+    ConvSpec(3, 16, 9, 9, 3, 3, 1, 1, spatial_div_h=3),     # crop, N 16 of 32
+    ConvSpec(2, 48, 8, 8, 3, 3, 1, 1),                      # K 18, N 48 of 64
+]
+
+
+@pytest.mark.parametrize("prec", [Precision.FP32, Precision.TF32])
+@pytest.mark.parametrize("spec", COL_STEMS, ids=lambda s: f"{s.ci}x{s.co}x{s.h}s{s.stride}")
+def test_col_stem_integer_exact(oracle, spec, prec):
+    c = nb.Context(0)
+    net = Network([Layer(spec, relu=False)], num_classes=4, seed=5)
+    net.init_weights()
+    rng = np.random.default_rng(spec.co + spec.h)
+    w = rng.integers(-3, 4, size=net.weights[0].shape).astype(np.float64)
+    net.weights[0] = w
+    n = 3
+    x = rng.integers(-3, 4, size=(n, spec.ci, spec.h, spec.w)).astype(np.float64)
+    batch = nb.Batch(x, np.arange(n, dtype=np.int32) % 4, 1)
+    c.set_profiling(True)
+    acts, _ = nb.activation_gradients(net, batch, precision=prec, ctx=c)
+    names = set(c.kernel_stats())
+    assert "conv_fprop_direct" not in names, names
+    y = acts[0].reshape((n,) + spec.output_shape())
+    for i in range(n):
+        want = oracle.conv(spec, x[i].astype(np.int64), w.astype(np.int64))
+        assert np.array_equal(y[i], want.astype(np.float64)), i
