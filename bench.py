@@ -349,6 +349,13 @@ def main():
                  "peak_source": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json); 3xTF32 "
                                 "issues 3 tf32 MMAs (tf32 = bf16/2) per fp32 product, so the "
                                 "kernel's own ceiling is peak/6"}
+            # the arithmetic the precision mode issues: 3xTF32 = 3 tf32 MMAs
+            # per fp32 product at half the bf16 rate; TF32 = 1 at half rate
+            div = {"fp32": 6.0, "tf32": 2.0}.get(args.precision)
+            if div:
+                r["kernel_ceiling"] = {"value": pk["bf16_tflops"] / div, "unit": "TFLOP/s",
+                                       "frac": ach / (pk["bf16_tflops"] / div),
+                                       "mode": args.precision}
         else:
             ach = dom["bytes"] / dom["launches"] / (avg_ms / 1e3) / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
