@@ -279,6 +279,8 @@ DENSE_SPECS = [
     ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, groups=8),            # slices of 8
     ConvSpec(32, 48, 8, 8, 3, 3, 2, 1, groups=2),              # 16 -> 24 per group, stride 2
     ConvSpec(128, 128, 4, 4, 3, 3, 1, 1, groups=8, bottleneck_out=2),  # 16 -> 8 per group
+    ConvSpec(64, 96, 8, 8, 3, 3, 1, 1,
+             channel_splits=[ChannelSplit(0, 32, 1), ChannelSplit(32, 96, 4)]),  # densified range
 ]
 TC_SPECS += PAD_SPECS + DENSE_SPECS
 
@@ -414,6 +416,8 @@ COL_STEMS = [
     ConvSpec(3, 32, 17, 17, 3, 3, 2, 1),                    # stride 2, odd size
     ConvSpec(3, 16, 9, 9, 3, 3, 1, 1, spatial_div_h=3),     # crop, N 16 of 32
     ConvSpec(2, 48, 8, 8, 3, 3, 1, 1),                      # K 18, N 48 of 64
+    ConvSpec(3, 8, 6, 6, 1, 1, 1, 0),                       # 1x1 stem, N 8 of 32
+    ConvSpec(3, 16, 8, 8, 3, 3, 1, 1, bottleneck_out=4),    # co_eff 4: N 4 of 32
 ]
 
 
