@@ -236,7 +236,6 @@ def main():
     costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
     assign = shard_lpt(costs, world, args.steps)
     mine = [n for n, a in zip(timed, assign) if a == rank]
-    my_flops = sum(c for c, a in zip(costs, assign) if a == rank)
 
     batch = nb.make_batch(origin, N_BATCH, 1)
     ctxs = [nb.Context(local) for _ in range(args.streams)]
@@ -409,7 +408,11 @@ def main():
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
-            "achieved_tflops_step": my_flops / (ms / 1e3) / 1e12,
+            # all ranks' algorithmic FLOPs over the max-over-ranks time
+            "achieved_tflops_step": sum(costs) / (ms / 1e3) / 1e12,
+            # LPT shard balance: the largest rank's estimated FLOPs over the mean
+            "lpt_max_over_mean": (max(sum(c for c, a in zip(costs, assign) if a == r)
+                                      for r in range(world)) / (sum(costs) / world)),
             "scheduler": {"evaluated": st.evaluated, "deduplicated": st.deduplicated,
                           "busy_ms": [round(b, 2) for b in st.busy_ms]},
             "roofline": roof,
