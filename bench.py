@@ -35,6 +35,19 @@ UNIT = "candidates/s"
 N_BATCH = 128
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
+# Precision tiers (the values live in
+# paper_2102_06599_b200/api.py TOLERANCE): what each mode computes in and
+# the stated tolerance of its Fisher scores against the fp64 reference.
+MODE_KEY = {"fp32": "fp32_3xtf32", "tf32": "tf32", "simt": "simt"}
+DTYPE = {"fp32_3xtf32": "3xtf32", "tf32": "tf32", "simt": "f32"}
+ARITH = {"fp32": "3xTF32 tcgen05 implicit GEMM (hi*hi + hi*lo + lo*hi, fp32 accumulate) for "
+                 "tensor-core-shaped ranges, fp32 FFMA for the rest; head/softmax/Fisher fp64",
+         "tf32": "1xTF32 tcgen05 (throughput tier); head/softmax/Fisher fp64",
+         "simt": "fp32 FFMA everywhere (true fp32); head/softmax/Fisher fp64"}
+TOL_NOTE = {"fp32_3xtf32": "Fisher totals <= 5e-4, per layer <= 5e-3 relative",
+            "tf32": "Fisher totals <= 5e-2, per layer <= 2e-1 relative",
+            "simt": "Fisher totals <= 1e-5, per layer <= 1e-4 relative"}
+
 
 def parse():
     p = argparse.ArgumentParser()
@@ -45,9 +58,10 @@ def parse():
     p.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "simt"])
     p.add_argument("--streams", type=int, default=4, help="concurrent sessions per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-modes", action="store_true",
+                   help="skip the other precision tiers' figures")
     p.add_argument("--no-kernel-events", action="store_true",
                    help="skip the per-launch CUDA events (no roofline; overhead check)")
-    p.add_argument("--cpu-sample-layers", type=int, default=2)
     return p.parse_args()
 
 
@@ -110,98 +124,136 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# reference CPU path (oracle/_ref: the unmodified nestopt compiled in place)
+# the candidate pool (plain JSON: the reference arm never loads the product)
 
-def timed_pool(args, world):
-    """The candidate networks the nb200 arm times (both arms use the same
-    selection): the reference's R34 per-layer pool in a fixed shuffled order,
-    the first W for warm-up, the next K x world timed."""
+def _out(l):
+    """(co_eff, out_h, out_w) of a layer JSON (ConvSpec, I/ir.hpp:40-50)."""
+    p, s = l.get("pad", 0), l.get("stride", 1)
+    oh = ((l["h"] + 2 * p - l.get("kh", 1)) // s + 1) // l.get("spatial_div_h", 1)
+    ow = ((l["w"] + 2 * p - l.get("kw", 1)) // s + 1) // l.get("spatial_div_w", 1)
+    return l["co"] // l.get("bottleneck", 1), oh, ow
+
+
+def timed_pool(steps, warmup, world):
+    """The candidate networks both arms use, as network JSON: the
+    reference's R34 per-layer pool (tests/golden/r34_candidates.json: each
+    candidate is the origin with one layer replaced, shapes repaired as
+    repair_network does, I/nnet.hpp:372-380) in a fixed shuffled order; the
+    first max(1, W) warm up, the next K x world are timed, the rest spare."""
     import numpy as np
-    from paper_2102_06599_b200.workloads import fixture_path, load_candidates, resnet34_chain
-
-    origin = resnet34_chain()
-    pool = load_candidates(fixture_path("r34_candidates.json"), origin)
+    with open(os.path.join(ROOT, "tests", "golden", "r34_candidates.json")) as f:
+        data = json.load(f)
+    origin = data["origin"]
+    pool = []
+    for c in data["candidates"]:
+        layers = [dict(l) for l in origin["layers"]]
+        layers[c["diff"][0]] = dict(c["diff"][1])
+        for l in range(1, len(layers)):
+            layers[l]["ci"], layers[l]["h"], layers[l]["w"] = _out(layers[l - 1])
+        pool.append(dict(origin, layers=layers))
     order = np.random.default_rng(0).permutation(len(pool))
     pool = [pool[i] for i in order]
-    warm = pool[:max(1, args.warmup)]
+    warm = pool[:max(1, warmup)]
     timed = pool[len(warm):]
-    need = args.steps * world
+    need = steps * world
     if need > len(timed):
         raise SystemExit(f"--steps x gpus = {need} exceeds the {len(timed)} distinct candidates")
-    return origin, warm, timed[:need]
+    return origin, warm, timed[:need], timed[need:]
 
 
-def fisher_macs(net, n):
-    """MACs of one fisher_potential: forward of every layer + dgrad of layers
-    >= 1 (I/nnet.hpp:225), per example, times n."""
-    from paper_2102_06599_b200.api import count_macs
-    m = [count_macs(l.spec) for l in net.layers]
-    return n * (sum(m) + sum(m[1:]))
+def _macs(l):
+    """count_macs of a layer JSON (I/interp.hpp:190-202)."""
+    co, oh, ow = _out(l)
+    ranges = l.get("channel_splits") or [{"begin": 0, "end": co, "groups": l.get("groups", 1)}]
+    return sum((r["end"] - r["begin"]) * oh * ow * (l["ci"] // r.get("groups", 1))
+               * l.get("kh", 1) * l.get("kw", 1) for r in ranges)
 
 
-def reference_sample(layers: int, threads: int, target_macs: float):
-    """Times the reference's fisher_potential on a bounded slice of the R34
-    chain (its first `layers` convs, one image) on `threads` host threads at
-    once (one evaluation per thread, like evaluate_all's jobs), and scales it
-    to candidates/s of candidates costing `target_macs` Fisher MACs (the
-    reference's cost is linear in MACs and examples, I/nnet.hpp:184,206)."""
-    from oracle.oracle import Reference
-    from paper_2102_06599_b200.api import Network
-    from paper_2102_06599_b200.workloads import resnet34_chain
+def config_block(steps, streams, world):
+    """`config` of both arms (identical, so the driver compares like with like)."""
+    return {"workload": "resnet34_chain_fisher_search", "global_batch": N_BATCH,
+            "network": "ResNet-34 CIFAR 33-conv chain (SURVEY App. B)",
+            "candidates": "tests/golden/r34_candidates.json (reference draw_candidates + "
+                          "host gates, 12 masked layers)",
+            "candidates_per_gpu": steps, "streams_per_gpu": streams,
+            "parallelism": f"candidate-sharded x{world} (LPT, no collective)",
+            "l2": "inputs larger than L2 (~0.5 GB of activations per evaluation)"}
 
-    full = resnet34_chain()
-    sl = Network(full.layers[:layers], num_classes=10, seed=42)
-    R = Reference()
-    errs = []
 
-    def one():
-        try:
-            R.fisher(sl, 1, 1)
-        except Exception as e:  # pragma: no cover
-            errs.append(e)
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref: the unmodified nestopt compiled in place)
 
-    t0 = time.perf_counter()
-    ts = [threading.Thread(target=one) for _ in range(threads)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    dt = time.perf_counter() - t0
-    if errs:
-        raise errs[0]
-    scale = target_macs / fisher_macs(sl, 1)
-    cand_per_s = threads / (dt * scale)
-    return cand_per_s, dt, (f"reference fisher_potential (oracle/_ref) on R34 layers 0-{layers - 1}"
-                            f" at N=1, {threads} concurrent on {threads} host threads, "
-                            f"{dt:.2f} s wall, scaled x{scale:.0f} by Fisher MACs to the mean "
-                            f"candidate of the timed pool at N={N_BATCH} (extrapolated)")
+def cpu_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Thread(s) per core", "Core(s) per socket",
+                             "Socket(s)", "CPU max MHz"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def cpu_baseline_sample(timed, threads):
+    """cpu_baseline of the nb200 arm: a bounded (~10-30 s) sample of the
+    reference on the box's host cores.  One timed-pool candidate is cut into
+    `threads` contiguous layer slices, each scored at N=1 by the reference's
+    fisher_potential on its own thread (evaluate_all's pool); every layer
+    runs in its own shape, the overlap layers' extra forwards are timed and
+    subtracted (oracle/refbench.py).  The candidate's N=1 thread-seconds,
+    x128 by the reference's exact linearity in N (I/nnet.hpp:184, 206), give
+    candidates/s on `threads` cores (extrapolated)."""
+    from oracle.refbench import RefArm, candidate_seconds_by_slices
+    net = timed[0]
+    sec, wall, parts = candidate_seconds_by_slices(RefArm(), net, threads)
+    v = threads / (sec * N_BATCH)
+    return v, (f"reference fisher_potential (oracle/_ref) on timed-pool candidate 0 at N=1, "
+               f"cut into {parts} layer slices run concurrently on {threads} host threads "
+               f"({wall:.1f} s wall); {sec:.1f} thread-s per N=1 evaluation x{N_BATCH} "
+               f"examples (exact linearity in N), {threads} candidates in flight (extrapolated)")
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path on this box's host
+    cores, through oracle/refbench.py only (the product is never imported):
+    each step is one timed-pool candidate's fisher_potential at N=1 (example
+    0 of the bench batch: make_batch's prefix property), the K steps
+    self-scheduled on every host thread exactly as evaluate_all does
+    (I/search.hpp:315-334).  value = K/128 candidates per timed second: a
+    candidate at N=128 is 128 such evaluations (I/nnet.hpp:184, 206),
+    labelled extrapolated."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle.refbench import RefArm
     threads = os.cpu_count() or 1
-    _, _, timed = timed_pool(args, int(os.environ.get("WORLD_SIZE", "1")))
-    target = sum(fisher_macs(n, N_BATCH) for n in timed) / len(timed)
-    # each step is a ~6-10 s sample; keep the whole arm within a few minutes
-    warm, steps = min(args.warmup, 1), min(args.steps, 8)
-    for _ in range(warm):
-        reference_sample(args.cpu_sample_layers, threads, target)
-    vals, walls, sample = [], [], ""
-    for _ in range(steps):
-        v, dt, sample = reference_sample(args.cpu_sample_layers, threads, target)
-        vals.append(v)
-        walls.append(dt)
-    v = statistics.mean(vals)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    _, warm, timed, spare = timed_pool(args.steps, args.warmup, world)
+    timed = timed[:args.steps]
+    arm = RefArm()
+    # warm-up: W untimed evaluations of the cheapest spare candidates (the
+    # CPU path has no caches to fill; this only pages the code in)
+    cheap = sorted(spare, key=lambda n: sum(_macs(l) for l in n["layers"]))[:max(1, args.warmup)]
+    arm.fisher_jobs(cheap, 1, threads)
+    totals, secs, wall = arm.fisher_jobs(timed, 1, threads)
+    v = len(timed) / N_BATCH / wall
+    sample = (f"reference fisher_potential (oracle/_ref, evaluate_all's thread pool) on the "
+              f"{len(timed)} timed-pool candidates, each whole network at N=1 (example 0 of "
+              f"the batch), on {threads} host threads: {wall:.1f} s wall, "
+              f"{statistics.mean(secs):.1f} s mean per evaluation; x{N_BATCH} examples per "
+              f"candidate (exact linearity in N, extrapolated)")
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-            "ms_per_step": 1e3 / v, "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": len(timed), "warmup": len(cheap),
+            "ms_per_step": 1e3 * wall / len(timed), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "resnet34_chain_fisher_search", "global_batch": N_BATCH,
-                       "network": "ResNet-34 CIFAR 33-conv chain (SURVEY App. B)"},
+            "config": config_block(args.steps, args.streams, world),
+            "precision": "fp64 (the reference's double arithmetic)",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
+            "cpu": cpu_info(),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -232,7 +284,10 @@ def main():
 
     # warm-up networks and the timed pool are disjoint; the timed pool is
     # K per rank, LPT-sharded over the ranks by estimated FLOPs
-    origin, warm_pool, timed = timed_pool(args, world)
+    origin_j, warm_j, timed_j, _ = timed_pool(args.steps, args.warmup, world)
+    origin = nb.Network.from_json(origin_j)
+    warm_pool = [nb.Network.from_json(n) for n in warm_j]
+    timed = [nb.Network.from_json(n) for n in timed_j]
     costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
     assign = shard_lpt(costs, world, args.steps)
     mine = [n for n, a in zip(timed, assign) if a == rank]
@@ -384,25 +439,35 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        target = sum(fisher_macs(n, N_BATCH) for n in timed) / len(timed)
-        v, dt, sample = reference_sample(args.cpu_sample_layers, threads, target)
+        v, sample = cpu_baseline_sample(timed_j, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                "sample": sample}
 
+    # ---- the other precision tiers on the same timed pool (device-timed,
+    # same sessions): SIMT = true fp32 FFMA everywhere, TF32 = 1xTF32
+    modes = {}
+    if not args.no_modes:
+        for name, pm in (("simt", Precision.SIMT), ("tf32", Precision.TF32),
+                         ("fp32_3xtf32", Precision.FP32)):
+            if pm == prec:
+                continue
+            nb.evaluate(sessions, warm_pool, pm)
+            mms, _ = timed_region(lambda: nb.evaluate(sessions, mine, pm))
+            modes[name] = {"value": total_units / (mms / 1e3), "unit": UNIT,
+                           "dtype": DTYPE[name], "tolerance": TOL_NOTE[name]}
+
     if rank == 0:
+        cfg = config_block(args.steps, args.streams, world)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if args.precision != "tf32" else "tf32", "data": "synthetic",
-            "config": {"workload": "resnet34_chain_fisher_search", "global_batch": N_BATCH,
-                       "network": "ResNet-34 CIFAR 33-conv chain (SURVEY App. B)",
-                       "candidates": "tests/golden/r34_candidates.json (reference "
-                                     "draw_candidates + host gates, 12 masked layers)",
-                       "candidates_per_gpu": args.steps, "streams_per_gpu": args.streams,
-                       "precision": args.precision,
-                       "parallelism": f"candidate-sharded x{world} (LPT, no collective)",
-                       "l2": "inputs larger than L2 (~0.5 GB of activations per evaluation)"},
+            "dtype": DTYPE[MODE_KEY[args.precision]], "data": "synthetic",
+            "config": cfg,
+            "precision": {"mode": args.precision,
+                          "arithmetic": ARITH[args.precision],
+                          "tolerance": TOL_NOTE[MODE_KEY[args.precision]]},
+            "other_precisions": modes,
             "inference_ms": inf_ms / 10, "inference_origin_ms": inf_o_ms / 10,
             "inference_net_macs": nb.network_macs(best),
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -420,6 +485,7 @@ def main():
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3)}
                         for k, v in kstats.items()},
             "cpu_baseline": cpu,
+            "cpu": cpu_info() if rank == 0 else None,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NB200_ABI_VERSION 1
+#define NB200_ABI_VERSION 2
 
 typedef enum nb_status {
   NB_OK = 0,
@@ -130,12 +130,17 @@ typedef struct nb_kernel_stat {
   double bytes;       /* algorithmic HBM bytes (read once + write once) */
 } nb_kernel_stat;
 
-/* Scheduler statistics of one nb_evaluate call. */
+/* Scheduler statistics of one nb_evaluate call.  The per-session arrays are
+ * caller-owned (num_sessions entries each) and may be NULL. */
 typedef struct nb_eval_stats {
-  int64_t evaluated;     /* distinct networks run on a device */
-  int64_t deduplicated;  /* candidates answered from an identical network */
-  double est_flops[16];  /* per context: LPT-assigned estimated FLOPs */
-  double busy_ms[16];    /* per context: wall time of its worker */
+  int64_t evaluated;       /* distinct networks run on a device */
+  int64_t deduplicated;    /* candidates answered from an identical network */
+  int64_t requeued;        /* evaluations handed back after a device failure */
+  int32_t failed_sessions; /* sessions retired by a device failure */
+  int32_t reserved;
+  double* est_flops;       /* per session: estimated FLOPs of what it ran */
+  double* busy_ms;         /* per session: device time of its evaluations */
+  int64_t* evaluations;    /* per session: networks it evaluated */
 } nb_eval_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -361,11 +366,16 @@ nb_status nb_session_forward(nb_session* s, const nb_network* net,
 
 /* ---- candidate scheduler (evaluate_all, I/search.hpp:315-334) ------------ */
 /* Scores `count` candidate networks (all drawn with init_weights) on the
- * given sessions -- one per GPU, all holding the same batch.  Identical
- * networks are evaluated once; the rest are assigned to sessions by LPT on
- * nb_fisher_flops and run by one host worker thread per session.  Results
- * land in outs[i] regardless of assignment, so the output is independent of
- * the number of sessions (the reference's jobs=k == jobs=1 guarantee,
+ * given sessions -- each on its own context (normally one or a few per GPU),
+ * all holding the same batch (NB_ERR_CONFIG otherwise).  Identical networks
+ * are evaluated once; the rest form one queue in longest-processing-time
+ * order (nb_fisher_flops) that every session pulls from as soon as its
+ * previous evaluation completes (the reference's self-scheduling,
+ * next.fetch_add(1)), one host worker thread per GPU.  A session that hits
+ * a device error is retired and its candidate re-queued for the others; the
+ * call fails only when no session is left.  Results land in outs[i]
+ * regardless of which session ran them, so the output is independent of the
+ * number of sessions and GPUs (the reference's jobs=k == jobs=1 guarantee,
  * T/test_search.cpp:83-94). */
 nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessions,
                       const nb_network* nets, int64_t count, nb_precision prec,

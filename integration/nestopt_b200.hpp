@@ -711,14 +711,28 @@ inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
   return true;
 }
 
-// Near-threshold band of each arithmetic mode: its stated tolerance on
-// Fisher totals (paper_2102_06599_b200/api.py
-// RECHECK_BAND).  A candidate scored within the band of the origin is
-// re-scored in NB_PREC_SIMT (fp32 FFMA, totals within 1e-5 of the fp64
-// reference) before the accept decision, so the throughput modes make the
-// reference's decisions except for ties closer than SIMT's tolerance.
+// Stated tolerance of each arithmetic mode on Fisher totals (DESIGN.md
+// section 3, paper_2102_06599_b200/api.py TOLERANCE["total"]).
+inline double total_tolerance(nb_precision p) {
+  return p == NB_PREC_FP32 ? 5e-4 : p == NB_PREC_TF32 ? 5e-2 : 1e-5;
+}
+
+// Near-threshold band of a throughput mode (api.py RECHECK_BAND): a
+// candidate's score and the origin's may each be off by the mode's total
+// tolerance in opposite directions, so a decision can only differ from the
+// reference's when |cand - origin| <= 2 x tolerance; the band adds 25% on
+// top.  Candidates inside it are re-scored, with the origin, in
+// NB_PREC_SIMT (fp32 FFMA, totals within 1e-5 of the fp64 reference) before
+// the accept decision.  Only ties closer than SIMT's own 2 x 1e-5 can then
+// differ from the reference (the documented near-threshold tie band).
 inline double recheck_band(nb_precision p) {
-  return p == NB_PREC_FP32 ? 5e-4 : p == NB_PREC_TF32 ? 5e-2 : 0.0;
+  return p == NB_PREC_SIMT ? 0.0 : 2.5 * total_tolerance(p);
+}
+
+// |cand - origin| <= band * |origin|: the decision needs the SIMT recheck.
+inline bool near_threshold(double cand, double origin, nb_precision p) {
+  const double band = recheck_band(p);
+  return band > 0 && std::fabs(cand - origin) <= band * std::fabs(origin);
 }
 
 inline bool same_network(const nestopt::Network& a, const nestopt::Network& b) {
@@ -800,7 +814,9 @@ inline long long legal_gpu_min() {
 // Scheduler statistics of one evaluate_all_gpu call.
 struct GpuStats {
   int64_t scored = 0, evaluated = 0, deduplicated = 0, origin_equal = 0, rechecked = 0;
+  int64_t rank_rechecked = 0, requeued = 0;
   std::vector<double> est_flops, busy_ms;
+  std::vector<int64_t> evaluations;
   double gates_ms = 0, gpu_ms = 0;
 };
 
@@ -877,41 +893,61 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
       pl[k].resize(nets[which[k]].layers.size());
       outs[k] = nb_fisher_out{nullptr, pl[k].data(), 0.0, 0, 0.0, nullptr};
     }
+    std::vector<double> est(sp.size()), busy(sp.size());
+    std::vector<int64_t> done(sp.size());
     nb_eval_stats es{};
+    es.est_flops = est.data();
+    es.busy_ms = busy.data();
+    es.evaluations = done.data();
     check(nb_evaluate(sp.data(), int32_t(sp.size()), cnets.data(), int64_t(cnets.size()), p,
                       outs.data(), &es));
     tot.resize(which.size());
     for (size_t k = 0; k < which.size(); ++k) tot[k] = outs[k].total;
-    return es;
+    if (p == prec) {
+      st.evaluated += es.evaluated;
+      st.deduplicated += es.deduplicated;
+      st.requeued += es.requeued;
+      st.est_flops.resize(sp.size());
+      st.busy_ms.resize(sp.size());
+      st.evaluations.resize(sp.size());
+      for (size_t k = 0; k < sp.size(); ++k) {
+        st.est_flops[k] += est[k];
+        st.busy_ms[k] += busy[k];
+        st.evaluations[k] += done[k];
+      }
+    }
   };
+  // the origin's SIMT score, computed once when a recheck needs it
+  bool have_simt_origin = false;
+  double simt_origin = 0.0;
+  auto origin_simt = [&]() {
+    if (!have_simt_origin) {
+      simt_origin = fisher_potential(*sessions[0], origin, NB_PREC_SIMT).total;
+      have_simt_origin = true;
+    }
+    return simt_origin;
+  };
+  std::vector<char> simt_scored(cands.size(), 0);
   if (!idx.empty()) {
     std::vector<double> tot;
     std::vector<std::vector<double>> pl;
-    nb_eval_stats es = score(idx, prec, tot, pl);
-    st.evaluated = es.evaluated;
-    st.deduplicated = es.deduplicated;
-    for (size_t k = 0; k < sp.size() && k < 16; ++k) {
-      st.est_flops.push_back(es.est_flops[k]);
-      st.busy_ms.push_back(es.busy_ms[k]);
-    }
+    score(idx, prec, tot, pl);
     // near-threshold candidates: re-score them and the origin in SIMT mode
-    double origin_total = origin_fisher.total;
-    const double band = recheck_band(prec);
     std::vector<size_t> near, near_k;
     for (size_t k = 0; k < idx.size(); ++k)
-      if (band > 0 && std::fabs(tot[k] - origin_fisher.total) <= band * std::fabs(origin_fisher.total)) {
+      if (near_threshold(tot[k], origin_fisher.total, prec)) {
         near.push_back(idx[k]);
         near_k.push_back(k);
       }
     if (!near.empty()) {
-      FisherReport exact_origin = fisher_potential(*sessions[0], origin, NB_PREC_SIMT);
-      origin_total = exact_origin.total;
+      origin_simt();
       std::vector<double> t2;
       std::vector<std::vector<double>> pl2;
       score(near, NB_PREC_SIMT, t2, pl2);
       for (size_t j = 0; j < near.size(); ++j) {
         tot[near_k[j]] = t2[j];
         pl[near_k[j]] = pl2[j];
+        simt_scored[near[j]] = 1;
       }
       st.rechecked = int64_t(near.size());
     }
@@ -920,17 +956,52 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
       cand.fisher_total = tot[k];
       cand.fisher_per_layer = pl[k];
       // a rechecked candidate is compared with the origin's SIMT score
-      const bool was_near = std::find(near_k.begin(), near_k.end(), k) != near_k.end();
-      const double ref = was_near ? origin_total : origin_fisher.total;
+      const double ref = simt_scored[idx[k]] ? simt_origin : origin_fisher.total;
       // fisher_accepts (I/nnet.hpp:356-359) and the message of
-      // I/search.hpp:303-309
+      // I/search.hpp:303-309, printing the value actually compared
       if (!(tot[k] >= ref)) {
         cand.status = CandidateStatus::RejectedFisher;
         std::ostringstream os;
-        os << "fisher potential dropped: " << tot[k] << " < " << origin_fisher.total;
+        os << "fisher potential dropped: " << tot[k] << " < " << ref;
         cand.reason = os.str();
       } else {
         cand.status = CandidateStatus::Survivor;
+      }
+    }
+    // rank_survivors (I/search.hpp:338-349) orders equal-MAC survivors by
+    // their totals: survivors whose totals are within the mode's band of an
+    // equal-MAC neighbour are re-scored in SIMT too, so that order is the
+    // reference's except for ties inside SIMT's own tolerance
+    if (recheck_band(prec) > 0) {
+      std::map<long long, std::vector<size_t>> by_macs;
+      for (size_t i : idx)
+        if (cands[i].status == CandidateStatus::Survivor) by_macs[cands[i].macs].push_back(i);
+      std::vector<size_t> more;
+      for (auto& kv : by_macs) {
+        auto& g = kv.second;
+        if (g.size() < 2) continue;
+        std::sort(g.begin(), g.end(), [&](size_t a, size_t b) {
+          return cands[a].fisher_total < cands[b].fisher_total;
+        });
+        std::vector<char> mark(g.size(), 0);
+        for (size_t j = 1; j < g.size(); ++j) {
+          const double a = cands[g[j - 1]].fisher_total, b = cands[g[j]].fisher_total;
+          if (a != b && near_threshold(a, b, prec)) mark[j - 1] = mark[j] = 1;
+        }
+        for (size_t j = 0; j < g.size(); ++j)
+          if (mark[j] && !simt_scored[g[j]]) more.push_back(g[j]);
+      }
+      if (!more.empty()) {
+        std::sort(more.begin(), more.end());
+        std::vector<double> t3;
+        std::vector<std::vector<double>> pl3;
+        score(more, NB_PREC_SIMT, t3, pl3);
+        for (size_t j = 0; j < more.size(); ++j) {
+          cands[more[j]].fisher_total = t3[j];
+          cands[more[j]].fisher_per_layer = pl3[j];
+          simt_scored[more[j]] = 1;
+        }
+        st.rank_rechecked = int64_t(more.size());
       }
     }
   }

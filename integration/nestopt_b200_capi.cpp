@@ -163,6 +163,12 @@ extern "C" {
 const char* nbi_last_error(void) { return g_err.c_str(); }
 void nbi_free(char* p) { std::free(p); }
 
+// nb200::near_threshold: whether the search driver re-scores a candidate
+// with this total against this origin total in SIMT before deciding.
+int nbi_near_threshold(double cand, double origin, int precision) {
+  return nb200::near_threshold(cand, origin, static_cast<nb_precision>(precision)) ? 1 : 0;
+}
+
 // Runs the search of `cfg_json` with candidate scoring on the GPU sessions
 // listed in `devices` ("0,1,2,3"; a device may repeat: several sessions on
 // one GPU exercise the multi-worker scheduler).  jobs > 0 overrides the
@@ -185,8 +191,11 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
                   {"deduplicated", st.deduplicated},
                   {"origin_equal", st.origin_equal},
                   {"rechecked", st.rechecked},
+                  {"rank_rechecked", st.rank_rechecked},
+                  {"requeued", st.requeued},
                   {"est_flops", st.est_flops},
                   {"busy_ms", st.busy_ms},
+                  {"evaluations", st.evaluations},
                   {"gates_ms", st.gates_ms},
                   {"gpu_ms", st.gpu_ms}};
     *report_json = dup(out.dump());

@@ -109,6 +109,17 @@ void make_batch(const nb_network* net, int64_t n, uint64_t seed, double* x,
   }
 }
 
+// Output columns whose tap iw = stride*ow - pad + kw lands inside [0, W):
+// ow >= first_tap(pad - kw) and ow <= last_tap(W - 1 + pad - kw).  Skipping
+// the others up front is the same MAC set (padded taps skipped,
+// I/nnet.hpp:121-123) and the same per-output summation order.
+inline int64_t first_tap(int64_t num, int64_t stride) {
+  return num <= 0 ? 0 : (num + stride - 1) / stride;
+}
+inline int64_t last_tap(int64_t num, int64_t stride) {
+  return num < 0 ? -1 : num / stride;
+}
+
 // Eq. 1-3 over the canonical MAC set of for_each_conv_mac (I/nnet.hpp:108-128)
 // / reference_conv (I/interp.hpp:151-186): for each range/group, out[co] +=
 // W[co, ci, kh, kw] * in[ci, s*oh-p+kh, s*ow-p+kw], padded taps skipped.
@@ -128,14 +139,14 @@ void conv_image(const nb_conv_spec* sp, const T* in, const T* w, T* out) {
           for (int64_t kw = 0; kw < s.kw; ++kw) {
             const T wv = w[((co * s.ci + ci) * s.kh + kh) * s.kw + kw];
             const T* ip = in + ci * H * Wd;
+            const int64_t ow0 = first_tap(s.pad - kw, s.stride),
+                          ow1 = std::min(OW, last_tap(Wd - 1 + s.pad - kw, s.stride) + 1);
             for (int64_t oh = 0; oh < OH; ++oh) {
               const int64_t ih = s.stride * oh - s.pad + kh;
               if (ih < 0 || ih >= H) continue;
-              for (int64_t ow = 0; ow < OW; ++ow) {
-                const int64_t iw = s.stride * ow - s.pad + kw;
-                if (iw < 0 || iw >= Wd) continue;
-                o[oh * OW + ow] += wv * ip[ih * Wd + iw];
-              }
+              T* orow = o + oh * OW;
+              const T* irow = ip + ih * Wd - s.pad + kw;
+              for (int64_t ow = ow0; ow < ow1; ++ow) orow[ow] += wv * irow[s.stride * ow];
             }
           }
     }
@@ -159,14 +170,14 @@ void dgrad_image(const nb_conv_spec* sp, const double* dy, const double* w, doub
           for (int64_t kw = 0; kw < s.kw; ++kw) {
             const double wv = w[((co * s.ci + ci) * s.kh + kh) * s.kw + kw];
             double* xp = dx + ci * H * Wd;
+            const int64_t ow0 = first_tap(s.pad - kw, s.stride),
+                          ow1 = std::min(OW, last_tap(Wd - 1 + s.pad - kw, s.stride) + 1);
             for (int64_t oh = 0; oh < OH; ++oh) {
               const int64_t ih = s.stride * oh - s.pad + kh;
               if (ih < 0 || ih >= H) continue;
-              for (int64_t ow = 0; ow < OW; ++ow) {
-                const int64_t iw = s.stride * ow - s.pad + kw;
-                if (iw < 0 || iw >= Wd) continue;
-                xp[ih * Wd + iw] += wv * d[oh * OW + ow];
-              }
+              double* xrow = xp + ih * Wd - s.pad + kw;
+              const double* drow = d + oh * OW;
+              for (int64_t ow = ow0; ow < ow1; ++ow) xrow[s.stride * ow] += wv * drow[ow];
             }
           }
     }

@@ -8,10 +8,13 @@
 //
 // Every entry point forwards to the reference function named in its comment;
 // no reference logic is restated here.
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "nestopt/nestopt.hpp"
@@ -281,6 +284,51 @@ int ref_search(const char* cfg_json, int jobs, char** out) {
     if (jobs > 0) cfg.jobs = jobs;
     SearchReport rep = run_search(net, cfg);
     *out = dup(search_report_to_json(rep).dump());
+  });
+}
+
+// The reference CPU arm of bench.py: fisher_potential (I/nnet.hpp:321) of
+// `count` networks, each scored on its own make_batch(net, n, batch_seed)
+// (I/nnet.hpp:87), scheduled exactly as evaluate_all does (I/search.hpp:
+// 315-334): `jobs` std::threads self-scheduling through next.fetch_add(1).
+// Every job pays what evaluate_candidate pays for a neural candidate's
+// score: network_from_json -> init_weights (the re-init repair_network
+// performs, I/nnet.hpp:372-381), make_batch and fisher_potential.
+// job_seconds[i] = that job's own duration, *wall_seconds = the whole pool.
+int ref_fisher_jobs(const char* const* net_jsons, int count, int64_t n,
+                    uint64_t batch_seed, int jobs, double* totals,
+                    double* job_seconds, double* wall_seconds) {
+  return guard([&] {
+    using clock = std::chrono::steady_clock;
+    std::atomic<int> next{0};
+    std::atomic<int> failed{0};
+    std::vector<std::string> errs(static_cast<size_t>(count));
+    auto worker = [&]() {
+      for (;;) {
+        const int i = next.fetch_add(1);
+        if (i >= count) return;
+        const auto t0 = clock::now();
+        try {
+          Network net = load_net(net_jsons[i]);
+          Batch batch = make_batch(net, static_cast<size_t>(n), batch_seed);
+          FisherReport rep = fisher_potential(net, batch);
+          if (totals) totals[i] = rep.total;
+        } catch (const std::exception& e) {
+          errs[static_cast<size_t>(i)] = e.what();
+          failed.fetch_add(1);
+        }
+        if (job_seconds)
+          job_seconds[i] = std::chrono::duration<double>(clock::now() - t0).count();
+      }
+    };
+    const auto t0 = clock::now();
+    std::vector<std::thread> pool;
+    for (int j = 0; j < std::max(1, jobs); ++j) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    if (wall_seconds) *wall_seconds = std::chrono::duration<double>(clock::now() - t0).count();
+    if (failed.load())
+      for (const auto& e : errs)
+        if (!e.empty()) throw Error(e);
   });
 }
 

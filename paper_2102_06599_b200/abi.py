@@ -69,7 +69,9 @@ class KernelStatC(C.Structure):
 
 class EvalStatsC(C.Structure):
     _fields_ = [("evaluated", C.c_int64), ("deduplicated", C.c_int64),
-                ("est_flops", C.c_double * 16), ("busy_ms", C.c_double * 16)]
+                ("requeued", C.c_int64), ("failed_sessions", C.c_int32),
+                ("reserved", C.c_int32), ("est_flops", C.POINTER(C.c_double)),
+                ("busy_ms", C.POINTER(C.c_double)), ("evaluations", C.POINTER(C.c_int64))]
 
 
 P = C.POINTER

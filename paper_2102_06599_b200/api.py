@@ -66,13 +66,15 @@ class Precision:
 # conv outputs relative to sum |w||x|.  RECHECK_BAND is the near-threshold band
 # of the search driver: a candidate whose score is within it of the origin's
 # is re-scored in SIMT mode before the accept decision
-# (integration/nestopt_b200.hpp, kept equal to these values).
+# (integration/nestopt_b200.hpp recheck_band, kept equal to these values).
 TOLERANCE = {
     Precision.SIMT: {"total": 1e-5, "layer": 1e-4, "conv": 2e-6},
     Precision.FP32: {"total": 5e-4, "layer": 5e-3, "conv": 1e-5},
     Precision.TF32: {"total": 5e-2, "layer": 2e-1, "conv": 2e-3},
 }
-RECHECK_BAND = {Precision.SIMT: 0.0, Precision.FP32: 5e-4, Precision.TF32: 5e-2}
+# 2.5 x the total tolerance: candidate and origin may each be off by the
+# tolerance in opposite directions (integration/nestopt_b200.hpp recheck_band)
+RECHECK_BAND = {Precision.SIMT: 0.0, Precision.FP32: 1.25e-3, Precision.TF32: 1.25e-1}
 
 
 # ---------------------------------------------------------------------------
@@ -636,8 +638,11 @@ def fisher_sharded(shards: Sequence[Session], net: Network,
 class EvalStats:
     evaluated: int
     deduplicated: int
-    est_flops: List[float]
-    busy_ms: List[float]
+    est_flops: List[float]    # per session: estimated FLOPs it ran
+    busy_ms: List[float]      # per session: device time of its evaluations
+    evaluations: List[int] = field(default_factory=list)  # per session
+    requeued: int = 0         # evaluations handed back after a device failure
+    failed_sessions: int = 0
 
 
 def evaluate(sessions: Sequence[Session], nets: Sequence[Network],
@@ -653,9 +658,13 @@ def evaluate(sessions: Sequence[Session], nets: Sequence[Network],
     bufs = [_fisher_buffers(n, sessions[0].n) for n in nets]
     outs = (abi.FisherOutC * max(1, len(nets)))(*[b[0] for b in bufs])
     sp = (C.c_void_p * len(sessions))(*[s.ptr for s in sessions])
-    st = abi.EvalStatsC()
+    est = np.zeros(len(sessions))
+    busy = np.zeros(len(sessions))
+    done = np.zeros(len(sessions), np.int64)
+    st = abi.EvalStatsC(0, 0, 0, 0, 0, _dp(est), _dp(busy),
+                        done.ctypes.data_as(C.POINTER(C.c_int64)))
     _check(abi.load().nb_evaluate(sp, len(sessions), arr, len(nets), precision, outs,
                                   C.byref(st)))
     reps = [_report(n, outs[i], b[1], b[2], b[3]) for i, (n, b) in enumerate(zip(nets, bufs))]
-    return reps, EvalStats(st.evaluated, st.deduplicated, list(st.est_flops[:len(sessions)]),
-                           list(st.busy_ms[:len(sessions)]))
+    return reps, EvalStats(st.evaluated, st.deduplicated, est.tolist(), busy.tolist(),
+                           done.tolist(), st.requeued, st.failed_sessions)

@@ -852,6 +852,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     fail(NB_ERR_CONFIG, "network class count does not match the session batch");
   const int64_t N = s->n, L = net.L(), K = net.num_classes;
   cudaStream_t st = c->stream;
+  NB_CUDA(cudaEventRecord(c->ev_start, st));
   c->prof.start_eval();
   using clk = std::chrono::steady_clock;
   auto tp = clk::now();
@@ -1046,6 +1047,7 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     }
   }
   NB_CUDA(cudaGetLastError());
+  NB_CUDA(cudaEventRecord(c->ev_done, st));
   pend.s = s;
   pend.out = out;
   pend.backward = backward;
@@ -1093,6 +1095,27 @@ void run_finish(Pending& pend) {
     if (out.per_channel) std::memcpy(out.per_channel, pend.h_perch, size_t(pend.ch_total) * 8);
     if (out.total) *out.total = tot;
   }
+}
+
+bool run_ready(const Pending& pend) {
+  if (!pend.active) return true;
+  nb_ctx* c = pend.s->ctx;
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  ctx_activate(c);
+  const cudaError_t e = cudaEventQuery(c->ev_done);
+  if (e == cudaErrorNotReady) {
+    (void)cudaGetLastError();  // not an error: clear it
+    return false;
+  }
+  return true;  // done, or failed (run_finish reports it)
+}
+
+double run_device_ms(nb_ctx* c) {
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  ctx_activate(c);
+  float ms = 0.f;
+  NB_CUDA(cudaEventElapsedTime(&ms, c->ev_start, c->ev_done));
+  return double(ms);
 }
 
 void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
@@ -1262,6 +1285,8 @@ nb_status nb_ctx_create(int device, nb_ctx** out) {
     }();
     if (prefer_shared) NB_CUDA(cudaDeviceSetCacheConfig(cudaFuncCachePreferShared));
     NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    NB_CUDA(cudaEventCreate(&c->ev_start));
+    NB_CUDA(cudaEventCreate(&c->ev_done));
     *out = c.release();
   });
 }
@@ -1274,8 +1299,11 @@ nb_status nb_ctx_destroy(nb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStream_t st = ctx->stream;
+    cudaEvent_t e0 = ctx->ev_start, e1 = ctx->ev_done;
     delete ctx;
     cudaStreamDestroy(st);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
   });
 }
 
@@ -1411,11 +1439,17 @@ nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count, const nb_n
     int64_t ch_total = 0;
     for (int64_t l = 0; l < L; ++l) ch_total += d.specs[l].co_eff();
     nb_ctx* root = shards[0]->ctx;
-    {
-      std::lock_guard<std::recursive_mutex> lk(root->mu);
-      ctx_activate(root);
-      root->shard_s.ensure(size_t(n_all * ch_total) * 8);
-    }
+    // Every shard context stays locked for the whole call (in one global
+    // order, so concurrent sharded calls cannot deadlock): the gather
+    // buffers are sized, written by the shards and read by the root's
+    // reduction without another call resizing or overwriting them between.
+    std::vector<nb_ctx*> held;
+    for (int32_t i = 0; i < count; ++i) held.push_back(shards[i]->ctx);
+    std::sort(held.begin(), held.end(), std::less<nb_ctx*>());
+    std::vector<std::unique_lock<std::recursive_mutex>> locks;
+    for (nb_ctx* c : held) locks.emplace_back(c->mu);
+    ctx_activate(root);
+    root->shard_s.ensure(size_t(n_all * ch_total) * 8);
     std::vector<double> ex_loss(static_cast<size_t>(n_all));
     std::vector<Pending> pend(static_cast<size_t>(count));
     std::vector<int64_t> first(static_cast<size_t>(count));
@@ -1425,7 +1459,6 @@ nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count, const nb_n
       first[size_t(i)] = n0;
       double* s_dev = root->shard_s.as<double>();
       if (i > 0) {
-        std::lock_guard<std::recursive_mutex> lk(sh->ctx->mu);
         ctx_activate(sh->ctx);
         sh->ctx->shard_s.ensure(size_t(sh->n * ch_total) * 8);
         s_dev = sh->ctx->shard_s.as<double>();
@@ -1444,7 +1477,6 @@ nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count, const nb_n
     out->loss = lsum / double(n_all);
     out->seed = shards[0]->seed;
 
-    std::lock_guard<std::recursive_mutex> lk(root->mu);
     ctx_activate(root);
     cudaStream_t st = root->stream;
     double* S = root->shard_s.as<double>();

@@ -145,6 +145,9 @@ struct nb_ctx {
   nb::DevBuf shard_s, shard_aux;  // example-sharded Fisher (nb_fisher_sharded)
   int num_sms = 148;
   nb::PinnedBuf host_io, host_out;
+  // bracket the evaluation in flight on this context's stream (one at a
+  // time): its device duration and completion, for the scheduler
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
   // device copies of z streams keyed by (seed, stream index)
   std::map<std::pair<uint64_t, int64_t>, std::unique_ptr<nb::DevBuf>> zdev;
   std::map<std::pair<uint64_t, int64_t>, int64_t> zlen;
@@ -211,6 +214,11 @@ struct Pending {
 void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
                  bool backward, const RunOut& out, Pending& pend);
 void run_finish(Pending& pend);
+// The evaluation's kernels and result copies have completed on the device
+// (run_finish will not block).
+bool run_ready(const Pending& pend);
+// Device time of the last evaluation collected on the context (ms).
+double run_device_ms(nb_ctx* c);
 void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
                  bool backward, const RunOut& out);
 

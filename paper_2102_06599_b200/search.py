@@ -34,6 +34,8 @@ def load() -> C.CDLL:
         lib.nbi_run_search.restype = C.c_int
         lib.nbi_run_search.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p)]
+        lib.nbi_near_threshold.restype = C.c_int
+        lib.nbi_near_threshold.argtypes = [C.c_double, C.c_double, C.c_int]
         lib.nbi_execute.restype = C.c_int
         lib.nbi_execute.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p,
                                     C.c_void_p]
@@ -68,6 +70,12 @@ def run_search_gpu(cfg: dict, devices: str = "0", precision: int = Precision.FP3
         return json.loads(C.cast(p, C.c_char_p).value.decode())
     finally:
         lib.nbi_free(p)
+
+
+def near_threshold(cand: float, origin: float, precision: int) -> bool:
+    """Whether the search driver re-scores this candidate in SIMT before the
+    accept decision (integration/nestopt_b200.hpp near_threshold)."""
+    return bool(load().nbi_near_threshold(cand, origin, int(precision)))
 
 
 def gate_candidates(cfg: dict, legal_device: int = -1) -> list:

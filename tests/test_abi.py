@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(abi.SIGNATURES), declared ^ set(abi.SIGNATURES)
-    assert abi.load().nb_abi_version() == 1
+    assert abi.load().nb_abi_version() == 2
 
 
 def test_spec_validation_errors():
