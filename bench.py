@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "simt"])
     p.add_argument("--streams", type=int, default=4, help="concurrent sessions per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-peaks", action="store_true", help="skip the peak microbenchmarks")
     p.add_argument("--no-modes", action="store_true",
                    help="skip the other precision tiers' figures")
     p.add_argument("--no-kernel-events", action="store_true",
@@ -72,6 +73,49 @@ def peaks():
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
             "fallback"
+
+
+def measured_peaks():
+    """The peaks of the arithmetic nb200 issues, measured on this GPU now
+    (scripts/peaks/peaks.cu): dense tcgen05 kind::tf32 and kind::f16 (bf16)
+    issue rates on every SM, fp32 FFMA, plus cuBLAS TF32 (torch.matmul
+    8192^3 fp32 with TF32 allowed) as a library cross-check."""
+    import ctypes as C
+    import torch
+    out = {}
+    so = os.path.join(ROOT, "scripts", "peaks", "libnb200_peaks.so")
+    if os.path.exists(so):
+        lib = C.CDLL(so)
+        lib.nbp_tc_tflops.restype = C.c_double
+        lib.nbp_tc_tflops.argtypes = [C.c_int]
+        lib.nbp_ffma_tflops.restype = C.c_double
+        out["tcgen05_tf32_tflops"] = lib.nbp_tc_tflops(0)
+        out["tcgen05_bf16_tflops"] = lib.nbp_tc_tflops(1)
+        out["ffma_fp32_tflops"] = lib.nbp_ffma_tflops()
+    try:
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(8192, 8192, device="cuda")
+        b = torch.randn(8192, 8192, device="cuda")
+        for _ in range(3):
+            a @ b
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out["cublas_tf32_tflops"] = 2 * 8192 ** 3 / (best / 1e3) / 1e12
+        torch.backends.cuda.matmul.allow_tf32 = prev
+        del a, b
+    except Exception as e:  # pragma: no cover
+        out["cublas_tf32_error"] = str(e)
+    out["how"] = ("scripts/peaks/peaks.cu: one launch of 148 CTAs, M=128 N=256 tcgen05.mma "
+                  "back to back from shared-memory operands, CUDA events; FFMA 8 chains/thread")
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -388,6 +432,7 @@ def main():
     # rank's timed pool (in the concurrent timed region a launch's event time
     # also covers other streams' kernels sharing the SMs; both are reported)
     pk, pk_kind = peaks()
+    pk_meas = measured_peaks() if not args.no_peaks else {}
 
     def roofline(stats, note):
         kern = {k: v for k, v in stats.items() if not k.startswith("host_")}
@@ -400,16 +445,16 @@ def main():
             ach = dom["flops"] / dom["launches"] / (avg_ms / 1e3) / 1e12
             r = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"],
                  "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"],
-                 "peak_source": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json); 3xTF32 "
-                                "issues 3 tf32 MMAs (tf32 = bf16/2) per fp32 product, so the "
-                                "kernel's own ceiling is peak/6"}
-            # the arithmetic the precision mode issues: 3xTF32 = 3 tf32 MMAs
-            # per fp32 product at half the bf16 rate; TF32 = 1 at half rate
-            div = {"fp32": 6.0, "tf32": 2.0}.get(args.precision)
-            if div:
-                r["kernel_ceiling"] = {"value": pk["bf16_tflops"] / div, "unit": "TFLOP/s",
-                                       "frac": ach / (pk["bf16_tflops"] / div),
-                                       "mode": args.precision}
+                 "peak_source": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json); "
+                                "kernel_ceiling = the measured peak of the arithmetic issued"}
+            # the arithmetic the precision mode issues, against its MEASURED
+            # peak: 3xTF32 = 3 tf32 MMAs per fp32 product, TF32 = 1
+            mp = pk_meas.get("tcgen05_tf32_tflops")
+            div = {"fp32": 3.0, "tf32": 1.0}.get(args.precision)
+            if div and mp and mp > 0:
+                r["kernel_ceiling"] = {"value": mp / div, "unit": "TFLOP/s",
+                                       "frac": ach / (mp / div), "mode": args.precision,
+                                       "source": "measured tcgen05 kind::tf32 peak / %g" % div}
         else:
             ach = dom["bytes"] / dom["launches"] / (avg_ms / 1e3) / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -482,6 +527,7 @@ def main():
                           "busy_ms": [round(b, 2) for b in st.busy_ms]},
             "roofline": roof,
             "roofline_concurrent": roof_conc,
+            "peaks_measured": pk_meas,
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3)}
                         for k, v in kstats.items()},
             "cpu_baseline": cpu,
