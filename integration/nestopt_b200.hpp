@@ -711,10 +711,11 @@ inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
   return true;
 }
 
-// Stated tolerance of each arithmetic mode on Fisher totals (DESIGN.md
-// section 3, paper_2102_06599_b200/api.py TOLERANCE["total"]).
+// Stated tolerance of each arithmetic mode on Fisher totals of deep chains
+// (paper_2102_06599_b200/api.py TOLERANCE_DEEP: the
+// 33-layer ResNet-34 chain at N=128).
 inline double total_tolerance(nb_precision p) {
-  return p == NB_PREC_FP32 ? 5e-4 : p == NB_PREC_TF32 ? 5e-2 : 1e-5;
+  return p == NB_PREC_FP32 ? 1.5e-3 : p == NB_PREC_TF32 ? 5e-2 : 3e-4;
 }
 
 // Near-threshold band of a throughput mode (api.py RECHECK_BAND): a
@@ -722,9 +723,10 @@ inline double total_tolerance(nb_precision p) {
 // tolerance in opposite directions, so a decision can only differ from the
 // reference's when |cand - origin| <= 2 x tolerance; the band adds 25% on
 // top.  Candidates inside it are re-scored, with the origin, in
-// NB_PREC_SIMT (fp32 FFMA, totals within 1e-5 of the fp64 reference) before
-// the accept decision.  Only ties closer than SIMT's own 2 x 1e-5 can then
-// differ from the reference (the documented near-threshold tie band).
+// NB_PREC_SIMT (true fp32, totals within 3e-4 of the fp64 reference on the
+// 33-layer chain) before the accept decision.  Only ties closer than SIMT's
+// own 2 x 3e-4 can then differ from the reference (the documented
+// near-threshold tie band, api.py TIE_BAND).
 inline double recheck_band(nb_precision p) {
   return p == NB_PREC_SIMT ? 0.0 : 2.5 * total_tolerance(p);
 }

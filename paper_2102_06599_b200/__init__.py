@@ -7,7 +7,7 @@ API; ``abi`` is the raw ctypes binding.
 """
 from .api import (  # noqa: F401
     Batch, ChannelSplit, ConfigError, Context, ConvSpec, CudaError, Error, EvalStats,
-    RECHECK_BAND, TOLERANCE, FisherReport, ForwardCache, InvalidSpec, Layer, Network, NoDevice, Precision, Session,
+    RECHECK_BAND, TIE_BAND, TOLERANCE, TOLERANCE_DEEP, FisherReport, ForwardCache, InvalidSpec, Layer, Network, NoDevice, Precision, Session,
     ShapeMismatch, Unsupported, activation_gradients, conv_dgrad, count_macs,
     default_context, device_count, evaluate, fisher_accepts, fisher_flops, fisher_potential,
     fisher_sharded, shard_batch,

@@ -63,18 +63,33 @@ class Precision:
 
 # Stated tolerances against the fp64 reference, measured
 # on the GPU: relative error of Fisher totals and per-layer values, and of
-# conv outputs relative to sum |w||x|.  RECHECK_BAND is the near-threshold band
-# of the search driver: a candidate whose score is within it of the origin's
-# is re-scored in SIMT mode before the accept decision
-# (integration/nestopt_b200.hpp recheck_band, kept equal to these values).
+# conv outputs relative to sum |w||x|.  TOLERANCE holds for chains of up to
+# ~10 layers (the reference's goldens, tests/test_gpu_parity.py);
+# TOLERANCE_DEEP for the benchmarked 33-layer ResNet-34 chain at N=128
+# (tests/test_r34_parity.py), where even true fp32 (SIMT) sits ~1e-4 from
+# fp64: rounding flips ReLU masks of near-zero activations, and every flip
+# re-routes gradient through 30 more layers (measured SIMT totals 1.4e-4,
+# layers 7.3e-4; 3xTF32 8.0e-4 / 2.4e-3, biased low by the tensor core's
+# truncating accumulation, profiles/r02_precision.md; TF32 3.0e-2 / 3.9e-2).
+# RECHECK_BAND is the near-threshold band of the search driver: a candidate
+# whose score is within it of the origin's is re-scored in SIMT mode before
+# the accept decision (integration/nestopt_b200.hpp recheck_band, kept equal
+# to these values): 2.5 x the deep total tolerance, since the candidate and
+# the origin may each be off by it in opposite directions.
 TOLERANCE = {
     Precision.SIMT: {"total": 1e-5, "layer": 1e-4, "conv": 2e-6},
     Precision.FP32: {"total": 5e-4, "layer": 5e-3, "conv": 1e-5},
     Precision.TF32: {"total": 5e-2, "layer": 2e-1, "conv": 2e-3},
 }
-# 2.5 x the total tolerance: candidate and origin may each be off by the
-# tolerance in opposite directions (integration/nestopt_b200.hpp recheck_band)
-RECHECK_BAND = {Precision.SIMT: 0.0, Precision.FP32: 1.25e-3, Precision.TF32: 1.25e-1}
+TOLERANCE_DEEP = {
+    Precision.SIMT: {"total": 3e-4, "layer": 1.5e-3},
+    Precision.FP32: {"total": 1.5e-3, "layer": 5e-3},
+    Precision.TF32: {"total": 5e-2, "layer": 2e-1},
+}
+RECHECK_BAND = {Precision.SIMT: 0.0, Precision.FP32: 3.75e-3, Precision.TF32: 1.25e-1}
+# decisions closer than this to the origin may differ from the fp64
+# reference even after the SIMT recheck (the documented near-threshold ties)
+TIE_BAND = 2 * TOLERANCE_DEEP[Precision.SIMT]["total"]
 
 
 # ---------------------------------------------------------------------------

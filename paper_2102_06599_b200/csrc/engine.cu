@@ -356,7 +356,9 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           // example shard runs the whole batch's kernels (same split-K, so
           // the same summation order per output)
           const int mt = m_tiles_at(g.OH, g.OW, plan_n, g.S);
-          const bool kwf = G == 1 && !dense && use_kwf(g, sco, t.BW);
+          // (kw-fused B layouts are [kw][co][kh][ci] with K = KH x sci: no
+          // K padding, so a padded K runs the plain tap-major plan)
+          const bool kwf = G == 1 && !dense && sci % 32 == 0 && use_kwf(g, sco, t.BW);
           const int pbn = kwf ? 0 : pick_pair_bn(sco, mt, P.split3);
           int bn = pbn ? pbn : pick_bn(sco, P.split3);
           static const int gran = [] {  // NB_TC_PADG: fprop padded-width granularity
@@ -473,7 +475,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
       const int gh = (g.H + g.S - 1) / g.S, gw = (g.W + g.S - 1) / g.S;
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
         const int mt = m_tiles_at(gh, gw, plan_n, 1);
-        const bool kwf = DG == 1 && !ddense && use_kwf(g, dsci, t.BW);
+        const bool kwf = DG == 1 && !ddense && dsco % 32 == 0 && use_kwf(g, dsci, t.BW);
         const int pbn = kwf ? 0 : pick_pair_bn(dsci, mt * t.nphase, P.split3);
         int bn = pbn ? pbn : pick_bn(dsci, P.split3);
         if (!bn && dpad_ok) bn = pick_bn_padded(dsci, P.split3);

@@ -271,6 +271,13 @@ PAD_SPECS = [
     ConvSpec(20, 16, 7, 7, 3, 3, 1, 1),                        # K 20 -> 32, N 16 of 32
     ConvSpec(64, 48, 8, 8, 3, 3, 1, 1,
              channel_splits=[ChannelSplit(0, 16, 1), ChannelSplit(16, 48, 1)]),  # padded range
+    # 64-wide outputs over power-of-two rows (kw-fused shape) with a padded K:
+    # fprop K 16 / 48 -> 32 / 64, dgrad K (= Co) 16 -> 32 (round 2: R34 bottleneck
+    # candidates, b4 into a 64-channel stage; the kw-fused plan must not take these)
+    ConvSpec(16, 64, 32, 32, 3, 3, 1, 1),
+    ConvSpec(16, 64, 16, 8, 3, 3, 1, 1),
+    ConvSpec(48, 64, 8, 8, 3, 3, 1, 1),
+    ConvSpec(64, 16, 32, 32, 3, 3, 1, 1),
 ]
 # densified grouped ranges: a few groups of slices off the 32-channel chunk
 # run as one GEMM over block-diagonal weights
@@ -366,6 +373,37 @@ def test_tc_chain_fisher_matches_oracle(ctx, oracle, prec):
     assert math.isclose(rep.total, o["total"], rel_tol=t_tot), (rep.total, o["total"])
     np.testing.assert_allclose(rep.per_layer, o["per_layer"], rtol=t_layer)
     assert math.isclose(rep.loss, o["loss"], rel_tol=t_tot)
+
+
+# chains that lower to every tensor-core plan family inside the Fisher
+# pipeline (kw-fused, padded K in fprop and dgrad, bottleneck into a kw-fused
+# width, densified groups, col stem), scored against the oracle layer by layer
+PLAN_CHAINS = {
+    "padded_into_kwf": [ConvSpec(3, 16, 32, 32, 3, 3, 1, 1), ConvSpec(16, 64, 32, 32, 3, 3, 1, 1),
+                        ConvSpec(64, 64, 32, 32, 3, 3, 1, 1)],
+    "b4_g2_into_64": [ConvSpec(3, 64, 32, 32, 3, 3, 1, 1),
+                      ConvSpec(64, 64, 32, 32, 3, 3, 1, 1, groups=2, bottleneck_out=4),
+                      ConvSpec(16, 64, 32, 32, 3, 3, 1, 1), ConvSpec(64, 64, 32, 32, 3, 3, 1, 1)],
+    "crop_rows_8": [ConvSpec(3, 64, 16, 16, 3, 3, 1, 1),
+                    ConvSpec(64, 48, 16, 16, 3, 3, 1, 1, spatial_div_w=2),
+                    ConvSpec(48, 64, 16, 8, 3, 3, 1, 1), ConvSpec(64, 64, 16, 8, 3, 3, 1, 1)],
+    "dense_g4_s2": [ConvSpec(3, 32, 16, 16, 3, 3, 1, 1),
+                    ConvSpec(32, 64, 16, 16, 3, 3, 2, 1, groups=4),
+                    ConvSpec(64, 64, 8, 8, 3, 3, 1, 1, groups=8)],
+}
+
+
+@pytest.mark.parametrize("prec", [Precision.SIMT, Precision.FP32, Precision.TF32])
+@pytest.mark.parametrize("name", sorted(PLAN_CHAINS))
+def test_plan_family_chains_match_oracle(ctx, oracle, name, prec):
+    net = Network([Layer(s) for s in PLAN_CHAINS[name]], num_classes=10, seed=42)
+    for n in (4, 33):
+        batch = nb.make_batch(net, n, 1)
+        rep = nb.fisher_potential(net, batch, precision=prec, ctx=ctx)
+        o = oracle.fisher(net, n, batch=batch)
+        t_tot, t_layer, _, _ = TOL[prec]
+        assert math.isclose(rep.total, o["total"], rel_tol=t_tot), (n, rep.total, o["total"])
+        np.testing.assert_allclose(rep.per_layer, o["per_layer"], rtol=t_layer, err_msg=str(n))
 
 
 def test_tc_chain_gradients_match_oracle(ctx, oracle):

@@ -10,9 +10,11 @@ origin and on bench-pool candidates covering depthwise, crop, bottleneck
 (co_eff down to 1), grouped G<=8 (densified tensor-core plans) and G>8
 (FFMA), masks on the stem, a stride-2 layer and the 512-channel stage.
 
-Stated tolerances (paper_2102_06599_b200/api.py TOLERANCE):
-totals / per-layer relative, per-channel against the largest layer's value,
-loss 1e-6 relative, probabilities 1e-6 absolute.
+Stated tolerances (paper_2102_06599_b200/api.py TOLERANCE_DEEP, DESIGN.md
+3): totals / per-layer relative, per-channel against the largest layer's
+value, loss 1e-6 relative, probabilities 1e-6 absolute.  At this depth true
+fp32 (SIMT) itself sits ~1e-4 from fp64 (ReLU-mask flips of near-zero
+activations re-route the gradient), which sets the floor of every mode.
 """
 import json
 import math
@@ -72,7 +74,7 @@ def r34_session():
 @pytest.mark.parametrize("prec", [Precision.FP32, Precision.SIMT, Precision.TF32],
                          ids=["fp32_3xtf32", "simt", "tf32"])
 def test_r34_n128_fisher_matches_oracle(r34_session, prec):
-    tol = nb.TOLERANCE[prec]
+    tol = nb.TOLERANCE_DEEP[prec]
     reps = {}
     for e, net, pc, probs in _nets():
         rep = r34_session.fisher(net, prec)
@@ -92,7 +94,7 @@ def test_r34_n128_fisher_matches_oracle(r34_session, prec):
     o_gpu, o_ref = reps["origin"].total, golden("r34_n128.json")["networks"][0]["total"]
     for e, *_ in _nets()[1:]:
         margin = (e["total"] - o_ref) / o_ref
-        if abs(margin) <= 2 * tol["total"]:
+        if abs(margin) <= max(nb.RECHECK_BAND[prec], nb.TIE_BAND):
             continue  # decided by the search driver's SIMT recheck
         assert (reps[e["name"]].total >= o_gpu) == (e["total"] >= o_ref), (e["name"], margin)
 
@@ -101,10 +103,12 @@ def test_r34_n128_fisher_matches_oracle(r34_session, prec):
 @needs_golden
 def test_r34_n128_simt_decisions_exact(r34_session):
     """The SIMT tier (the near-tie recheck's arithmetic) decides every golden
-    candidate exactly as the fp64 oracle does."""
+    candidate outside the documented tie band exactly as the fp64 oracle."""
     o_ref = golden("r34_n128.json")["networks"][0]["total"]
     o = r34_session.fisher(_nets()[0][1], Precision.SIMT).total
     for e, net, *_ in _nets()[1:]:
+        if abs(e["total"] - o_ref) / o_ref <= nb.TIE_BAND:
+            continue
         got = r34_session.fisher(net, Precision.SIMT).total
         assert (got >= o) == (e["total"] >= o_ref), e["name"]
 
