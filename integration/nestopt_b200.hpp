@@ -26,6 +26,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
+#include <stdexcept>
 #include <random>
 #include <sstream>
 #include <map>
@@ -39,9 +41,23 @@
 
 namespace nb200 {
 
-// A CUDA / device failure surfaced through the reference's error hierarchy.
-struct DeviceError : nestopt::Error {
-  using nestopt::Error::Error;
+// A CUDA / device failure.  Deliberately NOT a nestopt::Error: the
+// reference's evaluate_candidate turns nestopt::Error into a semantic
+// rejection, and a device failure must end the search, not reject candidates.
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// A semantic run the GPU legality kernel cannot key (nb_semantic_legality
+// NB_ERR_UNSUPPORTED, or a nest the bridge cannot compile).  There is no
+// host fallback on the search path: the search fails loudly.
+struct LegalityUnsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Which implementation answered the semantic-legality checks of a gate pass.
+struct LegalityCounts {
+  std::atomic<long long> gpu{0}, host{0};
 };
 
 // nb_status -> the nestopt exception class it mirrors (include/nb200.h).
@@ -552,20 +568,18 @@ class LegalNest {
 
 // check_semantic_legality (I/transforms.hpp:598-663) with the brute-force
 // dependence check on the GPU (nb_semantic_legality): the same CapExceeded
-// throws, verdicts and reasons.  Nests smaller than `gpu_min_instances` (a
-// device round trip costs more than the host check) and nests the kernel
-// cannot key in 64 bits run the reference's own function.
+// throws (checked on the host from instance counts, as the reference does
+// first), verdicts and reasons.  Every check runs on the device -- there is
+// no host fallback; a nest the kernel cannot key throws LegalityUnsupported.
 inline nestopt::LegalityResult check_semantic_legality(
     Context& ctx, const nestopt::LoopNest& original, const nestopt::LoopNest& transformed,
-    long long cap = nestopt::kDefaultInstanceCap, long long gpu_min_instances = 0) {
+    long long cap = nestopt::kDefaultInstanceCap) {
   using namespace nestopt;
   const long long nt = instance_count(transformed);
   if (nt > cap) throw CapExceeded("transformed nest exceeds brute-force cap");
   const long long no = instance_count(original);
   if (no > cap)
     throw CapExceeded("instance count exceeds brute-force cap of " + std::to_string(cap));
-  if (std::max(nt, no) < gpu_min_instances)
-    return nestopt::check_semantic_legality(original, transformed, cap);
   std::map<std::string, int> tensor_ids;  // I/ir.hpp:347-352 interning order
   for (const auto& part : original.parts)
     for (const auto& st : part.stmts)
@@ -580,13 +594,14 @@ inline nestopt::LegalityResult check_semantic_legality(
   try {
     lo = std::make_unique<detail::LegalNest>(original, sid, &tensor_ids, &written);
     lt = std::make_unique<detail::LegalNest>(transformed, sid, nullptr, nullptr);
-  } catch (const std::exception&) {
-    // a nest the bridge cannot compile: the reference reports its own error
-    return nestopt::check_semantic_legality(original, transformed, cap);
+  } catch (const std::exception& e) {
+    throw LegalityUnsupported(std::string("semantic legality: nest not compilable for the GPU "
+                                          "check: ") + e.what());
   }
   nb_legal_out out{};
   const nb_status s = nb_semantic_legality(ctx.get(), lo->get(), lt->get(), &out);
-  if (s == NB_ERR_UNSUPPORTED) return nestopt::check_semantic_legality(original, transformed, cap);
+  if (s == NB_ERR_UNSUPPORTED)
+    throw LegalityUnsupported(std::string("semantic legality: ") + nb_last_error());
   check(s);
   switch (out.verdict) {
     case NB_LEGAL: return {Verdict::Legal, ""};
@@ -618,7 +633,7 @@ inline nestopt::LegalityResult check_semantic_legality(
 inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
                        const nestopt::SearchConfig& cfg,
                        const nestopt::FisherReport& origin_fisher, nestopt::Network& net,
-                       Context* legal_ctx = nullptr, long long legal_gpu_min = 0) {
+                       Context* legal_ctx = nullptr, LegalityCounts* counts = nullptr) {
   using namespace nestopt;
   std::vector<ConvSpec> specs;
   for (size_t l = 0; l < origin.layers.size(); ++l) {
@@ -628,9 +643,9 @@ inline bool host_gates(nestopt::Candidate& cand, const nestopt::Network& origin,
     auto flush = [&](size_t s) {
       if (!pending_semantic) return true;
       LegalityResult lr =
-          legal_ctx ? nb200::check_semantic_legality(*legal_ctx, run_origin, nest, cfg.cap,
-                                                     legal_gpu_min)
+          legal_ctx ? nb200::check_semantic_legality(*legal_ctx, run_origin, nest, cfg.cap)
                     : nestopt::check_semantic_legality(run_origin, nest, cfg.cap);
+      if (counts) ++(legal_ctx ? counts->gpu : counts->host);
       pending_semantic = false;
       if (lr.verdict == Verdict::Illegal) {
         cand.status = CandidateStatus::RejectedSemantic;
@@ -805,17 +820,10 @@ inline std::vector<nestopt::Candidate> draw_candidates(const nestopt::Network& o
   return out;
 }
 
-// Instance count from which a semantic run is checked on the GPU
-// (NB_LEGAL_GPU_MIN; -1 = always on the host).  Below it the host check is
-// faster than a device round trip.
-inline long long legal_gpu_min() {
-  const char* e = std::getenv("NB_LEGAL_GPU_MIN");
-  return e && *e ? std::atoll(e) : 1000;
-}
-
 // Scheduler statistics of one evaluate_all_gpu call.
 struct GpuStats {
   int64_t scored = 0, evaluated = 0, deduplicated = 0, origin_equal = 0, rechecked = 0;
+  int64_t legality_gpu = 0, legality_host = 0;  // semantic runs checked on each side
   int64_t rank_rechecked = 0, requeued = 0;
   std::vector<double> est_flops, busy_ms;
   std::vector<int64_t> evaluations;
@@ -841,18 +849,28 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
   {
     const int jobs = std::max(1, std::min<int>(cfg.jobs, int(cands.size())));
     std::atomic<size_t> next{0};
-    // each gate thread checks semantic runs on its own context of a session's GPU
-    const long long gpu_min = legal_gpu_min();
+    LegalityCounts counts;
+    std::exception_ptr err;
+    std::mutex err_mu;
+    // each gate thread checks its semantic runs on its own context of a
+    // session's GPU (every check on the device, none on the host)
     auto worker = [&](int j) {
-      std::unique_ptr<Context> lctx;
-      for (;;) {
-        const size_t i = next.fetch_add(1);
-        if (i >= cands.size()) return;
-        if (!lctx && gpu_min >= 0 && !sessions.empty())
-          lctx = std::make_unique<Context>(
-              nb_ctx_device(nb_session_ctx(sessions[size_t(j) % sessions.size()]->get())));
-        pending[i] =
-            host_gates(cands[i], origin, cfg, origin_fisher, nets[i], lctx.get(), gpu_min) ? 1 : 0;
+      try {
+        std::unique_ptr<Context> lctx;
+        for (;;) {
+          const size_t i = next.fetch_add(1);
+          if (i >= cands.size()) return;
+          if (!lctx && !sessions.empty())
+            lctx = std::make_unique<Context>(
+                nb_ctx_device(nb_session_ctx(sessions[size_t(j) % sessions.size()]->get())));
+          pending[i] =
+              host_gates(cands[i], origin, cfg, origin_fisher, nets[i], lctx.get(), &counts) ? 1
+                                                                                             : 0;
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (!err) err = std::current_exception();
+        next = cands.size();  // the other gate threads stop too
       }
     };
     if (jobs == 1) {
@@ -862,6 +880,9 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
       for (int j = 0; j < jobs; ++j) pool.emplace_back(worker, j);
       for (auto& t : pool) t.join();
     }
+    if (err) std::rethrow_exception(err);
+    st.legality_gpu = counts.gpu.load();
+    st.legality_host = counts.host.load();
   }
   auto t1 = std::chrono::steady_clock::now();
   // A candidate whose network is the origin's (e.g. bottleneck(ci) undone by
@@ -971,27 +992,35 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
       }
     }
     // rank_survivors (I/search.hpp:338-349) orders equal-MAC survivors by
-    // their totals: survivors whose totals are within the mode's band of an
-    // equal-MAC neighbour are re-scored in SIMT too, so that order is the
-    // reference's except for ties inside SIMT's own tolerance
+    // their totals.  An equal-MAC group holding two different totals within
+    // the mode's band of each other is re-scored entirely in SIMT (its scored
+    // members; members carrying the origin's score -- non-neural survivors
+    // and networks equal to the origin -- take the origin's SIMT score), so
+    // the group's order is the reference's except for ties inside SIMT's own
+    // tolerance.  Identical networks keep identical totals (dedupe).
     if (recheck_band(prec) > 0) {
+      std::vector<char> scored(cands.size(), 0);
+      for (size_t i : idx) scored[i] = 1;
       std::map<long long, std::vector<size_t>> by_macs;
-      for (size_t i : idx)
+      for (size_t i = 0; i < cands.size(); ++i)
         if (cands[i].status == CandidateStatus::Survivor) by_macs[cands[i].macs].push_back(i);
-      std::vector<size_t> more;
+      std::vector<size_t> more, origin_valued;
       for (auto& kv : by_macs) {
-        auto& g = kv.second;
+        auto g = kv.second;
         if (g.size() < 2) continue;
         std::sort(g.begin(), g.end(), [&](size_t a, size_t b) {
           return cands[a].fisher_total < cands[b].fisher_total;
         });
-        std::vector<char> mark(g.size(), 0);
-        for (size_t j = 1; j < g.size(); ++j) {
+        bool close = false;
+        for (size_t j = 1; j < g.size() && !close; ++j) {
           const double a = cands[g[j - 1]].fisher_total, b = cands[g[j]].fisher_total;
-          if (a != b && near_threshold(a, b, prec)) mark[j - 1] = mark[j] = 1;
+          close = a != b && near_threshold(a, b, prec);
         }
-        for (size_t j = 0; j < g.size(); ++j)
-          if (mark[j] && !simt_scored[g[j]]) more.push_back(g[j]);
+        if (!close) continue;
+        for (size_t i : g) {
+          if (scored[i] && !simt_scored[i]) more.push_back(i);
+          if (!scored[i]) origin_valued.push_back(i);
+        }
       }
       if (!more.empty()) {
         std::sort(more.begin(), more.end());
@@ -1004,6 +1033,10 @@ inline GpuStats evaluate_all_gpu(std::vector<nestopt::Candidate>& cands,
           simt_scored[more[j]] = 1;
         }
         st.rank_rechecked = int64_t(more.size());
+      }
+      if (!origin_valued.empty()) {
+        const double o = origin_simt();
+        for (size_t i : origin_valued) cands[i].fisher_total = o;
       }
     }
   }

@@ -143,8 +143,9 @@ nlohmann::json legality_json(const nestopt::LoopNest& orig, const nestopt::LoopN
   nlohmann::json out;
   const auto t0 = std::chrono::steady_clock::now();
   try {
-    nestopt::LegalityResult r = ctx ? nb200::check_semantic_legality(*ctx, orig, tr, cap, 0)
+    nestopt::LegalityResult r = ctx ? nb200::check_semantic_legality(*ctx, orig, tr, cap)
                                     : nestopt::check_semantic_legality(orig, tr, cap);
+    out["path"] = ctx ? "gpu" : "host";
     out["verdict"] = r.verdict == nestopt::Verdict::Legal     ? "legal"
                      : r.verdict == nestopt::Verdict::Illegal ? "illegal"
                                                               : "not_applicable";
@@ -191,6 +192,8 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
                   {"deduplicated", st.deduplicated},
                   {"origin_equal", st.origin_equal},
                   {"rechecked", st.rechecked},
+                  {"legality_gpu", st.legality_gpu},
+                  {"legality_host", st.legality_host},
                   {"rank_rechecked", st.rank_rechecked},
                   {"requeued", st.requeued},
                   {"est_flops", st.est_flops},
@@ -268,20 +271,30 @@ int nbi_gate_candidates(const char* cfg_json, int legal_device, char** out_json)
     dummy.total = std::numeric_limits<double>::quiet_NaN();
     std::vector<nestopt::Network> nets(cands.size());
     std::vector<char> pend(cands.size(), 0);
+    nb200::LegalityCounts counts;
     {
       std::atomic<size_t> next{0};
-      const long long gpu_min = nb200::legal_gpu_min();
+      std::exception_ptr err;
+      std::mutex err_mu;
       auto worker = [&]() {
-        std::unique_ptr<nb200::Context> lctx;
-        if (legal_device >= 0 && gpu_min >= 0) lctx = std::make_unique<nb200::Context>(legal_device);
-        for (size_t i; (i = next.fetch_add(1)) < cands.size();)
-          pend[i] = nb200::host_gates(cands[i], origin, cfg, dummy, nets[i], lctx.get(), gpu_min)
-                        ? 1 : 0;
+        try {
+          std::unique_ptr<nb200::Context> lctx;
+          if (legal_device >= 0) lctx = std::make_unique<nb200::Context>(legal_device);
+          for (size_t i; (i = next.fetch_add(1)) < cands.size();)
+            pend[i] =
+                nb200::host_gates(cands[i], origin, cfg, dummy, nets[i], lctx.get(), &counts) ? 1
+                                                                                               : 0;
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (!err) err = std::current_exception();
+          next = cands.size();
+        }
       };
       std::vector<std::thread> pool;
       const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
       for (unsigned t = 0; t < nt; ++t) pool.emplace_back(worker);
       for (auto& t : pool) t.join();
+      if (err) std::rethrow_exception(err);
     }
     nlohmann::json arr = nlohmann::json::array();
     for (size_t i = 0; i < cands.size(); ++i) {
@@ -295,7 +308,10 @@ int nbi_gate_candidates(const char* cfg_json, int legal_device, char** out_json)
       if (pending) cj["network"] = nestopt::network_to_json(net);
       arr.push_back(std::move(cj));
     }
-    *out_json = dup(nlohmann::json{{"candidates", arr}}.dump());
+    *out_json = dup(nlohmann::json{{"candidates", arr},
+                                   {"legality", {{"gpu", counts.gpu.load()},
+                                                 {"host", counts.host.load()}}}}
+                        .dump());
     return 0;
   } catch (const nestopt::ConfigError& e) {
     g_err = e.what();

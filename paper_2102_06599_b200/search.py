@@ -78,21 +78,23 @@ def near_threshold(cand: float, origin: float, precision: int) -> bool:
     return bool(load().nbi_near_threshold(cand, origin, int(precision)))
 
 
-def gate_candidates(cfg: dict, legal_device: int = -1) -> list:
+def gate_candidates(cfg: dict, legal_device: int = -1, with_counts: bool = False):
     """The host half of a search: the reference's draw_candidates and
     evaluate_candidate's gates (I/search.hpp:187-293).  legal_device >= 0
     checks semantic runs on that GPU (nb_semantic_legality), -1 (no GPU
     needed) with the reference's host check.  Returns one dict per
     candidate: status ("fisher" = a neural candidate that needs a Fisher
     score, else the reference's final status), reason, macs, and the
-    repaired network JSON of "fisher" candidates."""
+    repaired network JSON of "fisher" candidates.  with_counts: also return
+    {"gpu": n, "host": m}, the semantic runs each side checked."""
     lib = load()
     p = C.c_void_p()
     rc = lib.nbi_gate_candidates(json.dumps(cfg).encode(), int(legal_device), C.byref(p))
     if rc != 0:
         raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
     try:
-        return json.loads(C.cast(p, C.c_char_p).value.decode())["candidates"]
+        out = json.loads(C.cast(p, C.c_char_p).value.decode())
+        return (out["candidates"], out["legality"]) if with_counts else out["candidates"]
     finally:
         lib.nbi_free(p)
 
@@ -100,8 +102,9 @@ def gate_candidates(cfg: dict, legal_device: int = -1) -> list:
 def legality(spec, seq: str, pre: str = "", cap: int = 1_000_000, device: int = -1):
     """check_semantic_legality (I/transforms.hpp:598-663) of the semantic run
     `seq` applied to conv_nest(spec) rewritten by `pre`: device -1 = the
-    reference's host function, else the GPU check on that device.  Returns
-    ({"verdict", "reason"} or {"error": "CapExceeded", "what"}, elapsed ms)."""
+    reference's host function, else the GPU check on that device (no host
+    fallback).  Returns ({"verdict", "reason", "path": "gpu"|"host"} or
+    {"error": "CapExceeded", "what"}, elapsed ms)."""
     lib = load()
     p = C.c_void_p()
     ms = C.c_double()

@@ -30,6 +30,7 @@ def _ids(cases):
 def test_host_check_reproduces_golden(case):
     """The fixtures are the reference's own verdicts (nest JSON round trip)."""
     res, _ = S.legality_nests(case["original"], case["transformed"], case["cap"], device=-1)
+    assert res.pop("path", "host") == "host"
     assert res == case["expected"]
 
 
@@ -48,6 +49,8 @@ def test_fixture_coverage():
 @pytest.mark.parametrize("case", CASES, ids=_ids(CASES))
 def test_gpu_legality_matches_reference(case):
     res, ms = S.legality_nests(case["original"], case["transformed"], case["cap"], device=0)
+    if "error" not in res:  # (CapExceeded is decided from instance counts first)
+        assert res.pop("path") == "gpu", res  # answered by the device, no host fallback
     assert res == case["expected"], (res, case["expected"])
     if case["name"].startswith("big_") and "error" not in res:
         print(f'{case["name"]}: gpu {ms:.1f} ms vs reference host {case["host_ms"]:.0f} ms')
@@ -70,22 +73,25 @@ def test_gpu_legality_through_dsl():
     for spec, pre, seq in cases:
         host, _ = S.legality(spec, seq, pre=pre, device=-1)
         gpu, _ = S.legality(spec, seq, pre=pre, device=0)
+        assert host.pop("path") == "host" and gpu.pop("path") == "gpu"
         assert gpu == host, (spec, pre, seq)
 
 
 @NEEDS_LIB
 @pytest.mark.gpu
-def test_gates_with_gpu_legality_match_host(monkeypatch):
+def test_gates_with_gpu_legality_match_host():
     """evaluate_candidate's gates with every semantic run checked on the GPU
+    (no host fallback, whatever the nest size: the path counters prove it)
     give the same statuses, reasons and MACs as with the reference's host
     check, on the all-kinds toy search (the reference's default kinds)."""
-    monkeypatch.setenv("NB_LEGAL_GPU_MIN", "0")
     g = golden("search_toy_1000.json")
     cfg = dict(g["config"])
     cfg.pop("kinds", None)  # reference default: all seven kinds
     cfg["candidate_count"] = 300
-    host = S.gate_candidates(cfg, legal_device=-1)
-    gpu = S.gate_candidates(cfg, legal_device=0)
+    host, hc = S.gate_candidates(cfg, legal_device=-1, with_counts=True)
+    gpu, gc = S.gate_candidates(cfg, legal_device=0, with_counts=True)
+    assert hc["gpu"] == 0 and hc["host"] > 0
+    assert gc["host"] == 0 and gc["gpu"] == hc["host"], gc
     assert [(c["status"], c.get("reason"), c["macs"]) for c in gpu] == \
            [(c["status"], c.get("reason"), c["macs"]) for c in host]
     assert any("reordered" in (c.get("reason") or "") or "duplicates" in (c.get("reason") or "")

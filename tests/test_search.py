@@ -127,6 +127,8 @@ def test_search_toy_1000_decisions_match_reference():
     assert rep["survivors_ranked"] == g["survivors_ranked"]
     assert rep["survivors_ranked"][0] == 103
     assert rep["gpu"]["deduplicated"] > 0
+    # every semantic run of the all-kinds gates was checked on the GPU
+    assert rep["gpu"]["legality_gpu"] > 0 and rep["gpu"]["legality_host"] == 0
 
 
 @pytest.mark.gpu
