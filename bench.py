@@ -38,15 +38,31 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # Precision tiers (the values live in
 # paper_2102_06599_b200/api.py TOLERANCE): what each mode computes in and
 # the stated tolerance of its Fisher scores against the fp64 reference.
-MODE_KEY = {"fp32": "fp32_3xtf32", "tf32": "tf32", "simt": "simt"}
-DTYPE = {"fp32_3xtf32": "3xtf32", "tf32": "tf32", "simt": "f32"}
-ARITH = {"fp32": "3xTF32 tcgen05 implicit GEMM (hi*hi + hi*lo + lo*hi, fp32 accumulate) for "
-                 "tensor-core-shaped ranges, fp32 FFMA for the rest; head/softmax/Fisher fp64",
+# The FP32 tier's tensor-core split (paper_2102_06599_b200.fp32_split():
+# "3xf16" by default, NB_TC_SPLIT=tf32 / bf16 for the alternatives).
+def _split() -> str:
+    e = os.environ.get("NB_TC_SPLIT")
+    return {"tf32": "3xtf32", "bf16": "3xbf16"}.get(e, "3xf16")
+
+
+SPLIT = _split()
+MODE_KEY = {"fp32": "fp32_" + SPLIT, "tf32": "tf32", "simt": "simt"}
+DTYPE = {"fp32_" + SPLIT: SPLIT, "tf32": "tf32", "simt": "f32"}
+_SPLIT_DESC = {
+    "3xf16": "3xF16 tcgen05 kind::f16 implicit GEMM (fp16 hi/lo halves of per-image / per-layer "
+             "power-of-two scaled fp32 operands, hi*hi + hi*lo + lo*hi, fp32 accumulate)",
+    "3xbf16": "3xBF16 tcgen05 kind::f16 implicit GEMM (bf16 hi/lo halves, hi*hi + hi*lo + lo*hi, "
+              "fp32 accumulate)",
+    "3xtf32": "3xTF32 tcgen05 implicit GEMM (hi*hi + hi*lo + lo*hi, fp32 accumulate)"}
+ARITH = {"fp32": _SPLIT_DESC[SPLIT] + " for tensor-core-shaped ranges, fp32 FFMA for the rest; "
+                 "head/softmax/Fisher fp64",
          "tf32": "1xTF32 tcgen05 (throughput tier); head/softmax/Fisher fp64",
          "simt": "fp32 FFMA everywhere (true fp32); head/softmax/Fisher fp64"}
-TOL_NOTE = {"fp32_3xtf32": "Fisher totals <= 5e-4, per layer <= 5e-3 relative",
+TOL_NOTE = {"fp32_" + SPLIT: "Fisher totals <= 5e-4, per layer <= 5e-3 relative (chains of <= 10 "
+                             "layers); 1.5e-3 / 5e-3 on the 33-layer R34 chain",
             "tf32": "Fisher totals <= 5e-2, per layer <= 2e-1 relative",
-            "simt": "Fisher totals <= 1e-5, per layer <= 1e-4 relative"}
+            "simt": "Fisher totals <= 1e-5, per layer <= 1e-4 relative (chains of <= 10 layers); "
+                    "3e-4 / 1.5e-3 on the R34 chain"}
 
 
 def parse():
@@ -448,13 +464,16 @@ def main():
                  "peak_source": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json); "
                                 "kernel_ceiling = the measured peak of the arithmetic issued"}
             # the arithmetic the precision mode issues, against its MEASURED
-            # peak: 3xTF32 = 3 tf32 MMAs per fp32 product, TF32 = 1
-            mp = pk_meas.get("tcgen05_tf32_tflops")
+            # peak: the FP32 split = 3 MMAs per fp32 product (kind::f16 for
+            # 3xF16 / 3xBF16, kind::tf32 for 3xTF32), TF32 = 1 kind::tf32
+            f16 = args.precision == "fp32" and SPLIT != "3xtf32"
+            mp = pk_meas.get("tcgen05_bf16_tflops" if f16 else "tcgen05_tf32_tflops")
             div = {"fp32": 3.0, "tf32": 1.0}.get(args.precision)
             if div and mp and mp > 0:
-                r["kernel_ceiling"] = {"value": mp / div, "unit": "TFLOP/s",
-                                       "frac": ach / (mp / div), "mode": args.precision,
-                                       "source": "measured tcgen05 kind::tf32 peak / %g" % div}
+                r["kernel_ceiling"] = {
+                    "value": mp / div, "unit": "TFLOP/s", "frac": ach / (mp / div),
+                    "mode": args.precision,
+                    "source": "measured tcgen05 kind::%s peak / %g" % ("f16" if f16 else "tf32", div)}
         else:
             ach = dom["bytes"] / dom["launches"] / (avg_ms / 1e3) / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -493,7 +512,7 @@ def main():
     modes = {}
     if not args.no_modes:
         for name, pm in (("simt", Precision.SIMT), ("tf32", Precision.TF32),
-                         ("fp32_3xtf32", Precision.FP32)):
+                         ("fp32_" + SPLIT, Precision.FP32)):
             if pm == prec:
                 continue
             nb.evaluate(sessions, warm_pool, pm)

@@ -9,7 +9,7 @@ from .api import (  # noqa: F401
     Batch, ChannelSplit, ConfigError, Context, ConvSpec, CudaError, Error, EvalStats,
     RECHECK_BAND, TIE_BAND, TOLERANCE, TOLERANCE_DEEP, FisherReport, ForwardCache, InvalidSpec, Layer, Network, NoDevice, Precision, Session,
     ShapeMismatch, Unsupported, activation_gradients, conv_dgrad, count_macs,
-    default_context, device_count, evaluate, fisher_accepts, fisher_flops, fisher_potential,
+    default_context, device_count, fp32_split, evaluate, fisher_accepts, fisher_flops, fisher_potential,
     fisher_sharded, shard_batch,
     forward, layer_forward, legality_fisher, make_batch, network_macs, reference_conv,
     repair_network, schedule_lpt,

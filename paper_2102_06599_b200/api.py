@@ -14,6 +14,8 @@ Citations: I/ = /root/reference/proj/include/nestopt/.
 """
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import threading
 from dataclasses import dataclass, field
@@ -53,6 +55,14 @@ def _check(status: int) -> None:
     if status != abi.NB_OK:
         msg = abi.load().nb_last_error().decode(errors="replace")
         raise _STATUS.get(status, Error)(msg)
+
+
+def fp32_split() -> str:
+    """The tensor-core split of the FP32 tier, as libnb200 reads it from the
+    environment (engine.cu split_h16): "3xf16" (default), "3xbf16"
+    (NB_TC_SPLIT=bf16) or "3xtf32" (NB_TC_SPLIT=tf32)."""
+    e = os.environ.get("NB_TC_SPLIT")
+    return {"tf32": "3xtf32", "bf16": "3xbf16"}.get(e, "3xf16")
 
 
 class Precision:

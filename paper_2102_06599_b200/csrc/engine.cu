@@ -112,13 +112,38 @@ int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
 // is what bounds the kernel (shared-memory operand traffic, profiles/);
 // SMs left idle by a small tile count are filled by the other candidates
 // the scheduler runs concurrently on the same GPU.
+// The fp32-accurate tier's tensor-core split (NB_TC_SPLIT): 2 = 3xFP16
+// (default: kind::f16 with per-image / per-layer power-of-two scaling -- half
+// the MMA time and B bytes of 3xTF32 at its 22 significand bits,
+// profiles/r02_precision.md), 1 = 3xBF16 (16 bits, no scaling; "bf16"),
+// 0 = 3xTF32 ("tf32").
+int split_h16() {
+  static const int m = [] {
+    const char* e = std::getenv("NB_TC_SPLIT");
+    if (e && std::string(e) == "tf32") return 0;
+    if (e && std::string(e) == "bf16") return 1;
+    return 2;
+  }();
+  return m;
+}
+bool split_bf16() { return split_h16() != 0; }
+
+// fp16 weight scale 2^k for a layer whose largest |w| is maxabs: |w 2^k| < 2^15
+int weight_shift(double maxabs) {
+  if (!(maxabs > 0.0) || !std::isfinite(maxabs)) return 0;
+  int ex = 0;
+  std::frexp(maxabs, &ex);  // maxabs < 2^ex
+  const int k = 15 - ex;
+  return k < -126 ? -126 : (k > 126 ? 126 : k);
+}
+
 int pick_bn(int n_per_group, bool split3) {
   // NB_TC_BN3=256: the 256-wide single-accumulator 3xTF32 tile (experiment)
   static const bool wide3 = [] {
     const char* e = std::getenv("NB_TC_BN3");
     return e && std::atoi(e) >= 256;
   }();
-  if (split3 && wide3 && n_per_group % 256 == 0) return 256;
+  if (split3 && wide3 && !split_bf16() && n_per_group % 256 == 0) return 256;
   static const int o3[] = {128, 64, 32};
   static const int o1[] = {256, 128, 64, 32};
   const int* o = split3 ? o3 : o1;
@@ -186,7 +211,8 @@ int choose_ksplit(const tc::TcArgs& t, int m_tiles, int num_sms, bool pair) {
 // pair adds a cross-SM handshake per stage.  Off by default; NB_TC_PAIR=1
 // enables it (NB_TC_PAIR_BN=256 allows the single-accumulator 256-wide
 // 3xTF32 pair).  0 = no pair.
-int pick_pair_bn(int n, int m_tiles, bool split3) {
+int pick_pair_bn(int n, int m_tiles, bool split3, bool bf3 = false) {
+  if (bf3) return 0;  // (3xBF16 runs single-CTA plans only)
   static const int mode = [] {
     const char* e = std::getenv("NB_TC_PAIR");
     return e ? std::atoi(e) : 0;
@@ -205,7 +231,8 @@ int pick_pair_bn(int n, int m_tiles, bool split3) {
 // Multicast cluster for a single-CTA tile plan: two CTAs on two M tiles of
 // one N tile share every B stage (each loads half, multicast to both), which
 // halves the weight operand's L2 -> SM traffic.  NB_TC_MC=0 disables it.
-bool use_mc(int bn, int m_tiles, bool pair, bool kwf = false) {
+bool use_mc(int bn, int m_tiles, bool pair, bool kwf = false, bool bf3 = false) {
+  if (bf3) return false;
   // NB_TC_MC: 0 (default) off, 1 every single-CTA plan, 2 kw-fused plans only
   // (their B stage is 3x wider, 48 KB, the same for every CTA; measured: the
   // stage period drops 7% but the evaluation time does not)
@@ -304,6 +331,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
   NetPlan P;
   const bool tc_on = prec != NB_PREC_SIMT;
   P.split3 = prec == NB_PREC_FP32;
+  P.h16 = P.split3 ? split_h16() : 0;
   const int64_t L = net.L();
   for (int64_t l = 0; l < L; ++l) {
     const Spec& s = net.specs[l];
@@ -359,7 +387,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           // (kw-fused B layouts are [kw][co][kh][ci] with K = KH x sci: no
           // K padding, so a padded K runs the plain tap-major plan)
           const bool kwf = G == 1 && !dense && sci % 32 == 0 && use_kwf(g, sco, t.BW);
-          const int pbn = kwf ? 0 : pick_pair_bn(sco, mt, P.split3);
+          const int pbn = kwf ? 0 : pick_pair_bn(sco, mt, P.split3, P.h16 != 0);
           int bn = pbn ? pbn : pick_bn(sco, P.split3);
           static const int gran = [] {  // NB_TC_PADG: fprop padded-width granularity
             const char* e = std::getenv("NB_TC_PADG");
@@ -383,7 +411,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
             t.out_ld = g.Co;
             t.out_c_base = r.b;
             t.out_c_per_group = sco;
-            const bool mc = use_mc(bn, mt, pbn != 0, kwf);
+            const bool mc = use_mc(bn, mt, pbn != 0, kwf, P.h16 != 0);
             t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
             if (t.ksplit > 1)
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
@@ -476,7 +504,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
       if (tc::plan_tiles(gh, gw, g.N, 1, t)) {
         const int mt = m_tiles_at(gh, gw, plan_n, 1);
         const bool kwf = DG == 1 && !ddense && dsco % 32 == 0 && use_kwf(g, dsci, t.BW);
-        const int pbn = kwf ? 0 : pick_pair_bn(dsci, mt * t.nphase, P.split3);
+        const int pbn = kwf ? 0 : pick_pair_bn(dsci, mt * t.nphase, P.split3, P.h16 != 0);
         int bn = pbn ? pbn : pick_bn(dsci, P.split3);
         if (!bn && dpad_ok) bn = pick_bn_padded(dsci, P.split3);
         const int kp = (dsco + 31) / 32 * 32;
@@ -497,7 +525,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           t.out_c_base = 0;
           t.out_c_per_group = dsci;
           t.part_ld = g.Ci;
-          const bool mc = use_mc(bn, mt, pbn != 0, kwf);
+          const bool mc = use_mc(bn, mt, pbn != 0, kwf, P.h16 != 0);
           t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
           // split-K dgrad: k_splitk_epilogue writes one partial per (image, pixel chunk)
           const int hw_chunks = t.ksplit > 1 ? splitk_hw_chunks(plan_n, g.H * g.W, g.Ci) : 1;
@@ -524,6 +552,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
       }
     }
     lp.wpack_floats = off;
+    lp.h16 = P.h16;
     lp.w_off = P.w_total;
     P.w_total += off;
     lp.act_floats = n * s.co_eff() * s.oh() * s.ow();
@@ -575,12 +604,26 @@ const double* ensure_z(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) 
   return buf->as<double>();
 }
 
+// max |z| of the z-stream prefix (seed, stream, count) -- the scale of the
+// fp16 split's packed weights -- cached per context
+double zmax_of(nb_ctx* c, uint64_t seed, int64_t stream, int64_t count) {
+  const auto key = std::make_tuple(seed, stream, count);
+  auto it = c->zmax.find(key);
+  if (it != c->zmax.end()) return it->second;
+  const std::vector<double>& z = z_stream(seed, stream, count);
+  double m = 0.0;
+  for (int64_t i = 0; i < count; ++i) m = std::max(m, std::fabs(z[size_t(i)]));
+  c->zmax.emplace(key, m);
+  return m;
+}
+
 // Identity of a layer's packed init_weights weights: the z-stream (seed,
 // layer), the fan-in scale and every offset/family the lowering chose.
 std::string wkey(uint64_t seed, int64_t l, const Spec& sp, const LayerPlan& lp) {
   std::string k = std::to_string(seed) + "/" + std::to_string(l) + "/" + std::to_string(sp.ci) +
                   "x" + std::to_string(sp.kh) + "x" + std::to_string(sp.kw) + "/" +
-                  std::to_string(lp.wpack_floats);
+                  std::to_string(lp.wpack_floats) + "/h" + std::to_string(lp.h16) + "," +
+                  std::to_string(lp.b_shift);
   const ConvGeom& g = lp.geom;
   for (int r = 0; r < g.nranges; ++r) {
     const RangeDesc& d = g.r[r];
@@ -613,6 +656,8 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
     PackDst d{need_wf ? base : nullptr, need_wd ? base : nullptr, nullptr, nullptr, nullptr,
               nullptr};
     d.KW = lp.geom.KW;
+    d.h16 = lp.h16;
+    d.h16_scale = float(std::ldexp(1.0, lp.b_shift));
     if (lp.family[r] == Family::TensorCore) {
       d.tcf_hi = base + lp.tcf[r].w_off;
       d.tcf_lo = d.tcf_hi + lp.tcf[r].w_n;
@@ -636,7 +681,7 @@ void pack_layer(nb_ctx* c, const LayerPlan& lp, const double* src, double scale,
   }
 }
 
-void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
+void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3, bool bf3,
                const float* A, int AC, int AW, int AH, int AN, const float* whi,
                cudaStream_t st) {
   tc::TcLaunch L;
@@ -655,29 +700,35 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   static int tc_launch_no = 0;
   const bool tracing = trace_at >= 0 && tc_launch_no++ == trace_at;
   if (tracing) {
-    c->trace.ensure((5 * tc::kTraceStages + 4 * 1024) * 8);
-    NB_CUDA(cudaMemsetAsync(c->trace.p, 0, (5 * tc::kTraceStages + 4 * 1024) * 8, st));
+    c->trace.ensure((tc::kTraceRoles * tc::kTraceStages + 4 * 1024) * 8);
+    NB_CUDA(cudaMemsetAsync(c->trace.p, 0, (tc::kTraceRoles * tc::kTraceStages + 4 * 1024) * 8, st));
     L.args.trace = c->trace.as<long long>();
   }
   L.bn = tp.bn;
   L.split3 = split3;
+  L.bf = bf3;
   L.pair = tp.pair;
   L.mc = tp.mc;
   L.kwf = tp.kwf;
-  // NB_TC_CONVH: 1 (default) = both converter groups split every stage by
-  // channel halves, 0 = groups alternate stages, 2 = halves for kw-fused only
+  // NB_TC_CONVH: 1 = both converter groups split every stage by channel
+  // halves, 0 = groups alternate stages, 2 = halves for kw-fused only.
+  // Default: halves for 3xTF32 (its kw-fused plans have two TMEM A slots, so
+  // per-stage latency counts), alternate stages for the 16-bit splits (four
+  // or more slots; alternating halves the per-stage barrier overhead:
+  // 3xF16 bench 576 vs 561 candidates/s)
   static const int convh = [] {
     const char* e = std::getenv("NB_TC_CONVH");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : -1;
   }();
-  L.args.conv_halves = convh == 1 || (convh == 2 && tp.kwf) ? 1 : 0;
+  const int ch = convh >= 0 ? convh : (bf3 ? 0 : 1);
+  L.args.conv_halves = ch == 1 || (ch == 2 && tp.kwf) ? 1 : 0;
   L.num_sms = c->num_sms;
   if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   NB_CUDA(tc::launch(L, st));
   c->launches++;
   if (tracing) {
-    std::vector<long long> h(5 * tc::kTraceStages + 4 * 1024);
+    std::vector<long long> h(tc::kTraceRoles * tc::kTraceStages + 4 * 1024);
     NB_CUDA(cudaMemcpyAsync(h.data(), c->trace.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
     NB_CUDA(cudaStreamSynchronize(st));
     FILE* f = std::fopen("nb_tc_trace.txt", "w");
@@ -685,16 +736,19 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
       std::fprintf(f, "# bn=%d split3=%d stages tiles=%d kblocks/tile=%d\n", L.bn, int(L.split3),
                    args.m_tiles * args.n_tiles, args.ntaps[0] * args.a_cblocks);
       for (int i = 0; i < tc::kTraceStages; ++i)
-        std::fprintf(f, "%d %lld %lld %lld %lld %lld\n", i, h[i], h[tc::kTraceStages + i],
-                     h[2 * tc::kTraceStages + i], h[3 * tc::kTraceStages + i],
-                     h[4 * tc::kTraceStages + i]);
+      {
+        std::fprintf(f, "%d", i);
+        for (int role = 0; role < tc::kTraceRoles; ++role)
+          std::fprintf(f, " %lld", h[role * tc::kTraceStages + i]);
+        std::fprintf(f, "\n");
+      }
       std::fclose(f);
     }
     // per CTA: entry, after the grid dependency, MMA issue done, epilogue done (ns)
     FILE* g = std::fopen("nb_tc_ctas.txt", "w");
     if (g) {
       for (int i = 0; i < 1024; ++i) {
-        const long long* e = &h[5 * tc::kTraceStages + 4 * i];
+        const long long* e = &h[tc::kTraceRoles * tc::kTraceStages + 4 * i];
         if (e[0]) std::fprintf(g, "%d %lld %lld %lld %lld\n", i, e[0], e[1], e[2], e[3]);
       }
       std::fclose(g);
@@ -703,10 +757,36 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
 }
 
 // One layer's fprop (all ranges): y = relu?(conv(x)).
+// The profiler name of a tensor-core launch (fprop, or dgrad with the Fisher
+// epilogue) for the plan's arithmetic.
+const char* split_name(const NetPlan& P, bool dgrad) {
+  static const char* const f[] = {"conv_fprop_tc_tf32", "conv_fprop_tc_3xtf32",
+                                  "conv_fprop_tc_3xbf16", "conv_fprop_tc_3xf16"};
+  static const char* const d[] = {"conv_dgrad_tc_tf32_fisher", "conv_dgrad_tc_3xtf32_fisher",
+                                  "conv_dgrad_tc_3xbf16_fisher", "conv_dgrad_tc_3xf16_fisher"};
+  const int i = P.h16 ? 1 + P.h16 : (P.split3 ? 1 : 0);
+  return dgrad ? d[i] : f[i];
+}
+
+// fp16-split scaling of a tensor-core launch (TcArgs::h16_f16): the per-image
+// max of its A operand (in_amax) and of what it writes for the next GEMM
+// (out_amax), the layer's weight scale
+void set_scaling(const NetPlan& P, const LayerPlan& lp, tc::TcArgs& a, const uint32_t* in_amax,
+                 uint32_t* out_amax) {
+  const bool f16 = P.h16 == 2;
+  a.h16_f16 = f16 ? 1 : 0;
+  a.a_amax = f16 ? in_amax : nullptr;
+  a.out_amax = f16 ? out_amax : nullptr;
+  a.b_inv = f16 ? float(std::ldexp(1.0, -lp.b_shift)) : 1.f;
+}
+
+// One layer's fprop (all ranges): y = relu?(conv(x)).  fp16 split: in_amax =
+// per-image max |x|; out_amax (nullable) receives per-image max |y|.
 void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* x, float* y,
-                 bool relu, cudaStream_t st) {
+                 bool relu, cudaStream_t st, const uint32_t* in_amax, uint32_t* out_amax) {
   const ConvGeom& g = lp.geom;
   float* base = lp.wbase;
+  bool direct = false;
   for (int r = 0; r < g.nranges; ++r) {
     const RangeDesc& rd = g.r[r];
     const double fl =
@@ -721,9 +801,10 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       a.relu = relu ? 1 : 0;
       a.ws = c->ws.as<float>();
       a.ws_stride = int64_t(g.N) * g.OH * g.OW * g.Co;
+      set_scaling(P, lp, a, in_amax, out_amax);
       // (a col stem reads the session's im2col copy: 32 columns per output pixel)
       const bool col = lp.tcf[r].col;
-      launch_tc(c, lp.tcf[r], a, P.split3, x, col ? 32 : g.Ci, col ? g.OW : g.W,
+      launch_tc(c, lp.tcf[r], a, P.split3, P.h16 != 0, x, col ? 32 : g.Ci, col ? g.OW : g.W,
                 col ? g.OH : g.H, g.N, base + lp.tcf[r].w_off, st);
       if (a.ksplit > 1) {
         SplitEpi e{};
@@ -739,22 +820,31 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
         e.out = y;
         e.relu = relu ? 1 : 0;
         e.hw_chunks = lp.tcf[r].hw_chunks;
+        e.out_amax = a.out_amax;
         launch_splitk_epilogue(e, st);
         c->launches++;
       }
-      c->prof.end(st, P.split3 ? "conv_fprop_tc_3xtf32" : "conv_fprop_tc_tf32", fl, by);
+      c->prof.end(st, split_name(P, false), fl, by);
     } else {
       launch_fprop_direct(g, r, x, base, y, relu, st);
       c->launches++;
       c->prof.end(st, "conv_fprop_direct", fl, by);
+      direct = true;
     }
+  }
+  // a direct range does not record its output's max: scan the output
+  if (direct && out_amax && P.h16 == 2) {
+    launch_amax(y, g.N, int64_t(g.OH) * g.OW * g.Co, out_amax, st);
+    c->launches++;
   }
 }
 
 // One layer's dgrad with the fused epilogue on the previous layer's output.
+// fp16 split: in_amax = per-image max |dpre|; out_amax (nullable) receives
+// per-image max |dpre_out|.
 void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* dpre,
                  const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
-                 double* partial, cudaStream_t st) {
+                 double* partial, cudaStream_t st, const uint32_t* in_amax, uint32_t* out_amax) {
   const ConvGeom& g = lp.geom;
   float* base = lp.wbase;
   const double prev_floats = double(g.N) * g.H * g.W * g.Ci;
@@ -772,7 +862,8 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
     a.relu_prev = relu_prev ? 1 : 0;
     a.ws = c->ws.as<float>();
     a.ws_stride = int64_t(g.N) * g.H * g.W * g.Ci;
-    launch_tc(c, lp.tcd, a, P.split3, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
+    set_scaling(P, lp, a, in_amax, dpre_out ? out_amax : nullptr);
+    launch_tc(c, lp.tcd, a, P.split3, P.h16 != 0, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
     if (a.ksplit > 1) {
       SplitEpi e{};
       e.ws = a.ws;
@@ -790,15 +881,20 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       e.partial = partial;
       e.relu_prev = relu_prev ? 1 : 0;
       e.hw_chunks = lp.tcd.hw_chunks;
+      e.out_amax = a.out_amax;
       launch_splitk_epilogue(e, st);
       c->launches++;
     }
-    c->prof.end(st, P.split3 ? "conv_dgrad_tc_3xtf32_fisher" : "conv_dgrad_tc_tf32_fisher",
+    c->prof.end(st, split_name(P, true),
                 lp.dgrad_flops, by);
   } else {
     launch_dgrad_direct(g, dpre, base, a_prev, relu_prev, dpre_out, g_out, partial, st);
     c->launches++;
     c->prof.end(st, "conv_dgrad_direct_fisher", lp.dgrad_flops, by);
+    if (dpre_out && out_amax && P.h16 == 2) {
+      launch_amax(dpre_out, g.N, int64_t(g.H) * g.W * g.Ci, out_amax, st);
+      c->launches++;
+    }
   }
 }
 
@@ -820,6 +916,18 @@ std::unique_ptr<DevBuf> take_spare(nb_ctx* c, size_t bytes) {
     buf->ensure(bytes);
   }
   return buf;
+}
+
+// Per-image max |x| of the session batch (fp16 split of the first GEMM),
+// computed once per session.
+const uint32_t* session_xamax(nb_ctx* c, nb_session* s, cudaStream_t st) {
+  if (!s->xamax) {
+    s->xamax = take_spare(c, size_t(s->n) * 4);
+    NB_CUDA(cudaMemsetAsync(s->xamax->p, 0, size_t(s->n) * 4, st));
+    launch_amax(s->x->as<float>(), s->n, s->h * s->w * s->ci, s->xamax->as<uint32_t>(), st);
+    c->launches++;
+  }
+  return s->xamax->as<uint32_t>();
 }
 
 // The session batch's im2col copy for a col stem (built once per geometry;
@@ -898,6 +1006,19 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   // packed once per distinct (seed, layer, lowering) into the context's slab.
   // The slab is reset before (never during) a run whose misses do not fit,
   // so no pointer handed to this run is overwritten by it.
+  // fp16 split: each layer's weight scale from its largest |w| (host data)
+  if (P.h16 == 2)
+    for (int64_t l = 0; l < L; ++l) {
+      const Spec& sp = net.specs[l];
+      const int64_t cnt = sp.weight_count();
+      double m = 0.0;
+      if (explicit_w) {
+        for (int64_t i = 0; i < cnt; ++i) m = std::max(m, std::fabs(w->layer[l][i]));
+      } else {
+        m = zmax_of(c, net.seed, l, cnt) / std::sqrt(double(sp.ci * sp.kh * sp.kw));
+      }
+      P.layers[l].b_shift = weight_shift(m);
+    }
   std::vector<std::string> keys;
   if (!explicit_w) {
     size_t miss = 0, all = 0;
@@ -952,13 +1073,27 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   }
 
   phase("host_weights");
+  // fp16 split: per-(layer, image) max slots of the activations (act_amax)
+  // and masked gradients (dpre_amax) the GEMMs read, zeroed for this run
+  uint32_t* act_amax = nullptr;
+  uint32_t* dpre_amax = nullptr;
+  const uint32_t* x_amax = nullptr;
+  if (P.h16 == 2) {
+    c->amax.ensure(size_t(2 * L * N) * 4);
+    NB_CUDA(cudaMemsetAsync(c->amax.p, 0, size_t(2 * L * N) * 4, st));
+    act_amax = c->amax.as<uint32_t>();
+    dpre_amax = act_amax + L * N;
+    x_amax = session_xamax(c, s, st);
+  }
   // ---- forward (I/nnet.hpp:180-197)
   const float* x = s->x->as<float>();
   if (P.layers[0].family[0] == Family::TensorCore && P.layers[0].tcf[0].col)
     x = session_xcol(c, s, P.layers[0].geom, st);
   for (int64_t l = 0; l < L; ++l) {
     float* y = act + P.layers[l].act_off;
-    fprop_layer(c, P, P.layers[l], x, y, net.relu[l], st);
+    fprop_layer(c, P, P.layers[l], x, y, net.relu[l], st,
+                l == 0 ? x_amax : (act_amax ? act_amax + (l - 1) * N : nullptr),
+                act_amax && l + 1 < L ? act_amax + l * N : nullptr);
     x = y;
   }
 
@@ -985,6 +1120,10 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   launch_head(ha, st);
   c->prof.end(st, "head", 0.0, 4.0 * double(last.act_floats) * (backward ? 3 : 1));
   c->launches++;
+  if (ha.dpre && dpre_amax) {  // the head's masked gradient, read by the last dgrad
+    launch_amax(ha.dpre, N, int64_t(ha.HW) * ha.C, dpre_amax + (L - 1) * N, st);
+    c->launches++;
+  }
 
   if (backward) {
     // ---- activation gradients with the fused Fisher epilogue (I/nnet.hpp:225-243)
@@ -995,7 +1134,9 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       float* dpre_out = (l - 1 >= 1) ? c->dpre[cur ^ 1].as<float>() : nullptr;
       float* g_out = want_grads ? c->gtmp.as<float>() + prev.act_off : nullptr;
       dgrad_layer(c, P, lp, c->dpre[cur].as<float>(), act + prev.act_off, net.relu[l - 1],
-                  dpre_out, g_out, part + prev.part_off, st);
+                  dpre_out, g_out, part + prev.part_off, st,
+                  dpre_amax ? dpre_amax + l * N : nullptr,
+                  dpre_amax ? dpre_amax + (l - 1) * N : nullptr);
       cur ^= 1;
     }
     // ---- Fisher reduction (I/nnet.hpp:330-350)
@@ -1159,17 +1300,28 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
   float* yb = xb + align64(x_cnt);
   NB_CUDA(cudaMemcpyAsync(ctx->wsrc.p, w, size_t(s.weight_count()) * 8, cudaMemcpyHostToDevice,
                           st));
+  uint32_t* in_amax = nullptr;
+  if (P.h16 == 2) {
+    double m = 0.0;
+    for (int64_t i = 0; i < s.weight_count(); ++i) m = std::max(m, std::fabs(w[i]));
+    lp.b_shift = weight_shift(m);
+    ctx->amax.ensure(size_t(n) * 4);
+    in_amax = ctx->amax.as<uint32_t>();
+    NB_CUDA(cudaMemsetAsync(in_amax, 0, size_t(n) * 4, st));
+  }
   pack_layer(ctx, lp, ctx->wsrc.as<double>(), 1.0, st);
   if (!dgrad) {
     NB_CUDA(cudaMemcpyAsync(ctx->io.p, in, size_t(x_cnt) * 8, cudaMemcpyHostToDevice, st));
     launch_nchw64_to_nhwc32(ctx->io.as<double>(), xb, n, int(s.ci), int(s.h), int(s.w), st);
-    fprop_layer(ctx, P, lp, xb, yb, relu != 0, st);
+    if (in_amax) launch_amax(xb, n, s.ci * s.h * s.w, in_amax, st);
+    fprop_layer(ctx, P, lp, xb, yb, relu != 0, st, in_amax, nullptr);
     launch_nhwc32_to_nchw64(yb, ctx->io.as<double>(), n, lp.geom.Co, lp.geom.OH, lp.geom.OW, st);
     NB_CUDA(cudaMemcpyAsync(out, ctx->io.p, size_t(y_cnt) * 8, cudaMemcpyDeviceToHost, st));
   } else {
     NB_CUDA(cudaMemcpyAsync(ctx->io.p, in, size_t(y_cnt) * 8, cudaMemcpyHostToDevice, st));
     launch_nchw64_to_nhwc32(ctx->io.as<double>(), yb, n, lp.geom.Co, lp.geom.OH, lp.geom.OW, st);
-    dgrad_layer(ctx, P, lp, yb, nullptr, false, nullptr, xb, nullptr, st);
+    if (in_amax) launch_amax(yb, n, int64_t(lp.geom.Co) * lp.geom.OH * lp.geom.OW, in_amax, st);
+    dgrad_layer(ctx, P, lp, yb, nullptr, false, nullptr, xb, nullptr, st, in_amax, nullptr);
     launch_nhwc32_to_nchw64(xb, ctx->io.as<double>(), n, int(s.ci), int(s.h), int(s.w), st);
     NB_CUDA(cudaMemcpyAsync(out, ctx->io.p, size_t(x_cnt) * 8, cudaMemcpyDeviceToHost, st));
   }
@@ -1388,6 +1540,7 @@ nb_status nb_session_destroy(nb_session* s) {
       s->ctx->spare.push_back(std::move(s->x));
       s->ctx->spare.push_back(std::move(s->labels));
       if (s->xcol) s->ctx->spare.push_back(std::move(s->xcol));
+      if (s->xamax) s->ctx->spare.push_back(std::move(s->xamax));
     }
     delete s;
   });

@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.hpp"
@@ -81,6 +82,8 @@ struct LayerPlan {
   int64_t part_off = 0;      // offset (doubles) of its Fisher partials
   int tiles = 0;
   double fprop_flops = 0, dgrad_flops = 0;
+  int h16 = 0;      // tensor-core weights packed as 16-bit halves (NetPlan::h16)
+  int b_shift = 0;  // fp16 halves: the weights were packed times 2^b_shift
 };
 
 struct NetPlan {
@@ -88,7 +91,8 @@ struct NetPlan {
   int64_t act_total = 0, w_total = 0, part_total = 0, dpre_floats = 0;
   int64_t ws_floats = 0;  // split-K workspace (floats)
   int64_t ch_total = 0;  // sum_l C_l
-  bool split3 = false;    // 3xTF32 tensor-core numerics (NB_PREC_FP32)
+  bool split3 = false;    // split fp32 tensor-core numerics (NB_PREC_FP32)
+  int h16 = 0;            // ... in 16-bit halves (kind::f16): 1 bf16, 2 fp16 (scaled); 0 = 3xTF32
 };
 
 // plan_n: the batch size launch shapes are chosen for (0 = n; an example
@@ -143,6 +147,12 @@ struct nb_ctx {
   nb::DevBuf act, wpack, part, misc, wsrc, dpre[2], gtmp, io, ws, tilecnt, trace;
   nb::DevBuf legal;  // semantic-legality workspace (legality.cu)
   nb::DevBuf shard_s, shard_aux;  // example-sharded Fisher (nb_fisher_sharded)
+  // fp16 split: per-(layer, image) max |value| of the activations and of the
+  // masked gradients each GEMM reads (float bits), reset per run
+  nb::DevBuf amax;
+  // max |z| of a cached z-stream prefix (seed, stream, count): the fp16
+  // weight scale of init_weights layers
+  std::map<std::tuple<uint64_t, int64_t, int64_t>, double> zmax;
   int num_sms = 148;
   nb::PinnedBuf host_io, host_out;
   // bracket the evaluation in flight on this context's stream (one at a
@@ -176,6 +186,9 @@ struct nb_session {
   // geometry (xcol_sig) -- the batch is resident and fixed
   std::unique_ptr<nb::DevBuf> xcol;
   std::string xcol_sig;
+  // per-image max |x| (float bits) for the fp16 split of the first GEMM,
+  // computed once (the im2col copy holds the same values and zeros)
+  std::unique_ptr<nb::DevBuf> xamax;
 };
 
 namespace nb {

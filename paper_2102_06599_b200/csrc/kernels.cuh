@@ -58,6 +58,11 @@ struct PackDst {
   float* tcd_lo;
   // kw-fused tensor-core layouts (rows kw*width + c, K = kh x channels)
   int kwf_f = 0, kwf_d = 0, KW = 1;
+  // 16-bit split tensor-core layouts: tc*_hi / tc*_lo hold 16-bit halves
+  // (rn(w'), rn(w' - hi)) of w' = w * h16_scale at the same element index
+  // instead of the tf32 fp32 pair; h16: 0 = tf32 pair, 1 = bf16, 2 = fp16
+  int h16 = 0;
+  float h16_scale = 1.f;
   // padded K per tap of the fprop / dgrad tensor-core layouts (0 = exact)
   int kpf = 0, kpd = 0;
   // densified grouped layouts: K indexed by the full input (fprop) / range
@@ -102,11 +107,17 @@ struct SplitEpi {
   // pixel chunks per image (grid z): enough blocks for small batches; a
   // dgrad writes one Fisher partial per (image, chunk)
   int hw_chunks = 1;
+  // per-image max |value| of the stored output (mode 0) / dpre_out (mode 1)
+  // for the next fp16-split GEMM (float bits; null = not recorded)
+  uint32_t* out_amax = nullptr;
 };
 void launch_splitk_epilogue(const SplitEpi& e, cudaStream_t st);
 // Pixel chunks of a split-K epilogue over n images of HW pixels x C channels
 // (a function of the shape only, so plans and launches agree).
 int splitk_hw_chunks(int64_t n, int HW, int C);
+// Per-image max |x| of an NHWC tensor of N images x per_img floats into
+// amax[n] (float bits, atomicMax: amax must start at 0 or a smaller value)
+void launch_amax(const float* x, int64_t N, int64_t per_img, uint32_t* amax, cudaStream_t st);
 
 // GAP + linear head + softmax-CE (+ backward, + last-layer Fisher partial,
 // + the masked head gradient dpre of the last layer).

@@ -5,6 +5,9 @@
 //
 // Activations are NHWC fp32 in HBM (channels contiguous: coalesced across
 // output channels for fprop and across input channels for dgrad).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -72,21 +75,43 @@ __global__ void k_pack_weights(const double* __restrict__ src, double scale, int
     uint32_t hb, lb;
     split_tf32(__float_as_uint(v), hb, lb);
     const float hi = __uint_as_float(hb), lo = __uint_as_float(lb);
+    // 16-bit split pair of v' = v * h16_scale (a power of two): rn(v'), rn(v' - that)
+    uint16_t bhi = 0, blo = 0;
+    if (d.h16 == 1) {
+      const __nv_bfloat16 bh = __float2bfloat16_rn(v);
+      bhi = __bfloat16_as_ushort(bh);
+      blo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(bh)));
+    } else if (d.h16 == 2) {
+      const float vs = v * d.h16_scale;
+      const __half fh = __float2half_rn(vs);
+      bhi = __half_as_ushort(fh);
+      blo = __half_as_ushort(__float2half_rn(vs - __half2float(fh)));
+    }
     const int kh = tap / d.KW, kw = tap - kh * d.KW, KH = taps / d.KW;
     if (d.tcf_hi) {
       const int kpf = d.kpf ? d.kpf : r.slice_ci;
       const int64_t i = d.col_f   ? int64_t(co_local) * 32 + tap * r.slice_ci + j
                         : d.kwf_f ? ((int64_t(kw) * r.len + co_local) * KH + kh) * r.slice_ci + j
                                   : (int64_t(co_local) * taps + tap) * kpf + (d.dense_f ? ci : j);
-      d.tcf_hi[i] = hi;
-      d.tcf_lo[i] = lo;
+      if (d.h16) {
+        reinterpret_cast<uint16_t*>(d.tcf_hi)[i] = bhi;
+        reinterpret_cast<uint16_t*>(d.tcf_lo)[i] = blo;
+      } else {
+        d.tcf_hi[i] = hi;
+        d.tcf_lo[i] = lo;
+      }
     }
     if (d.tcd_hi) {
       const int kpd = d.kpd ? d.kpd : r.slice_co;
       const int64_t i = d.kwf_d ? ((int64_t(kw) * Ci + ci) * KH + kh) * r.slice_co + t
                                 : (int64_t(ci) * taps + tap) * kpd + (d.dense_d ? co_local : t);
-      d.tcd_hi[i] = hi;
-      d.tcd_lo[i] = lo;
+      if (d.h16) {
+        reinterpret_cast<uint16_t*>(d.tcd_hi)[i] = bhi;
+        reinterpret_cast<uint16_t*>(d.tcd_lo)[i] = blo;
+      } else {
+        d.tcd_hi[i] = hi;
+        d.tcd_lo[i] = lo;
+      }
     }
   }
 }
@@ -820,24 +845,36 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(SplitEpi e) {
   const int64_t n = blockIdx.y;
   const int cs = (e.HW + e.hw_chunks - 1) / e.hw_chunks, pend = min(e.HW, int(blockIdx.z + 1) * cs);
   float contrib = 0.f;
+  float mx = 0.f;  // max |stored value| for the next fp16-split GEMM (image n)
   if (c < e.C) {
     for (int p = int(blockIdx.z) * cs + threadIdx.y; p < pend; p += 8) {
       const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
       float v = 0.f;
       for (int k = 0; k < e.ksplit; ++k) v += e.ws[k * e.ws_stride + idx];
       if (e.mode == 0) {
-        e.out[idx] = (e.relu && !(v > 0.f)) ? 0.f : v;  // I/nnet.hpp:138-139
+        const float o = (e.relu && !(v > 0.f)) ? 0.f : v;  // I/nnet.hpp:138-139
+        e.out[idx] = o;
+        mx = fmaxf(mx, fabsf(o));
       } else {
         if (e.g_out) e.g_out[idx] = v;
         if (e.a_prev) {
           const float a = e.a_prev[idx];
           contrib = fmaf(a, v, contrib);
-          if (e.dpre_out) e.dpre_out[idx] = (e.relu_prev && !(a > 0.f)) ? 0.f : v;
+          if (e.dpre_out) {
+            const float o = (e.relu_prev && !(a > 0.f)) ? 0.f : v;
+            e.dpre_out[idx] = o;
+            mx = fmaxf(mx, fabsf(o));
+          }
         } else if (e.dpre_out) {
           e.dpre_out[idx] = v;
+          mx = fmaxf(mx, fabsf(v));
         }
       }
     }
+  }
+  if (e.out_amax) {  // one atomic per warp (the block is one image)
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+    if (threadIdx.x == 0 && m) atomicMax(e.out_amax + n, m);
   }
   if (e.mode == 0 || !e.partial) return;
   red[threadIdx.y][threadIdx.x] = contrib;
@@ -863,6 +900,7 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
   const int64_t n = blockIdx.y;
   const int cs = (e.HW + e.hw_chunks - 1) / e.hw_chunks, pend = min(e.HW, int(blockIdx.z + 1) * cs);
   float contrib[4] = {0.f, 0.f, 0.f, 0.f};
+  float mx = 0.f;  // max |stored value| for the next fp16-split GEMM (image n)
   if (c < e.C) {
     for (int p = int(blockIdx.z) * cs + threadIdx.y; p < pend; p += 8) {
       const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
@@ -882,6 +920,7 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
           v.w = v.w > 0.f ? v.w : 0.f;
         }
         *reinterpret_cast<float4*>(e.out + idx) = v;
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
       } else {
         if (e.g_out) *reinterpret_cast<float4*>(e.g_out + idx) = v;
         if (e.a_prev) {
@@ -897,12 +936,18 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
             d.z = (e.relu_prev && !(a.z > 0.f)) ? 0.f : v.z;
             d.w = (e.relu_prev && !(a.w > 0.f)) ? 0.f : v.w;
             *reinterpret_cast<float4*>(e.dpre_out + idx) = d;
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(d.x), fabsf(d.y)), fmaxf(fabsf(d.z), fabsf(d.w))));
           }
         } else if (e.dpre_out) {
           *reinterpret_cast<float4*>(e.dpre_out + idx) = v;
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
         }
       }
     }
+  }
+  if (e.out_amax) {  // one atomic per warp (the block is one image)
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+    if (threadIdx.x == 0 && m) atomicMax(e.out_amax + n, m);
   }
   if (e.mode == 0 || !e.partial) return;
 #pragma unroll
@@ -921,6 +966,26 @@ int grid_for(int64_t total, int block) {
   int64_t g = (total + block - 1) / block;
   const int64_t cap = 148 * 32;
   return int(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+// per-image max |x| (blocks over (chunk, image); one atomic per warp)
+__global__ void __launch_bounds__(256) k_amax(const float* __restrict__ x, int64_t per_img,
+                                              uint32_t* __restrict__ amax) {
+  const int64_t n = blockIdx.y;
+  const float* p = x + n * per_img;
+  float mx = 0.f;
+  if (per_img % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < per_img / 4; i += int64_t(gridDim.x) * 256) {
+      const float4 v = q[i];
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  } else {
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < per_img; i += int64_t(gridDim.x) * 256)
+      mx = fmaxf(mx, fabsf(p[i]));
+  }
+  const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(amax + n, m);
 }
 
 }  // namespace
@@ -1122,6 +1187,14 @@ __global__ void k_im2col32(const float* __restrict__ x, int64_t N, int H, int W,
     }
     out[e] = v;
   }
+}
+
+void launch_amax(const float* x, int64_t N, int64_t per_img, uint32_t* amax, cudaStream_t st) {
+  if (N <= 0 || per_img <= 0) return;
+  int64_t bx = (per_img / 4 + 255) / 256;
+  const int64_t cap = (148 * 8 + N - 1) / N;
+  bx = bx < 1 ? 1 : (bx > cap ? cap : bx);
+  k_amax<<<dim3(unsigned(bx), unsigned(N)), 256, 0, st>>>(x, per_img, amax);
 }
 
 void launch_im2col32(const float* x, int64_t N, int H, int W, int Ci, int KH, int KW, int S,

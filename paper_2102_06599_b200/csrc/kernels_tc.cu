@@ -69,6 +69,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
       : "memory");
 }
 
+// Waits for two barrier phases; both probes are issued back to back, so an
+// already-completed pair costs one probe latency instead of two.
+__device__ __forceinline__ void mbar_wait2(uint64_t* b1, uint32_t p1, uint64_t* b2, uint32_t p2) {
+  asm volatile(
+      "{\n\t.reg .pred P1, P2;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P2, [%2], %3;\n\t"
+      "and.pred P1, P1, P2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b1)),
+      "r"(p1), "r"(smem_u32(b2)), "r"(p2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2, int c3) {
   asm volatile(
@@ -114,6 +128,70 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
+// The same for the 3xBF16 B stages: K-major, SWIZZLE_64B (64-byte rows of
+// 32 bf16), 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem], bf16 operands (kind::f16, K=16), fp32 accumulate
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+
+// The 3xBF16 split of two consecutive-K fp32 values (x0 at the lower K
+// index): hi = rn_bf16(x) and lo = rn_bf16(x - hi), each pair packed into
+// one 32-bit TMEM column (the lower K index in the low half).  hi + lo keeps
+// 16 significand bits; hi*hi + hi*lo + lo*hi drops terms of 2^-17 relative.
+__device__ __forceinline__ void split_bf16x2(uint32_t x0, uint32_t x1, uint32_t& hi,
+                                             uint32_t& lo) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(__uint_as_float(x1)), "f"(__uint_as_float(x0)));
+  const float l0 = __uint_as_float(x0) - __uint_as_float(hi << 16);
+  const float l1 = __uint_as_float(x1) - __uint_as_float(hi & 0xffff0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(l1), "f"(l0));
+}
+
+// The fp16 split of two consecutive-K values of x scaled by sA (a power of
+// two, so y = x sA is exact): hi = y rounded to 11 significand bits
+// (Veltkamp with the scale folded into its constant: t = x (2^13 + 1) sA,
+// hi = t - rn(t - y)), lo = y - hi exactly (one FMA), then one packed
+// cvt.rn.f16x2 per half -- two conversions per pair, as many as the bf16
+// split.  With |y| < 2^15, hi converts exactly wherever it is an fp16 normal
+// and hi + lo keeps 22 significand bits (3xTF32's) down to 2^-17 of the
+// image's max; below, both round as fp16 subnormals (2^-25 absolute, 2^-40
+// of the max).  Explicitly rounded intrinsics: the t product must not be
+// contracted into the FMAs that follow it.
+__device__ __forceinline__ void split_f16x2(uint32_t x0, uint32_t x1, float sA, float sAC,
+                                            uint32_t& hi, uint32_t& lo) {
+  const float a0 = __uint_as_float(x0), a1 = __uint_as_float(x1);
+  const float t0 = __fmul_rn(a0, sAC), t1 = __fmul_rn(a1, sAC);
+  const float h0 = __fsub_rn(t0, __fmaf_rn(-a0, sA, t0)), h1 = __fsub_rn(t1, __fmaf_rn(-a1, sA, t1));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(h1), "f"(h0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(__fmaf_rn(a1, sA, -h1)), "f"(__fmaf_rn(a0, sA, -h0)));
+}
+
+// The fp16 split's per-image scale 2^k, k = 14 - e (e = exponent of the
+// image's max |A|, so |A 2^k| < 2^15), and its inverse; 1 when the max is 0
+// or absent.
+__device__ __forceinline__ int amax_shift(uint32_t bits) {
+  if (bits == 0) return 0;
+  int k = 14 - (int((bits >> 23) & 0xff) - 127);
+  return k < -126 ? -126 : (k > 126 ? 126 : k);
+}
+__device__ __forceinline__ float pow2f(int k) { return __int_as_float((k + 127) << 23); }
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
                                          uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -145,6 +223,14 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 __device__ __forceinline__ void split_tf32_fast(uint32_t x, uint32_t& hi, uint32_t& lo) {
   hi = (x + 0x1000u) & 0xffffe000u;
   lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));
+}
+
+// 8 consecutive TMEM columns of this thread's lane <- v[0..7]
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
 }
 
 // 16 consecutive TMEM columns of this thread's lane <- v[0..15]
@@ -304,11 +390,16 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
 // left/right (one warp = one 32-pixel image row, so the neighbour is a lane
 // shuffle).  Same MACs; N=192 runs at the full tcgen05 rate where N=64 hits
 // the ~46-cycle instruction floor.
-template <int BN, bool SPLIT3, bool PAIR, bool KWF = false>
+// BF (3xBF16, with SPLIT3): B_hi / B_lo are bf16 (64-byte SWIZZLE_64B rows of
+// a 32-channel K block), the split A halves take 16 TMEM columns each, and
+// the MMAs are kind::f16 (K=16): half the B bytes and half the MMA time of a
+// 3xTF32 stage.
+template <int BN, bool SPLIT3, bool PAIR, bool KWF = false, bool BF = false>
 struct Cfg {
   static constexpr int kNM = KWF ? 3 * BN : BN;      // MMA N / accumulator columns
   static constexpr int kBRows = PAIR ? kNM / 2 : kNM;  // B rows staged per CTA
-  static constexpr int kBBytes = kBRows * 128;
+  static constexpr int kBBytes = kBRows * (BF ? 64 : 128);
+  static constexpr int kAslot = BF ? 32 : 64;  // TMEM columns of one split A stage
   // accumulator buffers: two (epilogue overlaps the next tile) unless the
   // 3xTF32 A stages would not fit next to them in TMEM
   static constexpr int kAcc = (SPLIT3 && kNM >= 256) ? 1 : 2;
@@ -316,7 +407,7 @@ struct Cfg {
   // live in TMEM (64 columns per stage, after the accumulators)
   static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
   static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
-  static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * kNM) / 64 : 99;
+  static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * kNM) / kAslot : 99;
   // the shared-memory ring (TMA stages) and, in 3xTF32, the TMEM ring of
   // split A stages are separate: a stage's TMEM slot is reused as soon as
   // its MMAs completed, so a wide accumulator (kw-fused N=192) that leaves
@@ -336,8 +427,9 @@ struct Cfg {
 };
 
 // Trace slots (CTA 0, first kTraceStages K blocks): [role][it]
-//   0 producer issues TMA   1 converter sees the data   2 converter done
-//   3 MMA thread sees ready 4 MMA thread committed
+//   0 producer issues TMA   1 converter group 0 sees the data   2 group 0 done
+//   3 MMA thread sees ready 4 MMA thread committed  5 / 6 converter group 1
+//   sees the data / done    7 / 8 group 0 starts waiting / A landed
 __device__ __forceinline__ void trace(const TcArgs& a, int role, int it) {
   if (a.trace && blockIdx.x == 0 && it < kTraceStages)
     a.trace[role * kTraceStages + it] = clock64();
@@ -370,12 +462,14 @@ __device__ __forceinline__ Tile decode(const TcArgs& a, int u, int rank) {
 // 2 = multicast cluster (MC): two CTAs on two M tiles of the same N tile,
 // each TMA-loading half of the B stage multicast into both, so the weight
 // operand crosses L2 -> SM once per cluster; MMAs stay cta_group::1.
-template <int BN, bool SPLIT3, int CL, bool KWF = false>
-__global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
+// H16: 16-bit split halves (with SPLIT3): 0 none (3xTF32), 1 bf16, 2 fp16 (scaled)
+template <int BN, bool SPLIT3, int CL, bool KWF = false, int H16 = 0>
+__global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
               const __grid_constant__ CUtensorMap mapBl, const TcArgs a) {
   constexpr bool PAIR = CL == 1, MC = CL == 2, CLUSTER = CL != 0;
-  using C = Cfg<BN, SPLIT3, PAIR, KWF>;
+  constexpr bool BF = H16 != 0, F16 = H16 == 2;
+  using C = Cfg<BN, SPLIT3, PAIR, KWF, BF>;
   constexpr int NM = C::kNM;
   // ring depth: the configured stage count, or fewer for experiments
   const int dcap = (a.debug >> 16) & 0xf;
@@ -419,7 +513,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   if (a.trace && threadIdx.x == 0) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[5 * kTraceStages + 4 * blockIdx.x] = t;
+    a.trace[kTraceRoles * kTraceStages + 4 * blockIdx.x] = t;
   }
   const int hw = __shfl_sync(0xffffffffu, int(threadIdx.x / 32), 0), lane = int(threadIdx.x % 32);
   const int warp = SPLIT3 ? (hw < 8 ? hw + 8 : hw < 12 ? hw - 4 : hw == 12 ? 2 : hw == 13 ? 3
@@ -429,7 +523,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   constexpr int kCtas = PAIR ? 2 : 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&ready[s], kCtas * (SPLIT3 && a.conv_halves ? 2 : 1));  // (1xTF32: relay arrivals)
+      // 3xTF32 / 3xBF16: one arrival per converter warp that converts the
+      // stage (8 with conv_halves, else 4) per CTA; 1xTF32 pair: relay arrivals
+      mbar_init(&ready[s], kCtas * (SPLIT3 ? (a.conv_halves ? 8 : 4) : 1));
       mbar_init(&tfree[s], 1);
     }
     for (int s = 0; s < S; ++s) {
@@ -479,7 +575,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   if (a.trace && threadIdx.x == 0) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[5 * kTraceStages + 4 * blockIdx.x + 1] = t;
+    a.trace[kTraceRoles * kTraceStages + 4 * blockIdx.x + 1] = t;
   }
   // the barriers the other CTA's threads signal live in the MMA CTA (rank 0)
   const uint32_t ready_remote = PAIR ? mapa(ready, 0) : 0;
@@ -544,7 +640,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       // The whole warp runs the loop (descriptors stay warp-uniform, in
       // uniform registers); each tcgen05.mma / commit is issued by one
       // elect.sync-chosen lane inside its asm block.
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NM >> 3) << 17) |
+      // D f32; A / B tf32 (2), or kind::f16 fp16 (0) / bf16 (1); K-major; N, M
+      constexpr uint32_t ab = BF ? (F16 ? 0u : 1u) : 2u;
+      constexpr uint32_t idesc = (1u << 4) | (ab << 7) | (ab << 10) | (uint32_t(NM >> 3) << 17) |
                                  (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
       int stage = 0, mit = 0, tslot = 0;
       uint32_t phase = 0, tph = 0;
@@ -565,16 +663,29 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           if (PAIR) {
             mbar_wait_cluster(SPLIT3 ? &ready[tslot] : &ready[stage], SPLIT3 ? tph : phase);
           } else if (SPLIT3) {
-            mbar_wait(&ready[tslot], tph);  // A converted (kSplitA: A landed before)
-            mbar_wait(&full[stage], phase);  // B landed
+            // B landed and A converted (kSplitA: A landed before), probed together
+            mbar_wait2(&full[stage], phase, &ready[tslot], tph);
           } else {
             mbar_wait(&full[stage], phase);
           }
           trace(a, 3, mit);
           tc_fence_after();
-          const uint64_t dbh = sw128_desc(smem_u32(b_hi(stage)));
+          const uint64_t dbh = BF ? sw64_desc(smem_u32(b_hi(stage))) : sw128_desc(smem_u32(b_hi(stage)));
           if (a.debug & 2) {
             // experiment: no MMAs (measures the TMA + converter pipeline alone)
+          } else if (BF) {
+            // 3xBF16: A_hi / A_lo in TMEM columns [a_t, a_t+16) / [a_t+16, a_t+32)
+            // (two bf16 per column), B_hi / B_lo 64-byte rows; two K=16 steps
+            const uint32_t a_t = tmem_base + uint32_t(C::kAcol0 + tslot * C::kAslot);
+            const uint64_t dbl = sw64_desc(smem_u32(b_lo(stage)));
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint64_t koff = uint64_t(k * 32) >> 4;  // 16 bf16 = 32 B along K
+              const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+              mma_bf16_ts(d_tmem, a_t + 8 * k, dbh + koff, idesc, accum);
+              mma_bf16_ts(d_tmem, a_t + 8 * k, dbl + koff, idesc, 1u);
+              mma_bf16_ts(d_tmem, a_t + 16 + 8 * k, dbh + koff, idesc, 1u);
+            }
           } else if (SPLIT3) {
             // A_hi / A_lo of this stage in TMEM columns [a_t, a_t+32) / [a_t+32, a_t+64)
             // (debug 128: every stage's MMAs read stage 0's columns -- no
@@ -686,7 +797,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * NM);
       // accumulator chunk [c, c+16) of the layer's output channels; KWF adds
       // the kw = 0 / 2 column blocks of the pixels kwf_sgn*(kw - 1) away
-      auto acc_ld16 = [&](int c, float* v) {
+      // fp16 split: undo the row's image scale and the weight scale
+      constexpr bool unscale = F16;
+      float inv_a = 1.f;
+      if (unscale && a.a_amax && valid) inv_a = pow2f(-amax_shift(a.a_amax[n]));
+      float out_mx = 0.f;  // max |value| this thread stores for the next GEMM (out_amax)
+      auto acc_ld16_raw = [&](int c, float* v) {
         if (!KWF) {
           tmem_ld16(trow + uint32_t(c), v);
         } else {
@@ -708,6 +824,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
             v[i] = __uint_as_float(m[i]) + (kw_lane > 0 ? from_left : 0.f) +
                    (kw_lane < a.kwf_w - 1 ? from_right : 0.f);
           }
+        }
+      };
+      auto acc_ld16 = [&](int c, float* v) {
+        acc_ld16_raw(c, v);
+        if (unscale) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = (v[i] * inv_a) * a.b_inv;
         }
       };
       // Fused dgrad epilogue of the Fisher pipeline (each warp's 32 rows in one
@@ -782,6 +905,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
               o.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
               o.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
               o.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+              if (valid)
+                out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
               *reinterpret_cast<float4*>(xp + lane * 20 + 4 * i) = o;
             }
             __syncwarp();
@@ -871,6 +996,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
                 x.z = x.z > 0.f ? x.z : 0.f;
                 x.w = x.w > 0.f ? x.w : 0.f;
               }
+              out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
               o[i] = x;
             }
           }
@@ -908,14 +1034,18 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
                   x.y = (a.relu_prev && !(av[4 * i + 1] > 0.f)) ? 0.f : v[4 * i + 1];
                   x.z = (a.relu_prev && !(av[4 * i + 2] > 0.f)) ? 0.f : v[4 * i + 2];
                   x.w = (a.relu_prev && !(av[4 * i + 3] > 0.f)) ? 0.f : v[4 * i + 3];
+                  out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
                   dp[i] = x;
                 }
               }
             } else if (a.dpre_out) {
               float4* dp = reinterpret_cast<float4*>(a.dpre_out + base);
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
+              for (int i = 0; i < 4; ++i) {
                 dp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(v[4 * i]), fabsf(v[4 * i + 1])),
+                                             fmaxf(fabsf(v[4 * i + 2]), fabsf(v[4 * i + 3]))));
+              }
             }
           }
           if (a.partial && tile_real && rows_per_img % 32 == 0) {
@@ -973,109 +1103,141 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
           mbar_arrive(&tempty[acc]);
         }
       }
+      // per-image max of what this tile stored for the next GEMM: lanes of
+      // one image reduce together, one atomic per image per warp
+      if (a.out_amax && a.ksplit == 1) {
+        const int key = (valid && tile_real) ? n : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const unsigned m = __reduce_max_sync(grp, __float_as_uint(out_mx));
+        if (key >= 0 && m && lane == __ffs(grp) - 1) atomicMax(a.out_amax + key, m);
+      }
     }
   } else if (SPLIT3 && warp >= 8) {
-    // ---------------- 3xTF32 split converter: thread r owns A row r (TMEM
-    // lane r): reads its 128-byte row from the swizzled stage (16-byte chunk
-    // c sits at c ^ (r & 7)), splits it into rn_tf32 hi/lo halves and stores
-    // them to the stage's 64 TMEM columns
-    // two groups of four warps take alternate K blocks, so one group's
-    // shared-memory reads and splits overlap the other's TMEM stores
+    // ---------------- split converter: thread ct owns A row ct (TMEM lane
+    // ct): reads its 128-byte row from the swizzled stage (16-byte chunk c
+    // sits at c ^ (ct & 7)), splits it into hi / lo halves (3xTF32: rn_tf32
+    // and the exact fp32 remainder, 32 + 32 TMEM columns; 3xBF16: packed
+    // rn_bf16 pairs, 16 + 16 columns) and stores them to the stage's TMEM
+    // slot.  conv_halves: both groups of four warps convert every stage, group
+    // cg the channels [16cg, 16cg + 16); else the groups alternate stages.
+    // Each warp signals `ready` itself once its stores completed (no group
+    // barrier), and the ring counters advance incrementally, so a stage
+    // costs the conversion plus one barrier probe.
     const int cg = (warp - 8) >> 2;
     const int ct = ((warp - 8) & 3) * 32 + lane;  // 0..127 == TMEM lane
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    int it = 0;  // K blocks seen by this CTA (both groups count all of them)
+    const bool halves = a.conv_halves != 0;
+    int it = 0, stage = 0, tslot = 0;  // K blocks seen by this CTA (both groups count all)
+    uint32_t phase = 0, tph = 0;
+    constexpr bool f16 = F16;
     for (int u = unit0; u < num_units; u += ustep) {
       const Tile d = decode<CLUSTER>(a, u, int(rank));
+      // fp16 split: this row's image scale (rows past the batch keep 1)
+      float sA = 1.f;
+      if (f16 && a.a_amax) {
+        const int ni = ct / (a.BW * a.BH), n = (d.m / (a.tiles_w * a.tiles_h)) * a.BNI + ni;
+        if (d.m < a.m_tiles && ni < a.BNI && n < a.nimg) sA = pow2f(amax_shift(a.a_amax[n]));
+      }
       for (int kb = d.kb0; kb < d.kb1; ++kb, ++it) {
-        // conv_halves: both groups convert every stage, group cg channels
-        // [16cg, 16cg+16) -- half the per-stage latency; else alternate stages
-        if (!a.conv_halves && (it & 1) != cg) continue;
-        const int stage = it % S;
-        const uint32_t phase = uint32_t(it / S) & 1u;
-        const int tslot = it % ST;
-        const uint32_t tph = uint32_t(it / ST) & 1u;
-        mbar_wait(kSplitA ? &fulla[stage] : &full[stage], phase);
-        if (PAIR) {
-          mbar_wait_cluster(&tfree[tslot], tph ^ 1);  // the slot's previous MMAs are done
-        } else {
-          mbar_wait(&tfree[tslot], tph ^ 1);
-        }
-        trace(a, 1, it);
-        if (a.debug & 32) {  // experiment: no conversion work
-          named_bar(2 + cg, 128);
-          if (ct == 0) {
-            if (PAIR) mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
-            else mbar_arrive(&ready[tslot]);
+        if (halves || (it & 1) == cg) {
+          if (ct == 0 && cg == 0) trace(a, 7, it);
+          if (PAIR) {
+            mbar_wait(&full[stage], phase);
+            mbar_wait_cluster(&tfree[tslot], tph ^ 1);  // the slot's previous MMAs are done
+          } else {
+            mbar_wait2(kSplitA ? &fulla[stage] : &full[stage], phase, &tfree[tslot], tph ^ 1);
           }
-          continue;
-        }
-        const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
-        if (a.conv_halves) {
-          uint32_t hi[16], lo[16];
+          if (ct == 0) trace(a, cg ? 5 : 1, it);
+          if (!(a.debug & 32)) {  // (debug 32: no conversion work; experiments)
+            const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
+            const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + tslot * C::kAslot);
+            if (BF) {
+              uint32_t hi[16], lo[16];
+              uint4 xs[8];
+              const int c0 = halves ? 4 * cg : 0, nc = halves ? 4 : 8;
+              // all of the row's loads first, then the splits
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint4 x;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                         : "r"(row + uint32_t(((4 * cg + c) ^ (ct & 7)) << 4)));
-            split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
-            split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
-            split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
-            split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+              for (int c = 0; c < 8; ++c)
+                if (c < nc)
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
+                               : "r"(row + uint32_t(((c0 + c) ^ (ct & 7)) << 4)));
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                if (c >= nc) break;
+                if (f16) {
+                  split_f16x2(xs[c].x, xs[c].y, sA, sA * 8193.0f, hi[2 * c], lo[2 * c]);
+                  split_f16x2(xs[c].z, xs[c].w, sA, sA * 8193.0f, hi[2 * c + 1], lo[2 * c + 1]);
+                } else {
+                  split_bf16x2(xs[c].x, xs[c].y, hi[2 * c], lo[2 * c]);
+                  split_bf16x2(xs[c].z, xs[c].w, hi[2 * c + 1], lo[2 * c + 1]);
+                }
+              }
+              if (halves) {
+                tmem_st8(ta + 8 * cg, hi);
+                tmem_st8(ta + 16 + 8 * cg, lo);
+              } else {
+                tmem_st16(ta, hi);
+                tmem_st16(ta + 16, lo);
+              }
+            } else if (halves) {
+              uint32_t hi[16], lo[16];
+              uint4 xs[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
+                             : "r"(row + uint32_t(((4 * cg + c) ^ (ct & 7)) << 4)));
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const uint4 x = xs[c];
+                split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
+                split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+                split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+                split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+              }
+              tmem_st16(ta + 16 * cg, hi);
+              tmem_st16(ta + 32 + 16 * cg, lo);
+            } else {
+              uint32_t hi[32], lo[32];
+              uint4 xs[8];
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
+                             : "r"(row + uint32_t((c ^ (ct & 7)) << 4)));
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 x = xs[c];
+                split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
+                split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+                split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+                split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+              }
+              tmem_st32(ta, hi);
+              tmem_st32(ta + 32, lo);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
-          const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + tslot * 64 + 16 * cg);
-          tmem_st16(ta, hi);
-          tmem_st16(ta + 32, lo);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          // this warp's 32 rows stored -> one arrival per warp on the MMA CTA's barrier
           tc_fence_before();
-          named_bar(2 + cg, 128);
-          if (ct == 0) trace(a, 2, it);
-          if (ct == 0) {
+          __syncwarp();
+          if (ct == 0) trace(a, cg ? 6 : 2, it);
+          if (lane == 0) {
             if (PAIR) {
               mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
             } else {
               mbar_arrive(&ready[tslot]);
             }
           }
-          continue;
         }
-        uint32_t hi[32], lo[32];
-        if (a.debug & 1024) {  // experiment: no smem reads / splits (store garbage)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) hi[i] = lo[i] = uint32_t(i);
-        } else
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 x;
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                       : "r"(row + uint32_t((c ^ (ct & 7)) << 4)));
-          split_tf32_fast(x.x, hi[4 * c], lo[4 * c]);
-          split_tf32_fast(x.y, hi[4 * c + 1], lo[4 * c + 1]);
-          split_tf32_fast(x.z, hi[4 * c + 2], lo[4 * c + 2]);
-          split_tf32_fast(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
-        // (debug 256: converters store to stage 0's columns only; experiments)
-        const uint32_t ta =
-            tmem_base + lane_base + uint32_t(C::kAcol0 + ((a.debug & 256) ? 0 : tslot) * 64);
-        if (a.debug & 512) {  // experiment: no TMEM stores
-          asm volatile("" ::"r"(hi[0] ^ lo[31] ^ hi[17] ^ lo[5]));
-        } else {
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        // all 128 rows stored -> one arrival per CTA on the MMA CTA's barrier
-        tc_fence_before();
-        named_bar(2 + cg, 128);
-        if (ct == 0) trace(a, 2, it);
-        if (ct == 0) {
-          if (PAIR) {
-            mbar_arrive_remote(ready_remote + uint32_t(tslot * 8));
-          } else {
-            mbar_arrive(&ready[tslot]);
-          }
+        if (++tslot == ST) {
+          tslot = 0;
+          tph ^= 1;
         }
       }
     }
@@ -1083,12 +1245,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF>::kThreads, 1)
   if (a.trace && warp == 1 && lane == 0) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[5 * kTraceStages + 4 * blockIdx.x + 2] = t;  // MMA warp done issuing
+    a.trace[kTraceRoles * kTraceStages + 4 * blockIdx.x + 2] = t;  // MMA warp done issuing
   }
   if (a.trace && warp == 4 && lane == 0) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[5 * kTraceStages + 4 * blockIdx.x + 3] = t;  // epilogue done
+    a.trace[kTraceRoles * kTraceStages + 4 * blockIdx.x + 3] = t;  // epilogue done
   }
   tc_fence_before();
   if (CLUSTER) {
@@ -1133,24 +1295,29 @@ bool make_map_4d(CUtensorMap* m, const float* base, int C, int W, int H, int N, 
   return r == CUDA_SUCCESS;
 }
 
-bool make_map_2d(CUtensorMap* m, const float* base, int K, int rows, int box_rows) {
+// B operand: [rows][K] fp32 (128-byte boxes of 32, SWIZZLE_128B) or, for
+// 3xBF16, bf16 (64-byte boxes of 32, SWIZZLE_64B)
+bool make_map_2d(CUtensorMap* m, const void* base, int K, int rows, int box_rows, bool bf,
+                 bool f16 = false) {
   cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(K) * 4};
+  cuuint64_t strides[1] = {cuuint64_t(K) * (bf ? 2 : 4)};
   cuuint32_t box[2] = {32, cuuint32_t(box_rows)};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode_fn()(m, bf ? (f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16)
+                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool SPLIT3, int CL, bool KWF = false>
+template <int BN, bool SPLIT3, int CL, bool KWF = false, int H16 = 0>
 cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
-  using C = Cfg<BN, SPLIT3, CL == 1, KWF>;
+  using C = Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3, CL, KWF>,
+    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN, SPLIT3, CL, KWF, H16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -1186,7 +1353,7 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL, KWF>, L.mapA, L.mapBh, L.mapBl, a);
+  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL, KWF, H16>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
 }  // namespace
@@ -1208,19 +1375,39 @@ bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a) {
   return true;
 }
 
-bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const float* Bhi,
-               const float* Blo, int BK, int Brows) {
+bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const void* Bhi,
+               const void* Blo, int BK, int Brows) {
   const TcArgs& a = L.args;
   if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
   // a pair stages half of B per CTA; a multicast cluster loads half per CTA
   const int nm = L.kwf ? 3 * L.bn : L.bn;  // MMA N (B rows of a stage)
   const int box_rows = (L.pair || L.mc) ? nm / 2 : nm;
-  if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, box_rows)) return false;
-  if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, box_rows)) return false;
+  const bool f16 = L.bf && a.h16_f16;
+  if (!make_map_2d(&L.mapBh, Bhi, BK, Brows, box_rows, L.bf, f16)) return false;
+  if (!make_map_2d(&L.mapBl, Blo ? Blo : Bhi, BK, Brows, box_rows, L.bf, f16)) return false;
   return true;
 }
 
 cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
+  if (L.bf) {  // 16-bit split: single-CTA plans only
+    if (!L.split3 || L.pair || L.mc) return cudaErrorInvalidValue;
+    if (L.args.h16_f16) {
+      if (L.kwf) return L.bn == 64 ? launch_t<64, true, 0, true, 2>(L, st) : cudaErrorInvalidValue;
+      switch (L.bn) {
+        case 32: return launch_t<32, true, 0, false, 2>(L, st);
+        case 64: return launch_t<64, true, 0, false, 2>(L, st);
+        case 128: return launch_t<128, true, 0, false, 2>(L, st);
+      }
+    } else {
+      if (L.kwf) return L.bn == 64 ? launch_t<64, true, 0, true, 1>(L, st) : cudaErrorInvalidValue;
+      switch (L.bn) {
+        case 32: return launch_t<32, true, 0, false, 1>(L, st);
+        case 64: return launch_t<64, true, 0, false, 1>(L, st);
+        case 128: return launch_t<128, true, 0, false, 1>(L, st);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
   if (L.kwf) {
     if (L.bn != 64 || L.pair) return cudaErrorInvalidValue;
     if (L.mc)

@@ -73,12 +73,25 @@ struct TcArgs {
   // 3xTF32 converters: both groups split every stage (channel halves) rather
   // than alternating stages (lower per-stage latency for shallow rings)
   int conv_halves;
+  // 16-bit split (Cfg BF): 1 = fp16 halves (kind::f16 f16, scaled), 0 = bf16.
+  // fp16 scaling: A row r of image n is multiplied by 2^(14 - e_n) before the
+  // split, e_n the exponent of a_amax[n] (max |A| of image n, float bits;
+  // null = no scaling), the weights were packed times b_scale; the epilogue
+  // multiplies the accumulator by 2^-(14 - e_n) and b_inv = 1 / b_scale.
+  // Powers of two: the scaled products and sums are the unscaled ones
+  // exactly, outside fp16 subnormals.
+  int h16_f16;
+  const uint32_t* a_amax;
+  float b_inv;
+  // per-image max |value| of what this launch writes for the next GEMM
+  // (fprop: the stored output; dgrad: dpre_out), atomicMax on float bits;
+  // null = not recorded
+  uint32_t* out_amax;
   // experiments only (NB_TC_DEBUG; every bit but the stage cap gives
   // garbage results): 2 = no MMAs, 4 = no A loads, 8 = no B loads, 16 = no
-  // epilogue, 32 = no 3xTF32 conversion, 64 = no tiles at all, 128 / 256 =
-  // MMAs read / converters write stage 0's TMEM columns only, 512 = no TMEM
-  // stores, 1024 = no split, 2048 = no A_prev loads, 4096 = no Fisher
-  // reduction, 8192 = no dpre stores; bits 16..19 cap the ring depth
+  // epilogue, 32 = no split conversion, 64 = no tiles at all, 128 = MMAs
+  // read stage 0's TMEM columns only, 2048 = no A_prev loads, 4096 = no
+  // Fisher reduction, 8192 = no dpre stores; bits 16..19 cap the ring depth
   // (0 = the configured stage count)
   int debug;
   // experiments only (NB_TC_TRACE): CTA 0 records clock64() stamps of its
@@ -86,6 +99,8 @@ struct TcArgs {
   long long* trace;
 };
 constexpr int kTraceStages = 256;
+// trace roles per stage (see kernels_tc.cu trace()); CTA stamps follow them
+constexpr int kTraceRoles = 9;
 
 struct TcLaunch {
   CUtensorMap mapA, mapBh, mapBl;
@@ -95,6 +110,8 @@ struct TcLaunch {
   bool pair;    // CTA pair (cluster of 2): M = 256 per tcgen05.mma.cta_group::2
   bool mc = false;  // multicast cluster of 2: B halves multicast, MMAs per CTA
   bool kwf = false;  // kw-fused 64-channel plan (MMA N = 192)
+  bool bf = false;   // 16-bit split (with split3): 16-bit B_hi / B_lo, kind::f16 MMAs
+                     // (args.h16_f16: fp16, else bf16)
   int num_sms;
 };
 
@@ -102,8 +119,9 @@ struct TcLaunch {
 // nimg images; false if the TMA box would be illegal.
 bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a);
 // Encodes the tensor maps (A: C x W x H x N activation, B: rows x K weights).
-bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const float* Bhi,
-               const float* Blo, int BK, int Brows);
+// (B_hi / B_lo are bf16 arrays when L.bf)
+bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const void* Bhi,
+               const void* Blo, int BK, int Brows);
 cudaError_t launch(const TcLaunch& L, cudaStream_t st);
 
 }  // namespace tc

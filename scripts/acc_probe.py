@@ -32,7 +32,7 @@ for K in (64, 512, 2048, 4096):
         x, w = tf32(x), tf32(w)
         exact = np.einsum("nchw,oc->nohw", x, w[:, :, 0, 0])
         scale = np.einsum("nchw,oc->nohw", np.abs(x), np.abs(w[:, :, 0, 0]))
-        for name, p in (("tf32", Precision.TF32), ("3xtf32", Precision.FP32),
+        for name, p in (("tf32", Precision.TF32), (nb.fp32_split(), Precision.FP32),
                         ("simt", Precision.SIMT)):
             y = nb.reference_conv(s, x, w, precision=p, ctx=ctx)
             m = np.abs(exact) > 1e-3 * scale

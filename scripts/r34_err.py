@@ -12,7 +12,7 @@ o = resnet34_chain()
 s = nb.Session(o, nb.make_batch(o, 128, 1), ctx=nb.Context(0))
 for e, net, pc, probs in _nets():
     line = [f"{e['name']:8s} {e['kind']:16s}"]
-    for name, p in (("3xtf32", Precision.FP32), ("simt", Precision.SIMT), ("tf32", Precision.TF32)):
+    for name, p in ((nb.fp32_split(), Precision.FP32), ("simt", Precision.SIMT), ("tf32", Precision.TF32)):
         r = s.fisher(net, p)
         pl = np.array(e["per_layer"])
         le = np.abs(r.per_layer - pl) / np.abs(pl)

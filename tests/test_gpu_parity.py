@@ -319,9 +319,10 @@ def test_padded_specs_run_on_tensor_cores(spec):
     c.set_profiling(True)
     s.fisher(net)
     names = set(c.kernel_stats())
-    assert "conv_fprop_tc_3xtf32" in names, names
+    split = nb.fp32_split()  # "3xbf16" (default) or "3xtf32"
+    assert f"conv_fprop_tc_{split}" in names, names
     if spec.ci % 16 == 0 and not spec.channel_splits:
-        assert "conv_dgrad_tc_3xtf32_fisher" in names, names
+        assert f"conv_dgrad_tc_{split}_fisher" in names, names
         assert "conv_dgrad_direct_fisher" not in names, names
 
 
