@@ -178,6 +178,13 @@ bool use_dense(const RangeDesc& r, int64_t Ci) {
          r.len % 16 == 0;
 }
 
+// Images per M tile of a tensor-core launch over `nimg` images.
+int plan_bni(int OH, int OW, int64_t nimg, int S) {
+  tc::TcArgs t{};
+  tc::plan_tiles(OH, OW, int(nimg), S, t);
+  return t.BNI;
+}
+
 // M tiles of a tensor-core launch over `nimg` images (plan_tiles' count).
 int m_tiles_at(int OH, int OW, int64_t nimg, int S) {
   tc::TcArgs t{};
@@ -417,6 +424,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
               P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.OH * g.OW * g.Co);
             TcPlan& tp = lp.tcf[i];
             tp.bn = bn;
+            tp.plan_bni = plan_bni(g.OH, g.OW, plan_n, g.S);
             tp.pair = pbn != 0;
             tp.mc = mc;
             tp.kwf = kwf;
@@ -535,6 +543,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
             P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
           tp.bn = bn;
+          tp.plan_bni = plan_bni(gh, gw, plan_n, 1);
           tp.pair = pbn != 0;
           tp.mc = mc;
           tp.kwf = kwf;
@@ -723,6 +732,49 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   const int ch = convh >= 0 ? convh : (bf3 ? 0 : 1);
   L.args.conv_halves = ch == 1 || (ch == 2 && tp.kwf) ? 1 : 0;
   L.num_sms = c->num_sms;
+  // Halo mode (NB_TC_HALO=1): a split-converter launch over a
+  // stride-1 A operand with several taps per phase loads one halo box per
+  // 32-channel chunk (tile + the taps' offsets) and its converters form the
+  // shifted rows of every tap from it, when the box fits the kernel's halo
+  // buffers.
+  // (off by default: on the R34 bench it moves nothing -- the split
+  // converters, not the A operand's L2 traffic, bound these launches --
+  // profiles/r02_kernels.md)
+  static const bool halo_on = [] {
+    const char* e = std::getenv("NB_TC_HALO");
+    return e && std::atoi(e) != 0;
+  }();
+  L.args.halo = 0;
+  if (halo_on && split3 && !tp.pair && !tp.mc && args.S == 1) {
+    int span_h = 0, span_w = 0, most = 0;
+    for (int ph = 0; ph < args.nphase; ++ph) {
+      int h0 = 0, h1 = 0, w0 = 0, w1 = 0;
+      for (int t = 0; t < args.ntaps[ph]; ++t) {
+        const int dh = tc::tap_dh(args.taps[ph][t]), dw = tc::tap_dw(args.taps[ph][t]);
+        h0 = t ? std::min(h0, dh) : dh;
+        h1 = t ? std::max(h1, dh) : dh;
+        w0 = t ? std::min(w0, dw) : dw;
+        w1 = t ? std::max(w1, dw) : dw;
+      }
+      L.args.halo_dh0[ph] = h0;
+      L.args.halo_dw0[ph] = w0;
+      span_h = std::max(span_h, h1 - h0);
+      span_w = std::max(span_w, w1 - w0);
+      most = std::max(most, args.ntaps[ph]);
+    }
+    const int hh = args.BH + span_h, hw = args.BW + span_w;
+    const int64_t bytes = int64_t(hh) * hw * std::max(args.BNI, tp.plan_bni) * 128;
+    if (most >= 2 && hh <= 256 && hw <= 256 && bytes <= tc::halo_capacity(L)) {
+      L.args.halo = 1;
+      L.args.halo_h = hh;
+      L.args.halo_w = hw;
+    }
+  }
+  static const bool halo_log = std::getenv("NB_TC_HALO_LOG") != nullptr;  // (experiments)
+  if (halo_log)
+    std::fprintf(stderr, "tc mode %d n %d BW %d BH %d BNI %d mt %d nt %d ks %d taps %d halo %d %dx%d\n",
+                 args.mode, args.nimg, args.BW, args.BH, args.BNI, args.m_tiles, args.n_tiles,
+                 args.ksplit, args.ntaps[0], L.args.halo, L.args.halo_w, L.args.halo_h);
   if (!tc::make_maps(L, A, AC, AW, AH, AN, whi, whi + tp.w_n, tp.b_k, tp.b_rows))
     fail(NB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   NB_CUDA(tc::launch(L, st));

@@ -65,6 +65,10 @@ struct TcPlan {
   // stem on the session's im2col copy of the batch: A = (N, OH, OW, 32) with
   // K = (tap, channel) in 32 columns, a 1x1 GEMM (session_xcol)
   bool col = false;
+  // images per M tile at the planning batch size: the halo-mode decision
+  // (launch_tc) is made on it, so an example shard (fewer images, possibly
+  // fewer per tile) runs the whole batch's K order
+  int plan_bni = 0;
 };
 
 // Lowered layer: geometry + per-range family + packed-weight offsets.

@@ -164,22 +164,28 @@ __device__ __forceinline__ void split_bf16x2(uint32_t x0, uint32_t x1, uint32_t&
 }
 
 // The fp16 split of two consecutive-K values of x scaled by sA (a power of
-// two, so y = x sA is exact): hi = y rounded to 11 significand bits
-// (Veltkamp with the scale folded into its constant: t = x (2^13 + 1) sA,
-// hi = t - rn(t - y)), lo = y - hi exactly (one FMA), then one packed
-// cvt.rn.f16x2 per half -- two conversions per pair, as many as the bf16
-// split.  With |y| < 2^15, hi converts exactly wherever it is an fp16 normal
-// and hi + lo keeps 22 significand bits (3xTF32's) down to 2^-17 of the
-// image's max; below, both round as fp16 subnormals (2^-25 absolute, 2^-40
-// of the max).  Explicitly rounded intrinsics: the t product must not be
-// contracted into the FMAs that follow it.
-__device__ __forceinline__ void split_f16x2(uint32_t x0, uint32_t x1, float sA, float sAC,
-                                            uint32_t& hi, uint32_t& lo) {
-  const float a0 = __uint_as_float(x0), a1 = __uint_as_float(x1);
-  const float t0 = __fmul_rn(a0, sAC), t1 = __fmul_rn(a1, sAC);
-  const float h0 = __fsub_rn(t0, __fmaf_rn(-a0, sA, t0)), h1 = __fsub_rn(t1, __fmaf_rn(-a1, sA, t1));
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(h1), "f"(h0));
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(__fmaf_rn(a1, sA, -h1)), "f"(__fmaf_rn(a0, sA, -h0)));
+// two, so y = x sA is exact): hi = y truncated to 11 significand bits (one
+// LOP on the fp32 bits), lo = y - hi exactly (13 bits, |lo| < 2^-10 |y|),
+// then one packed cvt.rn.f16x2 per half: hi converts exactly wherever it is
+// an fp16 normal, lo rounds to 11 bits, so hi + lo carries y to 2^-22 |y|
+// (3xTF32's accuracy) down to 2^-17 of the image's max; below, both round
+// as fp16 subnormals (2^-25 absolute, 2^-40 of the max).  The scaling and
+// the remainder run as packed fp32x2 instructions (6 instructions per pair).
+__device__ __forceinline__ void split_f16x2(uint32_t x0, uint32_t x1, float sA, uint32_t& hi,
+                                            uint32_t& lo) {
+  uint32_t y0, y1;
+  asm("{\n\t.reg .b64 xx, ss, yy;\n\t"
+      "mov.b64 xx, {%2, %3};\n\tmov.b64 ss, {%4, %4};\n\t"
+      "mul.rn.f32x2 yy, xx, ss;\n\tmov.b64 {%0, %1}, yy;\n\t}"
+      : "=r"(y0), "=r"(y1) : "r"(x0), "r"(x1), "f"(sA));
+  const uint32_t h0 = y0 & 0xffffe000u, h1 = y1 & 0xffffe000u;
+  uint32_t l0, l1;
+  asm("{\n\t.reg .b64 yy, hh, ll;\n\t"
+      "mov.b64 yy, {%2, %3};\n\tmov.b64 hh, {%4, %5};\n\t"
+      "sub.rn.f32x2 ll, yy, hh;\n\tmov.b64 {%0, %1}, ll;\n\t}"
+      : "=r"(l0), "=r"(l1) : "r"(y0), "r"(y1), "r"(h0), "r"(h1));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "r"(h1), "r"(h0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "r"(l1), "r"(l0));
 }
 
 // The fp16 split's per-image scale 2^k, k = 14 - e (e = exponent of the
@@ -403,18 +409,35 @@ struct Cfg {
   // accumulator buffers: two (epilogue overlaps the next tile) unless the
   // 3xTF32 A stages would not fit next to them in TMEM
   static constexpr int kAcc = (SPLIT3 && kNM >= 256) ? 1 : 2;
-  // smem stage: [A fp32 (TMA) | B_hi | B_lo?]; in 3xTF32 the split A halves
-  // live in TMEM (64 columns per stage, after the accumulators)
-  static constexpr int kStageBytes = kABytes + kBBytes * (SPLIT3 ? 2 : 1);
-  static constexpr int kSmemStages = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
+  // smem stage: A fp32 (TMA) + B_hi + B_lo?; in the split modes the split A
+  // halves live in TMEM (kAslot columns per stage, after the accumulators).
+  // Layout: [A of every stage | B of every stage | ...]: in halo mode the A
+  // region holds two halo buffers of kStages / 2 A stages each instead.
+  static constexpr int kBStageBytes = kBBytes * (SPLIT3 ? 2 : 1);
+  static constexpr int kStageBytes = kABytes + kBStageBytes;
+  // split modes: kConvGroups groups of four converter warps take the stages
+  // in turn.  Two by default; NB_TC_BF_GROUPS=3 (compile time) gives the
+  // 16-bit splits a third group (20 warps, at most 96 registers per thread:
+  // measured 3-5% slower on the bench than two, profiles/r02_kernels.md).
+  // A group waits only on the stages it converts, so with three groups the
+  // rings hold a multiple of three stages (a barrier is then never more than
+  // one phase ahead of a waiter).
+#ifndef NB_TC_BF_GROUPS
+#define NB_TC_BF_GROUPS 2
+#endif
+  static constexpr int kConvGroups = SPLIT3 ? (BF ? NB_TC_BF_GROUPS : 2) : 0;
+  static constexpr int kRing = kConvGroups == 3 ? 3 : 1;  // (two groups: see halves_on)
+  static constexpr int kSmemStages0 = (192 * 1024) / kStageBytes > 6 ? 6 : (192 * 1024) / kStageBytes;
+  static constexpr int kSmemStages = kSmemStages0 / kRing * kRing;
   static constexpr int kTmemStages = SPLIT3 ? (512 - kAcc * kNM) / kAslot : 99;
   // the shared-memory ring (TMA stages) and, in 3xTF32, the TMEM ring of
   // split A stages are separate: a stage's TMEM slot is reused as soon as
   // its MMAs completed, so a wide accumulator (kw-fused N=192) that leaves
   // room for only two A slots still gets a three-deep TMA ring
   static constexpr int kStages = kSmemStages;
-  static constexpr int kTStages = kTmemStages < kSmemStages ? kTmemStages : kSmemStages;
-  static constexpr int kThreads = SPLIT3 ? 512 : 256;  // 3xTF32: two converter groups
+  static constexpr int kTStages =
+      (kTmemStages < kSmemStages ? kTmemStages : kSmemStages) / kRing * kRing;
+  static constexpr int kThreads = SPLIT3 ? 128 * (kConvGroups + 2) : 256;
   static constexpr int kTmemCols = SPLIT3 ? 512
                                  : (kAcc * kNM) <= 32 ? 32 : (kAcc * kNM) <= 64 ? 64
                                  : (kAcc * kNM) <= 128 ? 128 : (kAcc * kNM) <= 256 ? 256 : 512;
@@ -424,6 +447,12 @@ struct Cfg {
   static constexpr int kXposeBytes = 4 * 32 * 20 * 4;
   static constexpr int kRedBytes = 128 * 17 * 4 + kXposeBytes;
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 512;
+  // halo buffer capacity (bytes) of halo mode (TcArgs::halo)
+#ifndef NB_TC_INTERLEAVED
+  static constexpr int halo_cap() { return (kStages / 2) * kABytes; }
+#else
+  static constexpr int halo_cap() { return 0; }
+#endif
 };
 
 // Trace slots (CTA 0, first kTraceStages K blocks): [role][it]
@@ -473,16 +502,25 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   constexpr int NM = C::kNM;
   // ring depth: the configured stage count, or fewer for experiments
   const int dcap = (a.debug >> 16) & 0xf;
-  const int S = dcap > 0 && dcap < C::kStages ? dcap : C::kStages;
+  const int S = dcap > 0 && dcap < C::kStages ? (dcap / C::kRing > 0 ? dcap / C::kRing * C::kRing : C::kRing)
+                                               : C::kStages;
   const int ST = SPLIT3 ? (S < C::kTStages ? S : C::kTStages) : S;  // TMEM A slots
   constexpr int NACC = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage layout: [A | B_hi | B_lo?]
+  // layout: [A_0 .. A_{S-1} | (B_hi B_lo?)_0 .. | red | barriers]; halo mode:
+  // halo buffer h = A stages [h * kStages/2, (h + 1) * kStages/2)
+#ifndef NB_TC_INTERLEAVED
+  auto a_hi = [&](int s) { return smem + s * kABytes; };
+  auto b_hi = [&](int s) { return smem + C::kStages * kABytes + s * C::kBStageBytes; };
+  auto b_lo = [&](int s) { return smem + C::kStages * kABytes + s * C::kBStageBytes + C::kBBytes; };
+#else
   auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
   auto b_hi = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
   auto b_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes + C::kBBytes; };
+#endif
+  auto halo_buf = [&](int h) { return smem + h * (C::kStages / 2) * kABytes; };
   float* red = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kRedBytes);
   uint64_t* full = bars;            // S: this CTA's TMA bytes landed
@@ -496,8 +534,20 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   // converters start while the (3x larger) B stage is still in flight;
   // `full` then covers B only
   uint64_t* fulla = bars + 2 * S + 2 * ST + 4;  // S
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2 * ST + 4);
+  // halo mode: a halo buffer landed / released by every converter warp
+  uint64_t* halo_full = bars + 3 * S + 2 * ST + 4;   // 2
+  uint64_t* halo_empty = bars + 3 * S + 2 * ST + 6;  // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2 * ST + 8);
   constexpr bool kSplitA = SPLIT3 && !PAIR;
+  // Halo mode (split converters, single CTA, stride-1 A): one TMA box per
+  // 32-channel chunk covers the tile's pixels plus the taps' halo; the K
+  // blocks run chunk-major (all taps of a chunk back to back) and the
+  // converters form each tap's shifted A rows from the halo while splitting
+  // them -- one A load per chunk instead of one per (tap, chunk).
+  const bool halo = kSplitA && !MC && a.halo;
+  // channel-halves conversion (two groups per stage) needs exactly two groups
+  // (two alternating groups need even rings: an odd ring converts by halves)
+  const bool halves_on = SPLIT3 && C::kConvGroups == 2 && (a.conv_halves != 0 || (S & 1) || (ST & 1));
 
   // Role of each warp.  An SM sub-partition issues from its eligible warps
   // highest-warp-id first, so the single MMA-issuing thread sits in the
@@ -505,7 +555,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   // sharing it delay every tcgen05.mma); warps that read TMEM keep
   // (physical warp % 4) == their TMEM lane quarter.
   //   3xTF32 (16 warps): physical 0-7 converters, 8-11 epilogue, 12 TMEM
-  //   allocator, 13 relay, 14 TMA producer, 15 MMA;
+  //   allocator, 13 relay, 14 TMA producer, 15 MMA; 16-bit splits (20
+  //   warps): 0-11 converters, 12-15 epilogue, 16-19 as 12-15;
   //   1xTF32 (8 warps): physical 5 MMA, 1 epilogue quarter 1, rest as logical.
   // (the warp index is shuffled from lane 0 so the compiler can prove it
   // warp-uniform: role branches are then uniform and the MMA warp's
@@ -516,8 +567,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
     a.trace[kTraceRoles * kTraceStages + 4 * blockIdx.x] = t;
   }
   const int hw = __shfl_sync(0xffffffffu, int(threadIdx.x / 32), 0), lane = int(threadIdx.x % 32);
-  const int warp = SPLIT3 ? (hw < 8 ? hw + 8 : hw < 12 ? hw - 4 : hw == 12 ? 2 : hw == 13 ? 3
-                                                                 : hw == 14 ? 0 : 1)
+  // (split modes, G = kConvGroups: physical 0 .. 4G-1 converters -> logical
+  // 8 .., the next four the epilogue, then allocator, relay, producer, MMA)
+  constexpr int G4 = 4 * C::kConvGroups;
+  const int warp = SPLIT3 ? (hw < G4 ? hw + 8 : hw < G4 + 4 ? hw - G4 + 4 : hw == G4 + 4 ? 2
+                                                : hw == G4 + 5 ? 3 : hw == G4 + 6 ? 0 : 1)
                           : (hw == 5 ? 1 : hw == 1 ? 5 : hw);
   const uint32_t rank = CLUSTER ? cluster_rank() : 0;
   constexpr int kCtas = PAIR ? 2 : 1;
@@ -525,7 +579,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
     for (int s = 0; s < ST; ++s) {
       // 3xTF32 / 3xBF16: one arrival per converter warp that converts the
       // stage (8 with conv_halves, else 4) per CTA; 1xTF32 pair: relay arrivals
-      mbar_init(&ready[s], kCtas * (SPLIT3 ? (a.conv_halves ? 8 : 4) : 1));
+      mbar_init(&ready[s], kCtas * (SPLIT3 ? (halves_on ? 8 : 4) : 1));
       mbar_init(&tfree[s], 1);
     }
     for (int s = 0; s < S; ++s) {
@@ -536,6 +590,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kCtas);
+      mbar_init(&halo_full[i], 1);
+      mbar_init(&halo_empty[i], G4);  // every converter warp releases every chunk
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -590,8 +646,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs: own A rows, own B rows)
-      int stage = 0, pit = 0;
+      int stage = 0, pit = 0, hidx = 0;
       uint32_t phase = 0;
+      const uint32_t halo_bytes = uint32_t(a.halo_w) * a.halo_h * a.BNI * 128;
       for (int u = unit0; u < num_units; u += ustep) {
         const Tile d = decode<CLUSTER>(a, u, int(rank));
         const int m = d.m, nt = d.nt;
@@ -600,22 +657,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         const int c_base = a.a_c_base + g * a.a_c_per_group;
         const int row = a.b_row_base + g * a.b_row_per_group + nn * BN + (PAIR ? int(rank) * C::kBRows : 0);
         const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
-        for (int kb = d.kb0; kb < d.kb1; ++kb) {
-          const int32_t tp = a.taps[d.ph][kb / a.a_cblocks];
-          const int cb = kb % a.a_cblocks;
-          const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
-          mbar_wait(&empty[stage], phase ^ 1);
-          trace(a, 0, pit++);
-          const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
-          if (kSplitA) {
-            mbar_expect_tx(&fulla[stage], ld_a ? a_box_bytes : 0u);
-            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &fulla[stage], c_base + cb * 32, aw, ah, n0);
-            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
-          } else {
-            mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
-                                             (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
-            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
-          }
+        const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
+        // B of K block (tap tp, chunk cb) into the stage
+        auto load_b = [&](int32_t tp, int cb) {
           const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
           if (MC) {
             // this CTA's half of the B rows, into both CTAs' stage buffers
@@ -631,6 +675,49 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             stage = 0;
             phase ^= 1;
           }
+        };
+        if (halo) {
+          // chunk-major K blocks (chunk cb, tap t): one halo box per chunk
+          const int ntp = a.ntaps[d.ph];
+          int cb = d.kb0 / ntp, t = d.kb0 - cb * ntp;
+          for (int kb = d.kb0; kb < d.kb1; ++kb) {
+            if (kb == d.kb0 || t == 0) {
+              const int hbuf = hidx & 1;
+              mbar_wait(&halo_empty[hbuf], ((hidx >> 1) & 1) ^ 1);
+              mbar_expect_tx(&halo_full[hbuf], ld_a ? halo_bytes : 0u);
+              if (ld_a)
+                tma_load_4d(halo_buf(hbuf), &mapA, &halo_full[hbuf], c_base + cb * 32,
+                            w0 + a.halo_dw0[d.ph], h0 + a.halo_dh0[d.ph], n0);
+              ++hidx;
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            trace(a, 0, pit++);
+            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
+            load_b(a.taps[d.ph][t], cb);
+            if (++t == ntp) {
+              t = 0;
+              ++cb;
+            }
+          }
+          continue;
+        }
+        for (int kb = d.kb0; kb < d.kb1; ++kb) {
+          // tap-major K blocks (tap kb / cblocks, chunk kb % cblocks)
+          const int32_t tp = a.taps[d.ph][kb / a.a_cblocks];
+          const int cb = kb % a.a_cblocks;
+          const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
+          mbar_wait(&empty[stage], phase ^ 1);
+          trace(a, 0, pit++);
+          if (kSplitA) {
+            mbar_expect_tx(&fulla[stage], ld_a ? a_box_bytes : 0u);
+            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &fulla[stage], c_base + cb * 32, aw, ah, n0);
+            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
+          } else {
+            mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
+                                             (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
+            if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
+          }
+          load_b(tp, cb);
         }
       }
     }
@@ -1126,30 +1213,77 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
     const int cg = (warp - 8) >> 2;
     const int ct = ((warp - 8) & 3) * 32 + lane;  // 0..127 == TMEM lane
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const bool halves = a.conv_halves != 0;
-    int it = 0, stage = 0, tslot = 0;  // K blocks seen by this CTA (both groups count all)
+    const bool halves = halves_on;
+    int rot = 0;  // the group whose turn the current stage is (alternating groups)
+    int it = 0, stage = 0, tslot = 0;  // K blocks seen by this CTA (all groups count all)
     uint32_t phase = 0, tph = 0;
     constexpr bool f16 = F16;
+    // halo mode: chunks started (every warp counts every chunk), whether this
+    // warp waited for the current one; this row's pixel in the tile
+    int hcnt = 0;
+    bool hwaited = false;
+    const int tile_px = a.BW * a.BH;
+    const int r_ni = ct / tile_px, r_hi = (ct % tile_px) / a.BW, r_wi = ct % a.BW;
+    const bool r_ok = r_ni < a.BNI;
     for (int u = unit0; u < num_units; u += ustep) {
       const Tile d = decode<CLUSTER>(a, u, int(rank));
+      const int ntp = a.ntaps[d.ph];
+      const int hdh0 = a.halo_dh0[d.ph], hdw0 = a.halo_dw0[d.ph];
       // fp16 split: this row's image scale (rows past the batch keep 1)
       float sA = 1.f;
       if (f16 && a.a_amax) {
         const int ni = ct / (a.BW * a.BH), n = (d.m / (a.tiles_w * a.tiles_h)) * a.BNI + ni;
         if (d.m < a.m_tiles && ni < a.BNI && n < a.nimg) sA = pow2f(amax_shift(a.a_amax[n]));
       }
+      // halo mode: the tap of K block kb (chunk-major), advanced incrementally
+      int htap = halo ? d.kb0 % ntp : 0;
+      int32_t htp = a.taps[d.ph][htap];
       for (int kb = d.kb0; kb < d.kb1; ++kb, ++it) {
-        if (halves || (it & 1) == cg) {
+        if (halo && (kb == d.kb0 || htap == 0)) {
+          // a new chunk: this warp is done reading the previous one
+          if (hcnt > 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&halo_empty[(hcnt - 1) & 1]);
+          }
+          ++hcnt;
+          // every warp waits for every chunk (also those it converts no stage
+          // of), so it never runs a full phase ahead of the halo barriers
+          mbar_wait(&halo_full[(hcnt - 1) & 1], uint32_t((hcnt - 1) >> 1) & 1u);
+          hwaited = true;
+        }
+        if (halves || rot == cg) {
           if (ct == 0 && cg == 0) trace(a, 7, it);
           if (PAIR) {
             mbar_wait(&full[stage], phase);
             mbar_wait_cluster(&tfree[tslot], tph ^ 1);  // the slot's previous MMAs are done
+          } else if (halo) {
+            if (!hwaited) {
+              mbar_wait2(&halo_full[(hcnt - 1) & 1], uint32_t((hcnt - 1) >> 1) & 1u, &tfree[tslot],
+                         tph ^ 1);
+              hwaited = true;
+            } else {
+              mbar_wait(&tfree[tslot], tph ^ 1);
+            }
           } else {
             mbar_wait2(kSplitA ? &fulla[stage] : &full[stage], phase, &tfree[tslot], tph ^ 1);
           }
           if (ct == 0) trace(a, cg ? 5 : 1, it);
           if (!(a.debug & 32)) {  // (debug 32: no conversion work; experiments)
-            const uint32_t row = smem_u32(a_hi(stage) + ct * 128);
+            // this row's 128-byte A row: the stage's row ct, or in halo mode
+            // the halo pixel the tap shifts row ct onto (rows past the box read
+            // pixel 0 and are zeroed); 16-byte chunk c sits at c ^ (pixel & 7)
+            int px = ct;
+            uint8_t* abase = a_hi(stage);
+            if (halo) {
+              px = r_ok ? (r_ni * a.halo_h + r_hi + tap_dh(htp) - hdh0) * a.halo_w + r_wi +
+                              tap_dw(htp) - hdw0
+                        : 0;
+              abase = halo_buf((hcnt - 1) & 1);
+              if (a.debug & 1024) px = ct;  // (experiment: the stage's row pattern)
+            }
+            const bool zrow = halo && !r_ok;
+            const uint32_t row = smem_u32(abase + px * 128);
+            const int sw = px & 7;
             const uint32_t ta = tmem_base + lane_base + uint32_t(C::kAcol0 + tslot * C::kAslot);
             if (BF) {
               uint32_t hi[16], lo[16];
@@ -1161,19 +1295,27 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
                 if (c < nc)
                   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                                : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
-                               : "r"(row + uint32_t(((c0 + c) ^ (ct & 7)) << 4)));
+                               : "r"(row + uint32_t(((c0 + c) ^ sw) << 4)));
+              if (zrow)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) xs[c] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 if (c >= nc) break;
                 if (f16) {
-                  split_f16x2(xs[c].x, xs[c].y, sA, sA * 8193.0f, hi[2 * c], lo[2 * c]);
-                  split_f16x2(xs[c].z, xs[c].w, sA, sA * 8193.0f, hi[2 * c + 1], lo[2 * c + 1]);
+                  split_f16x2(xs[c].x, xs[c].y, sA, hi[2 * c], lo[2 * c]);
+                  split_f16x2(xs[c].z, xs[c].w, sA, hi[2 * c + 1], lo[2 * c + 1]);
                 } else {
                   split_bf16x2(xs[c].x, xs[c].y, hi[2 * c], lo[2 * c]);
                   split_bf16x2(xs[c].z, xs[c].w, hi[2 * c + 1], lo[2 * c + 1]);
                 }
               }
-              if (halves) {
+              if (a.debug & 512) {  // (experiment: no TMEM stores)
+                uint32_t z = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) z ^= hi[i] ^ lo[i];
+                asm volatile("" ::"r"(z));
+              } else if (halves) {
                 tmem_st8(ta + 8 * cg, hi);
                 tmem_st8(ta + 16 + 8 * cg, lo);
               } else {
@@ -1187,7 +1329,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
               for (int c = 0; c < 4; ++c)
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
-                             : "r"(row + uint32_t(((4 * cg + c) ^ (ct & 7)) << 4)));
+                             : "r"(row + uint32_t(((4 * cg + c) ^ sw) << 4)));
+              if (zrow)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) xs[c] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const uint4 x = xs[c];
@@ -1205,7 +1350,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
               for (int c = 0; c < 8; ++c)
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(xs[c].x), "=r"(xs[c].y), "=r"(xs[c].z), "=r"(xs[c].w)
-                             : "r"(row + uint32_t((c ^ (ct & 7)) << 4)));
+                             : "r"(row + uint32_t((c ^ sw) << 4)));
+              if (zrow)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) xs[c] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 const uint4 x = xs[c];
@@ -1238,6 +1386,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         if (++tslot == ST) {
           tslot = 0;
           tph ^= 1;
+        }
+        if (++rot == C::kConvGroups) rot = 0;
+        if (halo) {
+          if (++htap == ntp) htap = 0;
+          htp = a.taps[d.ph][htap];
         }
       }
     }
@@ -1356,7 +1509,24 @@ cudaError_t launch_t(const TcLaunch& L, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, SPLIT3, CL, KWF, H16>, L.mapA, L.mapBh, L.mapBl, a);
 }
 
+template <int BN, bool KWF, bool BF>
+int halo_cap_t() {
+  return Cfg<BN, true, false, KWF, BF>::halo_cap();
+}
+
 }  // namespace
+
+int halo_capacity(const TcLaunch& L) {
+  if (!L.split3 || L.pair || L.mc) return 0;
+  if (L.kwf) return L.bn == 64 ? (L.bf ? halo_cap_t<64, true, true>() : halo_cap_t<64, true, false>()) : 0;
+  switch (L.bn) {
+    case 32: return L.bf ? halo_cap_t<32, false, true>() : halo_cap_t<32, false, false>();
+    case 64: return L.bf ? halo_cap_t<64, false, true>() : halo_cap_t<64, false, false>();
+    case 128: return L.bf ? halo_cap_t<128, false, true>() : halo_cap_t<128, false, false>();
+    case 256: return L.bf ? 0 : halo_cap_t<256, false, false>();
+  }
+  return 0;
+}
 
 bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a) {
   a.OH = OH;
@@ -1378,7 +1548,11 @@ bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a) {
 bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const void* Bhi,
                const void* Blo, int BK, int Brows) {
   const TcArgs& a = L.args;
-  if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) return false;
+  if (a.halo) {  // one halo box per chunk: halo_w x halo_h pixels, unit element stride
+    if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.halo_w, a.halo_h, a.BNI, 1)) return false;
+  } else if (!make_map_4d(&L.mapA, A, AC, AW, AH, AN, a.BW, a.BH, a.BNI, a.S)) {
+    return false;
+  }
   // a pair stages half of B per CTA; a multicast cluster loads half per CTA
   const int nm = L.kwf ? 3 * L.bn : L.bn;  // MMA N (B rows of a stage)
   const int box_rows = (L.pair || L.mc) ? nm / 2 : nm;

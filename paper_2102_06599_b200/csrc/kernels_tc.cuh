@@ -81,6 +81,11 @@ struct TcArgs {
   // Powers of two: the scaled products and sums are the unscaled ones
   // exactly, outside fp16 subnormals.
   int h16_f16;
+  // halo mode (split converters, single CTA, S == 1; kernels_tc.cu): the A
+  // map's box is halo_w x halo_h pixels (x BNI images) at the tile origin
+  // plus (halo_dw0, halo_dh0)[phase], the smallest tap offsets of the phase
+  int halo, halo_w, halo_h;
+  int halo_dh0[kMaxPhases], halo_dw0[kMaxPhases];
   const uint32_t* a_amax;
   float b_inv;
   // per-image max |value| of what this launch writes for the next GEMM
@@ -123,6 +128,8 @@ bool plan_tiles(int OH, int OW, int nimg, int S, TcArgs& a);
 bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, const void* Bhi,
                const void* Blo, int BK, int Brows);
 cudaError_t launch(const TcLaunch& L, cudaStream_t st);
+// Halo buffer bytes the kernel configuration of L offers (0: no halo mode)
+int halo_capacity(const TcLaunch& L);
 
 }  // namespace tc
 }  // namespace nb

@@ -8,7 +8,7 @@ Stated tolerances, per arithmetic mode:
     per layer 1e-4, per channel 1e-4 of the largest layer; loss 1e-6.
   NB_PREC_FP32  3xTF32 on the tensor cores (hi/lo split products, fp32
     accumulation inside tcgen05.mma, measured rms 4e-7..9e-7 of sum|w||x| for
-    K = 576..4608 vs 3e-8 for SIMT -- scripts/precision_probe.py):
+    K = 576..4608 vs 3e-8 for SIMT -- scripts/experiments/precision_probe.py):
     conv outputs 1e-5 * sum|w||x|; Fisher totals 5e-4 (measured 1.3e-5 on
     10 layers, 1.0e-4 on the 33-layer R34 chain), per layer 5e-3, per channel
     5e-3 of the largest layer; loss 1e-6.
