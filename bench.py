@@ -19,6 +19,7 @@ Prints one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -362,6 +363,11 @@ def main():
             dist.barrier()
 
     def timed_region(fn):
+        # (Python's cyclic GC is collected before and held off inside, as
+        # timeit does: a gen-2 pass over torch's heap costs ~40 ms of host
+        # time that is not the product's)
+        gc.collect()
+        gc.disable()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -371,6 +377,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms = e0.elapsed_time(e1)
+        gc.enable()
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -411,22 +418,25 @@ def main():
     lab = torch.from_numpy(batch.labels).pin_memory()
     hbatch = nb.Batch(xin.numpy(), lab.numpy(), batch.seed)
 
+    # the e2e run gets the timed run's starting state on its own contexts:
+    # fresh caches warmed by the same warm-up pool and origin evaluation (a
+    # cache cleared in place does not return to that state: its device
+    # z-streams and slab refill differently), then new sessions from the
+    # host batch inside the timed region
+    ectxs = [nb.Context(local) for _ in range(args.streams)]
+
     def e2e(pool=mine):
-        ss = [nb.Session(origin, hbatch, ctx=c) for c in ctxs]
+        ss = [nb.Session(origin, hbatch, ctx=c) for c in ectxs]
         r = nb.evaluate(ss, pool, prec)
         for s in ss:
             s.close()
         return r
 
-    # untimed warm-up of the e2e path on the warm-up pool (session buffers
-    # come from the contexts' pools), then the same cache state as the
-    # timed run: the warm-up's and the origin's packed layers
-    e2e(warm_pool)
-    for c in ctxs:
-        c.clear_caches()
-    nb.evaluate(sessions, warm_pool, prec)
-    for s in sessions:  # the origin's full z-streams, as in the first warm-up
+    wsess = [nb.Session(origin, batch, ctx=c) for c in ectxs]
+    nb.evaluate(wsess, warm_pool, prec)
+    for s in wsess:
         s.fisher(origin, prec)
+        s.close()
     e2e_ms, _ = timed_region(e2e)
     e2e_val = total_units / (e2e_ms / 1e3)
     h2d = (batch.inputs.nbytes + batch.labels.nbytes) * len(ctxs) / args.steps

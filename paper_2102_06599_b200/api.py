@@ -17,7 +17,9 @@ from __future__ import annotations
 import os
 
 import ctypes as C
+import sys
 import threading
+import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -675,6 +677,7 @@ def evaluate(sessions: Sequence[Session], nets: Sequence[Network],
     """The candidate scheduler (evaluate_all, I/search.hpp:315-334): scores
     every network (init_weights draws) across the sessions' GPUs.  Returns
     (reports, EvalStats); reports[i] belongs to nets[i]."""
+    _t0 = time.perf_counter()
     holders = [n.c_struct() for n in nets]
     for n in nets:
         if n.weights is not None:
@@ -688,8 +691,13 @@ def evaluate(sessions: Sequence[Session], nets: Sequence[Network],
     done = np.zeros(len(sessions), np.int64)
     st = abi.EvalStatsC(0, 0, 0, 0, 0, _dp(est), _dp(busy),
                         done.ctypes.data_as(C.POINTER(C.c_int64)))
+    _t1 = time.perf_counter()
     _check(abi.load().nb_evaluate(sp, len(sessions), arr, len(nets), precision, outs,
                                   C.byref(st)))
+    _t2 = time.perf_counter()
     reps = [_report(n, outs[i], b[1], b[2], b[3]) for i, (n, b) in enumerate(zip(nets, bufs))]
+    if os.environ.get("NB_EVAL_LOG"):  # (experiments: host time around the C call)
+        print(f"evaluate: prepare {1e3 * (_t1 - _t0):.1f} ms, nb_evaluate {1e3 * (_t2 - _t1):.1f} ms, "
+              f"reports {1e3 * (time.perf_counter() - _t2):.1f} ms", file=sys.stderr, flush=True)
     return reps, EvalStats(st.evaluated, st.deduplicated, est.tolist(), busy.tolist(),
                            done.tolist(), st.requeued, st.failed_sessions)

@@ -24,6 +24,8 @@ void cuda_check(cudaError_t e, const char* what) {
 
 void DevBuf::ensure(size_t n) {
   if (n <= bytes) return;
+  // grow by at least half (a reallocation synchronizes the whole device)
+  n = std::max(n, bytes + bytes / 2);
   if (p) {
     NB_CUDA(cudaDeviceSynchronize());
     NB_CUDA(cudaFree(p));
@@ -359,6 +361,7 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
     if (int(rs.size()) > kMaxRanges)
       fail(NB_ERR_UNSUPPORTED, "more than 16 channel ranges in one layer");
     g.nranges = int(rs.size());
+    lp.tcf.resize(size_t(g.nranges));
     int64_t off = 0;
     const int taps = int(s.kh * s.kw);
     for (int i = 0; i < g.nranges; ++i) {
@@ -1002,8 +1005,29 @@ const float* session_xcol(nb_ctx* c, nb_session* s, const ConvGeom& g, cudaStrea
   return s->xcol->as<float>();
 }
 
+// Sizes the context's run buffers for plan P over N examples (grow-only; a
+// growth synchronizes the device, so nb_evaluate reserves for every
+// candidate of a call before any runs).
+void reserve_run(nb_ctx* c, const NetPlan& P, int64_t N, int64_t K, int64_t L, bool want_grads,
+                 bool explicit_w) {
+  c->act.ensure(size_t(P.act_total) * 4);
+  if (explicit_w) c->wpack.ensure(size_t(P.w_total) * 4);
+  c->part.ensure(size_t(P.part_total) * 8);
+  if (P.ws_floats) c->ws.ensure(size_t(P.ws_floats) * 4);
+  c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
+  c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
+  if (want_grads) c->gtmp.ensure(size_t(P.act_total) * 4);
+  // misc: probs N*K | ex_loss N | per_channel sum C | fisher table L
+  c->misc.ensure(size_t(align64(N * K) + align64(N) + align64(P.ch_total) +
+                        align64(int64_t(L) * int64_t(sizeof(FisherLayer)) / 8 + 1)) *
+                 8);
+  if (P.h16 == 2) c->amax.ensure(size_t(2 * L * N) * 4);
+  c->host_io.ensure(size_t(L) * sizeof(FisherLayer));
+  c->host_out.ensure(size_t(N * K + N + P.ch_total) * 8);
+}
+
 void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
-                 bool backward, const RunOut& out, Pending& pend) {
+                 bool backward, const RunOut& out, Pending& pend, NetPlan* pre) {
   nb_ctx* c = s->ctx;
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   ctx_activate(c);
@@ -1023,22 +1047,15 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
     c->prof.host(name, std::chrono::duration<double, std::milli>(now - tp).count());
     tp = now;
   };
-  NetPlan P = lower(net, N, prec, c->num_sms, out.grad_n > 0 ? out.grad_n : N, true);
+  // (a plan lowered ahead by the scheduler for this batch size and GPU)
+  NetPlan own;
+  if (!pre) own = lower(net, N, prec, c->num_sms, out.grad_n > 0 ? out.grad_n : N, true);
+  NetPlan& P = pre ? *pre : own;
   const bool want_grads = out.grads != nullptr;
   phase("host_lower");
 
-  c->act.ensure(size_t(P.act_total) * 4);
   const bool explicit_w = w && w->layer;
-  if (explicit_w) c->wpack.ensure(size_t(P.w_total) * 4);
-  c->part.ensure(size_t(P.part_total) * 8);
-  if (P.ws_floats) c->ws.ensure(size_t(P.ws_floats) * 4);
-  c->dpre[0].ensure(size_t(P.dpre_floats) * 4);
-  c->dpre[1].ensure(size_t(P.dpre_floats) * 4);
-  if (want_grads) c->gtmp.ensure(size_t(P.act_total) * 4);
-  // misc: probs N*K | ex_loss N | per_channel sum C | fisher table L
-  const int64_t misc_doubles = align64(N * K) + align64(N) + align64(P.ch_total) +
-                               align64(int64_t(L) * int64_t(sizeof(FisherLayer)) / 8 + 1);
-  c->misc.ensure(size_t(misc_doubles) * 8);
+  reserve_run(c, P, N, K, L, want_grads, explicit_w);
   double* d_probs = c->misc.as<double>();
   double* d_exloss = d_probs + align64(N * K);
   double* d_perch = d_exloss + align64(N);
@@ -1131,7 +1148,6 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
   uint32_t* dpre_amax = nullptr;
   const uint32_t* x_amax = nullptr;
   if (P.h16 == 2) {
-    c->amax.ensure(size_t(2 * L * N) * 4);
     NB_CUDA(cudaMemsetAsync(c->amax.p, 0, size_t(2 * L * N) * 4, st));
     act_amax = c->amax.as<uint32_t>();
     dpre_amax = act_amax + L * N;
@@ -1192,7 +1208,6 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
       cur ^= 1;
     }
     // ---- Fisher reduction (I/nnet.hpp:330-350)
-    c->host_io.ensure(size_t(L) * sizeof(FisherLayer));
     FisherLayer* ht = c->host_io.as<FisherLayer>();
     int64_t off = 0;
     int max_c = 1;
@@ -1213,8 +1228,6 @@ void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
 
   phase("host_launch");
   // ---- results back to the host (pinned staging; completed by run_finish)
-  const int64_t stage_doubles = N * K + N + P.ch_total;
-  c->host_out.ensure(size_t(stage_doubles) * 8);
   double* h_probs = c->host_out.as<double>();
   double* h_exl = h_probs + N * K;
   double* h_perch = h_exl + N;

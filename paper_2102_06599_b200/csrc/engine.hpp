@@ -75,7 +75,9 @@ struct TcPlan {
 struct LayerPlan {
   ConvGeom geom{};
   Family family[kMaxRanges]{};
-  TcPlan tcf[kMaxRanges];    // fprop tensor-core plans (family == TensorCore)
+  // fprop tensor-core plans of ranges 0 .. nranges-1 (family == TensorCore);
+  // sized per layer (a plan is lowered per candidate and copied around)
+  std::vector<TcPlan> tcf;
   Family dgrad_family = Family::Direct;
   TcPlan tcd;                // dgrad tensor-core plan
   int64_t wpack_floats = 0;  // floats of all packings of this layer
@@ -228,8 +230,13 @@ struct Pending {
 // on the session's resident batch: run_enqueue issues every kernel and the
 // result copies asynchronously on the session's stream, run_finish waits for
 // them and fills `out`.  One evaluation per session may be in flight.
+// `pre`: the network's plan lowered ahead for this session's batch size and
+// GPU (nb_evaluate), used and updated in place; null = lower here.
 void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
-                 bool backward, const RunOut& out, Pending& pend);
+                 bool backward, const RunOut& out, Pending& pend, NetPlan* pre = nullptr);
+// Sizes a context's run buffers for plan P (grow-only).
+void reserve_run(nb_ctx* c, const NetPlan& P, int64_t N, int64_t K, int64_t L, bool want_grads,
+                 bool explicit_w);
 void run_finish(Pending& pend);
 // The evaluation's kernels and result copies have completed on the device
 // (run_finish will not block).

@@ -123,7 +123,40 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
       if (std::find(devs.begin(), devs.end(), sessions[k]->ctx->device) == devs.end())
         devs.push_back(sessions[k]->ctx->device);
 
+    // Every session's run buffers sized for the largest distinct network
+    // before any evaluation starts: a buffer grown mid-call reallocates, and
+    // a reallocation synchronizes the whole device (stalling every stream).
+    {
+      const int64_t L0 = uniq.empty() ? 0 : descs[uniq[0]].L();
+      NetPlan need;
+      int64_t maxL = L0, maxK = 1;
+      bool h16 = false;
+      for (size_t u = 0; u < uniq.size(); ++u) {
+        const NetDesc& d = descs[uniq[u]];
+        const NetPlan P = lower(d, N, prec, sessions[0]->ctx->num_sms, N, true);
+        need.act_total = std::max(need.act_total, P.act_total);
+        need.part_total = std::max(need.part_total, P.part_total);
+        need.ws_floats = std::max(need.ws_floats, P.ws_floats);
+        need.dpre_floats = std::max(need.dpre_floats, P.dpre_floats);
+        need.ch_total = std::max(need.ch_total, P.ch_total);
+        maxL = std::max(maxL, d.L());
+        maxK = std::max(maxK, d.num_classes);
+        h16 = h16 || P.h16 == 2;
+      }
+      need.h16 = h16 ? 2 : 0;
+      if (!uniq.empty())
+        for (int32_t k = 0; k < num_sessions; ++k) {
+          nb_ctx* c = sessions[k]->ctx;
+          std::lock_guard<std::recursive_mutex> lk(c->mu);
+          ctx_activate(c);
+          reserve_run(c, need, N, maxK, maxL, false, false);
+        }
+    }
+
     const size_t S = size_t(num_sessions);
+    // NB_SCHED_LOG: per-evaluation enqueue / completion times (experiments)
+    static const bool sched_log = std::getenv("NB_SCHED_LOG") != nullptr;
+    const auto t_call = std::chrono::steady_clock::now();
     std::vector<double> busy(S, 0.0), est(S, 0.0);
     std::vector<int64_t> done(S, 0);
     std::mutex mu;  // guards queue, outstanding, alive, fatal, requeued
@@ -174,6 +207,11 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
             try {
               run_finish(pend[j]);
               busy[size_t(k)] += run_device_ms(sessions[k]->ctx);
+              if (sched_log)
+                std::fprintf(stderr, "sched s%d done at %.3f ms (device %.3f ms)\n", k,
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t_call).count(),
+                             run_device_ms(sessions[k]->ctx));
               ++done[size_t(k)];
               std::lock_guard<std::mutex> lk(mu);
               --outstanding;
@@ -203,7 +241,13 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
             ro.total = &r.total;
             ro.loss = &r.loss;
             ro.probs = r.probs.data();
+            const auto te0 = std::chrono::steady_clock::now();
             run_enqueue(sessions[k], descs[uniq[u]], nullptr, prec, true, ro, pend[j]);
+            if (sched_log)
+              std::fprintf(stderr, "sched s%d enq u%zu at %.3f ms (%.3f ms)\n", k, u,
+                           std::chrono::duration<double, std::milli>(te0 - t_call).count(),
+                           std::chrono::duration<double, std::milli>(
+                               std::chrono::steady_clock::now() - te0).count());
             est[size_t(k)] += cost[u];
             busy_slots = true;
             progress = true;
