@@ -13,6 +13,8 @@ of the pool through the product's scheduler (nb_evaluate: --streams
 concurrent sessions per GPU), weak scaling, no collective on the data path.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nb200|reference]
+                  [--single-process]   (one process driving all N GPUs through
+                                        nb_evaluate instead of torchrun ranks)
 
 Prints one JSON line on rank 0.
 """
@@ -69,6 +71,9 @@ TOL_NOTE = {"fp32_" + SPLIT: "Fisher totals <= 5e-4, per layer <= 5e-3 relative 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--single-process", action="store_true",
+                   help="drive all --gpus GPUs from this one process through the scheduler "
+                        "(nb_evaluate's per-GPU workers) instead of one rank per GPU")
     p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=8)
     p.add_argument("--impl", default="nb200", choices=["nb200", "reference"])
@@ -345,16 +350,21 @@ def main():
 
     # warm-up networks and the timed pool are disjoint; the timed pool is
     # K per rank, LPT-sharded over the ranks by estimated FLOPs
-    origin_j, warm_j, timed_j, _ = timed_pool(args.steps, args.warmup, world)
+    # single-process multi-GPU: one rank drives every GPU (sessions on each)
+    devs = list(range(args.gpus)) if (args.single_process and world == 1) else [local]
+    ngpu = world * len(devs)
+    origin_j, warm_j, timed_j, _ = timed_pool(args.steps, args.warmup, ngpu)
     origin = nb.Network.from_json(origin_j)
     warm_pool = [nb.Network.from_json(n) for n in warm_j]
     timed = [nb.Network.from_json(n) for n in timed_j]
     costs = [nb.fisher_flops(n, N_BATCH) for n in timed]
-    assign = shard_lpt(costs, world, args.steps)
+    # (a single process driving several GPUs takes them all: nb_evaluate's
+    # dynamic queue balances them over its per-GPU workers)
+    assign = shard_lpt(costs, world, args.steps * len(devs))
     mine = [n for n, a in zip(timed, assign) if a == rank]
 
     batch = nb.make_batch(origin, N_BATCH, 1)
-    ctxs = [nb.Context(local) for _ in range(args.streams)]
+    ctxs = [nb.Context(d) for d in devs for _ in range(args.streams)]
     sessions = [nb.Session(origin, batch, ctx=c) for c in ctxs]
     stream = torch.cuda.current_stream()
 
@@ -408,7 +418,7 @@ def main():
             a = kstats.setdefault(k, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
             for f in a:
                 a[f] += v[f]
-    total_units = args.steps * world
+    total_units = args.steps * ngpu
     value = total_units / (ms / 1e3)
 
     # ---- e2e: the reference-facing call with HOST buffers: sessions built
@@ -423,7 +433,7 @@ def main():
     # cache cleared in place does not return to that state: its device
     # z-streams and slab refill differently), then new sessions from the
     # host batch inside the timed region
-    ectxs = [nb.Context(local) for _ in range(args.streams)]
+    ectxs = [nb.Context(d) for d in devs for _ in range(args.streams)]
 
     def e2e(pool=mine):
         ss = [nb.Session(origin, hbatch, ctx=c) for c in ectxs]
@@ -531,9 +541,11 @@ def main():
                            "dtype": DTYPE[name], "tolerance": TOL_NOTE[name]}
 
     if rank == 0:
-        cfg = config_block(args.steps, args.streams, world)
+        cfg = config_block(args.steps, args.streams, ngpu)
+        if len(devs) > 1:
+            cfg["parallelism"] += ", one process driving every GPU"
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ngpu,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": DTYPE[MODE_KEY[args.precision]], "data": "synthetic",

@@ -30,6 +30,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
+#include <cstring>
+#include <unordered_map>
 
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
@@ -1434,6 +1436,49 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled through a per-thread memo: a search re-launches the
+// same layer shapes over the same arena / packed-weight pointers, so most of
+// the ~200 encodes of an evaluation repeat (a lookup costs a hash of the
+// ~120-byte parameter block instead of a driver call).
+CUresult encode_cached(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* base,
+                       const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                       const cuuint32_t* es, CUtensorMapSwizzle sw,
+                       CUtensorMapL2promotion l2) {
+  struct Key {
+    uint64_t w[20];
+    bool operator==(const Key& o) const { return std::memcmp(w, o.w, sizeof(w)) == 0; }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      uint64_t h = 1469598103934665603ull;
+      for (uint64_t v : k.w) h = (h ^ v) * 1099511628211ull;
+      return size_t(h);
+    }
+  };
+  Key k{};
+  k.w[0] = uint64_t(dt) | (uint64_t(rank) << 8) | (uint64_t(sw) << 16) | (uint64_t(l2) << 24);
+  k.w[1] = reinterpret_cast<uint64_t>(base);
+  for (cuuint32_t i = 0; i < rank; ++i) {
+    k.w[2 + i] = dims[i];
+    k.w[7 + i] = i + 1 < rank ? strides[i] : 0;
+    k.w[12 + i] = uint64_t(box[i]) | (uint64_t(es[i]) << 32);
+  }
+  thread_local std::unordered_map<Key, CUtensorMap, Hash> memo;
+  auto it = memo.find(k);
+  if (it != memo.end()) {
+    *m = it->second;
+    return CUDA_SUCCESS;
+  }
+  const CUresult r = encode_fn()(m, dt, rank, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS) {
+    if (memo.size() > 8192) memo.clear();
+    memo.emplace(k, *m);
+  }
+  return r;
+}
+
 bool make_map_4d(CUtensorMap* m, const float* base, int C, int W, int H, int N, int boxW,
                  int boxH, int boxN, int stride) {
   cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
@@ -1441,10 +1486,9 @@ bool make_map_4d(CUtensorMap* m, const float* base, int C, int W, int H, int N, 
   cuuint32_t box[4] = {32, cuuint32_t(boxW * stride), cuuint32_t(boxH * stride),
                        cuuint32_t(boxN)};
   cuuint32_t es[4] = {1, cuuint32_t(stride), cuuint32_t(stride), 1};
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode_cached(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
+                             strides, box, es, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
   return r == CUDA_SUCCESS;
 }
 
@@ -1456,12 +1500,11 @@ bool make_map_2d(CUtensorMap* m, const void* base, int K, int rows, int box_rows
   cuuint64_t strides[1] = {cuuint64_t(K) * (bf ? 2 : 4)};
   cuuint32_t box[2] = {32, cuuint32_t(box_rows)};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(m, bf ? (f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16)
-                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                           2, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode_cached(
+      m, bf ? (f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16)
+            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+      2, const_cast<void*>(base), dims, strides, box, es,
+      bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   return r == CUDA_SUCCESS;
 }
 
