@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -1038,9 +1039,123 @@ bool grouped_smem_ok(const ConvGeom& g, const RangeDesc& r) {
   return size_t(IH) * IW * cic * 4 <= 96 * 1024;
 }
 
+// Depthwise 3x3 stride-1 pad-1 fprop as a register sliding window (NHWC,
+// channel pairs): thread (pair, column) walks a strip of kDwStrip output
+// rows keeping its 3x3 window in registers; each step prefetches the next
+// input row's three pairs (the side columns are the neighbouring threads'
+// centres: L1 hits), runs 18 FMAs and stores one output pair (coalesced
+// across the pairs).  Pairs rather than quads keep the state at ~60
+// registers, so four 256-thread blocks share an SM: the strip loops need
+// warps, not barriers, to keep DRAM busy.  DRAM sees each input and output
+// once (plus the strips' halo rows).
+constexpr int kDwStrip = 16;
+
+// V = channels per thread (1 or 2): vector type and its lanes
+template <int V>
+struct DwVec;
+template <>
+struct DwVec<1> {
+  using T = float;
+  __device__ static float zero() { return 0.f; }
+  __device__ static float& at(float& v, int) { return v; }
+};
+template <>
+struct DwVec<2> {
+  using T = float2;
+  __device__ static float2 zero() { return make_float2(0.f, 0.f); }
+  __device__ static float& at(float2& v, int i) { return i ? v.y : v.x; }
+};
+
+template <int V>
+__global__ void __launch_bounds__(256, V == 1 ? 8 : 4)
+    k_dw3_nhwc(ConvGeom g, int ri, const float* __restrict__ x, const float* __restrict__ wbase,
+               float* __restrict__ y, bool relu) {
+  using DV = DwVec<V>;
+  using T = typename DV::T;
+  const RangeDesc r = g.r[ri];
+  const int np = r.len / V;
+  const int p = blockIdx.z * blockDim.x + threadIdx.x;  // channel group (range-local)
+  const int ow = blockIdx.x * blockDim.y + threadIdx.y;
+  const int strips = (g.OH + kDwStrip - 1) / kDwStrip;
+  const int64_t n = blockIdx.y / strips;
+  const int oh0 = int(blockIdx.y % strips) * kDwStrip, oh1 = min(g.OH, oh0 + kDwStrip);
+  if (p >= np || ow >= g.OW) return;
+  const int c = V * p;  // depthwise: input channel == range-local output channel
+  const float* __restrict__ wf = wbase + r.wf_off;  // Wf[tap][0][co]
+  T w[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) w[t] = __ldg(reinterpret_cast<const T*>(wf + int64_t(t) * r.len + c));
+  const int64_t row = int64_t(g.W) * g.Ci;
+  const float* __restrict__ xn = x + n * g.H * row + c;
+  auto ld = [&](int ih, int iw) {
+    return (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+               ? __ldg(reinterpret_cast<const T*>(xn + ih * row + int64_t(iw) * g.Ci))
+               : DV::zero();
+  };
+  T win[3][3];  // [input row - (oh - 1)][kw]
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int kw = 0; kw < 3; ++kw) win[i][kw] = ld(oh0 - 1 + i, ow - 1 + kw);
+  float* __restrict__ yp = y + (n * g.OH * g.OW + ow) * int64_t(g.Co) + r.b + c;
+  for (int oh = oh0; oh < oh1; ++oh) {
+    T nxt[3];  // the next step's input row, in flight while this one computes
+#pragma unroll
+    for (int kw = 0; kw < 3; ++kw) nxt[kw] = oh + 1 < oh1 ? ld(oh + 2, ow - 1 + kw) : DV::zero();
+    T a = DV::zero();
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+          DV::at(a, i) = fmaf(DV::at(win[kh][kw], i), DV::at(w[kh * 3 + kw], i), DV::at(a, i));
+    if (relu)
+#pragma unroll
+      for (int i = 0; i < V; ++i) DV::at(a, i) = DV::at(a, i) > 0.f ? DV::at(a, i) : 0.f;
+    *reinterpret_cast<T*>(yp + int64_t(oh) * g.OW * g.Co) = a;
+#pragma unroll
+    for (int kw = 0; kw < 3; ++kw) {
+      win[0][kw] = win[1][kw];
+      win[1][kw] = win[2][kw];
+      win[2][kw] = nxt[kw];
+    }
+  }
+}
+
+bool dw3_ok(const ConvGeom& g, const RangeDesc& r) {
+  static const bool on = [] {  // NB_DW3=0: the shared-memory halo kernel instead
+    const char* e = std::getenv("NB_DW3");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on && r.groups == r.len && r.slice_ci == 1 && r.slice_co == 1 && g.KH == 3 &&
+         g.KW == 3 && g.S == 1 && g.P == 1 && r.len % 4 == 0 && r.b % 4 == 0 && g.Ci % 4 == 0 &&
+         g.Co % 4 == 0 && (r.wf_off % 2) == 0;
+}
+
 void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const float* wbase,
                          float* y, bool relu, cudaStream_t st) {
   const RangeDesc& r = g.r[range];
+  if (dw3_ok(g, r)) {
+    // NB_DW3_V: channels per thread (2 default; 1 = one channel per thread,
+    // measured 2x slower: instruction-bound at 8 blocks / SM)
+    static const int V = [] {
+      const char* e = std::getenv("NB_DW3_V");
+      return e && std::atoi(e) == 1 ? 1 : 2;
+    }();
+    const int np = r.len / V;
+    const int tp = np < 32 ? np : 32, tw = std::max(1, std::min(256 / tp, g.OW));
+    dim3 block(tp, tw);
+    dim3 grid(unsigned((g.OW + tw - 1) / tw),
+              unsigned(int64_t(g.N) * ((g.OH + kDwStrip - 1) / kDwStrip)),
+              unsigned((np + tp - 1) / tp));
+    if (V == 2) {
+      k_dw3_nhwc<2><<<grid, block, 0, st>>>(g, range, x, wbase, y, relu);
+    } else {
+      k_dw3_nhwc<1><<<grid, block, 0, st>>>(g, range, x, wbase, y, relu);
+    }
+    return;
+  }
   if (grouped_smem_ok(g, r)) {
     const GTile T = gtile(g.OH, g.OW);
     const int tiles = ((g.OH + T.th - 1) / T.th) * ((g.OW + T.tw - 1) / T.tw);
