@@ -205,6 +205,13 @@ nb_status nb_conv_forward(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n,
 nb_status nb_conv_dgrad(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n,
                         const double* dy, const double* w, double* dx,
                         nb_precision prec);
+/* reference_conv restricted to the output rows [oh_lo, oh_hi) (the other
+ * rows of y are left undefined): one box of the masked box executor of
+ * nests with no ConvSpec (integration/nestopt_b200.hpp execute_boxes), the
+ * tensor-core tiles covering only the band.  No ReLU. */
+nb_status nb_conv_band(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* x,
+                       const double* w, int32_t oh_lo, int32_t oh_hi, double* y,
+                       nb_precision prec);
 
 /* ---- general loop nests (execute, I/interp.hpp:67-145) -------------------- */
 /* A transformed conv loop nest in executable form, for nests with no
@@ -251,6 +258,12 @@ typedef struct nb_nest {
  * or fp64).  is_int != 0: in/w/out are int64, else double. */
 nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int, const void* in,
                           const void* w, void* out);
+/* The masked box executor's cell pass over the same nest: per output cell
+ * (out_shape order), the smallest / largest input channel (index 0 of the
+ * statement's "I" access; INT32_MAX-ish / -1 when nothing adds into it) and
+ * the number of multiply-accumulate instances that add into it. */
+nb_status nb_nest_cells(nb_ctx* ctx, const nb_nest* nest, int32_t* ci_lo, int32_t* ci_hi,
+                        int64_t* count);
 
 /* ---- semantic legality (check_semantic_legality, I/transforms.hpp:598-663) */
 /* The brute-force dependence-preservation check of a semantic run (split /

@@ -28,6 +28,8 @@
 #include <memory>
 #include <mutex>
 #include <stdexcept>
+#include <tuple>
+#include <type_traits>
 #include <random>
 #include <sstream>
 #include <map>
@@ -52,6 +54,12 @@ struct DeviceError : std::runtime_error {
 // NB_ERR_UNSUPPORTED, or a nest the bridge cannot compile).  There is no
 // host fallback on the search path: the search fails loudly.
 struct LegalityUnsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// A nest the masked box executor cannot decompose into dense boxes
+// (execute_boxes); nb200::execute interprets any nest.
+struct BoxUnsupported : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -393,6 +401,132 @@ nestopt::Tensor<T> execute(Context& ctx, const nestopt::LoopNest& nest,
   NestProgram prog(nest, out_name, out.shape, ti.shape, tk.shape);
   check(nb_nest_execute(ctx.get(), prog.get(), std::is_integral<T>::value ? 1 : 0,
                         ti.data.data(), tk.data.data(), out.data.data()));
+  return out;
+}
+
+// ---- the masked box executor (SURVEY 7 "Non-ConvSpec nests", 8(f) #2) -------
+
+// What execute_boxes ran: the boxes (output channel range x output row band x
+// input channel range, every column and tap) and their MACs against the
+// nest's own instance count.
+struct BoxReport {
+  struct Box {
+    long long co_lo, co_hi, oh_lo, oh_hi, ci_lo, ci_hi;
+  };
+  std::vector<Box> boxes;
+  long long box_macs = 0, nest_macs = 0;
+};
+
+// execute<T> (I/interp.hpp:67-145) of a transformed conv nest -- one with
+// no ConvSpec such as the paper's Sequence 1 included -- as tensor-core
+// implicit GEMMs over boxes.  A GPU cell pass (nb_nest_cells) finds, per
+// output cell, the input-channel range and the number of MAC instances
+// adding into it.  Every covered cell must receive exactly its channel
+// range x every tap (a dense box row); cells with the same range over whole
+// output rows are grouped into (output-channel range x row band) boxes,
+// and each box runs as a conv over its channel slices restricted to its row
+// band (nb_conv_band: the tensor-core tiles cover only the band).  Cells no
+// instance writes stay zero, as in execute.  The arithmetic is the
+// requested precision tier's (FP32 default: exact for integer inputs whose
+// sums stay below 2^22, within the tier's tolerance otherwise); a nest that
+// does not decompose throws BoxUnsupported (nb200::execute interprets it).
+template <typename T>
+nestopt::Tensor<T> execute_boxes(Context& ctx, const nestopt::LoopNest& nest,
+                                 const nestopt::ExecEnv<T>& env,
+                                 nb_precision prec = NB_PREC_FP32, BoxReport* report = nullptr) {
+  using namespace nestopt;
+  if (!nest.provenance) throw UnboundTensor("output tensor 'O' is not bound");
+  std::string out_name;
+  for (const auto& part : nest.parts)
+    for (const auto& st : part.stmts)
+      for (const auto& acc : st.accesses)
+        if (acc.mode != AccessMode::Read) out_name = acc.tensor;
+  if (out_name.empty()) throw Error("nest has no written tensor");
+  const Tensor<T>& ti = env.bindings.at("I");
+  const Tensor<T>& tk = env.bindings.at("K");
+  const ConvSpec& ps = *nest.provenance;
+  Tensor<T> out(output_shape(ps));
+  NestProgram prog(nest, out_name, out.shape, ti.shape, tk.shape);
+  const long long Co = out.shape[0], OH = out.shape[1], OW = out.shape[2];
+  const long long Ci = ti.shape[0], H = ti.shape[1], W = ti.shape[2];
+  const long long taps = ps.kh * ps.kw;
+  const size_t cells = size_t(Co * OH * OW);
+  std::vector<int32_t> lo(cells), hi(cells);
+  std::vector<int64_t> cnt(cells);
+  check(nb_nest_cells(ctx.get(), prog.get(), lo.data(), hi.data(), cnt.data()));
+  long long nest_macs = 0;
+  for (size_t i = 0; i < cells; ++i) {
+    nest_macs += cnt[i];
+    if (cnt[i] && cnt[i] != (long long)(hi[i] - lo[i] + 1) * taps)
+      throw BoxUnsupported("execute_boxes: an output cell is not a dense channel-range box");
+  }
+  // (channel range, row band) -> the output channels computing it over whole rows
+  std::map<std::tuple<int, int, long long, long long>, std::vector<long long>> runs;
+  for (long long co = 0; co < Co; ++co) {
+    long long oh = 0;
+    while (oh < OH) {
+      const size_t c0 = size_t((co * OH + oh) * OW);
+      for (long long ow = 1; ow < OW; ++ow)
+        if ((cnt[c0 + size_t(ow)] != 0) != (cnt[c0] != 0) ||
+            (cnt[c0] && (lo[c0 + size_t(ow)] != lo[c0] || hi[c0 + size_t(ow)] != hi[c0])))
+          throw BoxUnsupported("execute_boxes: an output row mixes channel ranges");
+      if (!cnt[c0]) {
+        ++oh;
+        continue;
+      }
+      long long end = oh + 1;
+      while (end < OH) {
+        const size_t c1 = size_t((co * OH + end) * OW);
+        if (!cnt[c1] || lo[c1] != lo[c0] || hi[c1] != hi[c0]) break;
+        ++end;
+      }
+      runs[{lo[c0], hi[c0], oh, end}].push_back(co);
+      oh = end;
+    }
+  }
+  BoxReport rep;
+  rep.nest_macs = nest_macs;
+  for (auto& [key, cos] : runs) {
+    const auto [clo, chi, oh0, oh1] = key;
+    for (size_t i = 0; i < cos.size();) {
+      size_t j = i + 1;
+      while (j < cos.size() && cos[j] == cos[j - 1] + 1) ++j;
+      rep.boxes.push_back({cos[i], cos[j - 1] + 1, oh0, oh1, clo, chi + 1});
+      i = j;
+    }
+  }
+  for (const auto& b : rep.boxes) {
+    const long long nci = b.ci_hi - b.ci_lo, nco = b.co_hi - b.co_lo;
+    ConvSpec bs = ps;
+    bs.ci = nci;
+    bs.co = nco;
+    bs.groups = 1;
+    bs.bottleneck_out = 1;
+    bs.channel_splits.clear();
+    std::vector<double> xs(size_t(nci * H * W)), ws(size_t(nco * nci * taps)),
+        ys(size_t(nco * OH * OW));
+    for (long long c = 0; c < nci; ++c)
+      for (long long k = 0; k < H * W; ++k)
+        xs[size_t(c * H * W + k)] = double(ti.data[size_t((b.ci_lo + c) * H * W + k)]);
+    for (long long o = 0; o < nco; ++o)
+      for (long long c = 0; c < nci; ++c)
+        for (long long t = 0; t < taps; ++t)
+          ws[size_t((o * nci + c) * taps + t)] =
+              double(tk.data[size_t(((b.co_lo + o) * Ci + b.ci_lo + c) * taps + t)]);
+    SpecDesc d(bs);
+    check(nb_conv_band(ctx.get(), &d.c, 1, xs.data(), ws.data(), int32_t(b.oh_lo),
+                       int32_t(b.oh_hi), ys.data(), prec));
+    for (long long o = 0; o < nco; ++o)
+      for (long long oh = b.oh_lo; oh < b.oh_hi; ++oh)
+        for (long long ow = 0; ow < OW; ++ow) {
+          const double v = ys[size_t((o * OH + oh) * OW + ow)];
+          T& dst = out.data[size_t(((b.co_lo + o) * OH + oh) * OW + ow)];
+          if constexpr (std::is_integral<T>::value) dst += T(std::llround(v));
+          else dst += T(v);
+        }
+    rep.box_macs += nco * (b.oh_hi - b.oh_lo) * OW * nci * taps;
+  }
+  if (report) *report = std::move(rep);
   return out;
 }
 

@@ -219,6 +219,46 @@ int nbi_run_search(const char* cfg_json, const char* devices, int precision, int
 // by a DSL sequence (parse_sequence, I/transforms.hpp:756): any nest,
 // including the ones with no ConvSpec (Sequence 1).  in (Ci,H,W), w
 // (Co_eff,Ci,Kh,Kw), out (Co_eff,out_h,out_w); int64 when is_int else double.
+// execute_boxes: the masked box executor in precision `prec`; fills
+// *nboxes, *box_macs, *nest_macs (nullable).  Returns NB_ERR_UNSUPPORTED
+// (last error says why) for a nest that does not decompose into boxes.
+int nbi_execute_boxes(const char* spec_json, const char* dsl, int is_int, const void* in,
+                      const void* w, void* out, int prec, long long* nboxes, long long* box_macs,
+                      long long* nest_macs) {
+  try {
+    nestopt::ConvSpec s = nestopt::conv_spec_from_json(nlohmann::json::parse(spec_json));
+    nestopt::LoopNest nest = nestopt::apply(nestopt::conv_nest(s), nestopt::parse_sequence(dsl));
+    nb200::Context ctx(0);
+    nb200::BoxReport rep;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      nestopt::ExecEnv<T> env;
+      nestopt::Tensor<T> ti({s.ci, s.h, s.w}), tw({s.co_eff(), s.ci, s.kh, s.kw});
+      std::memcpy(ti.data.data(), in, ti.data.size() * 8);
+      std::memcpy(tw.data.data(), w, tw.data.size() * 8);
+      env.bindings["I"] = ti;
+      env.bindings["K"] = tw;
+      nestopt::Tensor<T> to = nb200::execute_boxes(ctx, nest, env, nb_precision(prec), &rep);
+      std::memcpy(out, to.data.data(), to.data.size() * 8);
+    };
+    if (is_int) run((long long)0);
+    else run(0.0);
+    if (nboxes) *nboxes = (long long)rep.boxes.size();
+    if (box_macs) *box_macs = rep.box_macs;
+    if (nest_macs) *nest_macs = rep.nest_macs;
+    return 0;
+  } catch (const nb200::BoxUnsupported& e) {
+    g_err = e.what();
+    return NB_ERR_UNSUPPORTED;
+  } catch (const nb200::DeviceError& e) {
+    g_err = e.what();
+    return NB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NB_ERR_GENERIC;
+  }
+}
+
 int nbi_execute(const char* spec_json, const char* dsl, int is_int, const void* in, const void* w,
                 void* out) {
   try {

@@ -151,6 +151,9 @@ SIGNATURES = {
     "nb_conv_forward": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int32, C.c_int]),
     "nb_conv_dgrad": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, dp, C.c_int]),
     "nb_nest_execute": (C.c_int, [vp, P(NestC), C.c_int32, vp, vp, vp]),
+    "nb_nest_cells": (C.c_int, [vp, P(NestC), P(C.c_int32), P(C.c_int32), P(C.c_int64)]),
+    "nb_conv_band": (C.c_int, [vp, P(ConvSpecC), C.c_int64, dp, dp, C.c_int32, C.c_int32, dp,
+                               C.c_int]),
     "nb_semantic_legality": (C.c_int, [vp, P(LegalNestC), P(LegalNestC), P(LegalOutC)]),
     "nb_ctx_device": (C.c_int, [vp]),
     "nb_forward": (C.c_int, [vp, P(NetworkC), P(WeightsC), P(BatchC), C.c_int, dp, dp, dp]),

@@ -1336,7 +1336,8 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
 // Single-layer entry points (reference_conv / the dgrad step) through the
 // same per-layer executors as the network pipeline.
 void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* in,
-                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad) {
+                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad,
+                 int oh_lo, int oh_hi) {
   nb_layer layer{*spec, relu, 0};
   nb_network one{1, &layer, 2, 0};
   NetDesc d = NetDesc::from(&one);
@@ -1379,6 +1380,28 @@ void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double*
     NB_CUDA(cudaMemcpyAsync(ctx->io.p, in, size_t(x_cnt) * 8, cudaMemcpyHostToDevice, st));
     launch_nchw64_to_nhwc32(ctx->io.as<double>(), xb, n, int(s.ci), int(s.h), int(s.w), st);
     if (in_amax) launch_amax(xb, n, s.ci * s.h * s.w, in_amax, st);
+    if (oh_hi > oh_lo && (oh_lo > 0 || oh_hi < lp.geom.OH)) {
+      // a band of output rows (nb_conv_band): tensor-core ranges tile only
+      // the band's rows (the other rows of y are left undefined); direct
+      // ranges compute every row
+      for (int r = 0; r < lp.geom.nranges; ++r) {
+        if (lp.family[r] != Family::TensorCore) continue;
+        tc::TcArgs& t = lp.tcf[r].tile;
+        tc::TcArgs b{};
+        if (!tc::plan_tiles(oh_hi - oh_lo, t.OW, t.nimg, t.S, b)) continue;
+        t.OH = b.OH;
+        t.BW = b.BW;
+        t.BH = b.BH;
+        t.BNI = b.BNI;
+        t.tiles_w = b.tiles_w;
+        t.tiles_h = b.tiles_h;
+        t.tiles_n = b.tiles_n;
+        t.m_tiles = b.m_tiles;
+        t.OHp[0] = oh_hi - oh_lo;
+        t.oh_base = oh_lo;
+        t.ksplit = 1;
+      }
+    }
     fprop_layer(ctx, P, lp, xb, yb, relu != 0, st, in_amax, nullptr);
     launch_nhwc32_to_nchw64(yb, ctx->io.as<double>(), n, lp.geom.Co, lp.geom.OH, lp.geom.OW, st);
     NB_CUDA(cudaMemcpyAsync(out, ctx->io.p, size_t(y_cnt) * 8, cudaMemcpyDeviceToHost, st));
@@ -1815,6 +1838,22 @@ nb_status nb_conv_forward(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, cons
     need(w, "weights");
     need(y, "output");
     conv_single(ctx, spec, n, x, w, y, relu, prec, false);
+  });
+}
+
+nb_status nb_conv_band(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* x,
+                       const double* w, int32_t oh_lo, int32_t oh_hi, double* y,
+                       nb_precision prec) {
+  return guard([&] {
+    need(ctx, "context");
+    need(spec, "spec");
+    need(x, "input");
+    need(w, "weights");
+    need(y, "output");
+    Spec s = Spec::from(*spec);
+    s.validate();
+    if (oh_lo < 0 || oh_hi > s.oh() || oh_lo >= oh_hi) fail(NB_ERR_CONFIG, "bad output row band");
+    conv_single(ctx, spec, n, x, w, y, 0, prec, false, oh_lo, oh_hi);
   });
 }
 

@@ -247,8 +247,11 @@ void run_network(nb_session* s, const NetDesc& net, const nb_weights* w, nb_prec
                  bool backward, const RunOut& out);
 
 void ctx_activate(nb_ctx* c);
+// oh_lo < oh_hi: fprop of the output rows [oh_lo, oh_hi) only (the rest of
+// out undefined; nb_conv_band)
 void conv_single(nb_ctx* ctx, const nb_conv_spec* spec, int64_t n, const double* in,
-                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad);
+                 const double* w, double* out, int32_t relu, nb_precision prec, bool dgrad,
+                 int oh_lo = 0, int oh_hi = 0);
 void warm_z(nb_ctx* c, const NetDesc& net);
 
 }  // namespace nb

@@ -658,7 +658,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
         const int c_base = a.a_c_base + g * a.a_c_per_group;
         const int row = a.b_row_base + g * a.b_row_per_group + nn * BN + (PAIR ? int(rank) * C::kBRows : 0);
-        const int w0 = wb * a.BW * a.S, h0 = hb * a.BH * a.S, n0 = nb * a.BNI;
+        // (oh_base: a band of output rows starting there, fprop only)
+        const int w0 = wb * a.BW * a.S, h0 = (hb * a.BH + a.oh_base) * a.S, n0 = nb * a.BNI;
         const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
         // B of K block (tap tp, chunk cb) into the stage
         auto load_b = [&](int32_t tp, int cb) {
@@ -869,8 +870,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       const int wb = m % a.tiles_w, hb = (m / a.tiles_w) % a.tiles_h, nb = m / (a.tiles_w * a.tiles_h);
       const int g = nt / a.n_tiles_per_group, nn = nt % a.n_tiles_per_group;
       const int wi = r % a.BW, hi = (r / a.BW) % a.BH, ni = r / rows_per_img;
-      const int n = nb * a.BNI + ni, oh = hb * a.BH + hi, ow = wb * a.BW + wi;
-      const bool valid = m < a.m_tiles && ni < a.BNI && n < a.nimg && oh < a.OHp[ph] &&
+      const int n = nb * a.BNI + ni, oh = hb * a.BH + hi + a.oh_base, ow = wb * a.BW + wi;
+      const bool valid = m < a.m_tiles && ni < a.BNI && n < a.nimg && oh < a.oh_base + a.OHp[ph] &&
                          ow < a.OWp[ph];
       const int64_t pix =
           (int64_t(n) * a.OutH + oh * a.PS + a.py[ph]) * a.OutW + ow * a.PS + a.px[ph];

@@ -56,6 +56,9 @@ struct TcArgs {
   int a_cblocks, a_c_base, a_c_per_group;
   // B operand (2-D K-major weights [rows][taps*K]): K per tap, row bases
   int b_k_per_tap, b_row_base, b_row_per_group;
+  // fprop over a band of output rows [oh_base, oh_base + OHp[0]) of the
+  // OutH-row output (the masked box executor, nb_conv_band); 0 otherwise
+  int oh_base;
   // epilogue output (NHWC over OutH x OutW pixels, ld channels)
   float* out;
   int OutH, OutW;

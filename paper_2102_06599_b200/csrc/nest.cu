@@ -79,26 +79,57 @@ __global__ void k_nest_exec(DevStmt s, int64_t count, const int64_t* __restrict_
   }
 }
 
+// The masked box executor's cell pass: per output cell, the smallest and
+// largest input channel (index 0 of the statement's "I" access) and the
+// number of multiply-accumulate instances adding into it.
+__global__ void k_nest_cells(DevStmt s, int64_t count, const int64_t* __restrict__ code,
+                             longlong4 shp_o, longlong4 shp_i, longlong4 shp_w, int* ci_lo,
+                             int* ci_hi, unsigned long long* cnt) {
+  for (int64_t inst = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; inst < count;
+       inst += int64_t(gridDim.x) * blockDim.x) {
+    int64_t loops[kMaxDepth];
+    int64_t r = inst;
+    for (int d = s.depth - 1; d >= 0; --d) {
+      loops[d] = r % s.extents[d];
+      r /= s.extents[d];
+    }
+    int64_t dom[kMaxDomain];
+    for (int i = 0; i < s.ndomain; ++i) dom[i] = run(code, s.coord_off[i], loops);
+    int64_t o_lin = -1, ci = -1;
+    for (int a = 0; a < s.naccess; ++a) {
+      const DevAccess& acc = s.acc[a];
+      if (acc.tensor == 2) continue;
+      const long long* dims = acc.tensor == 0 ? &shp_o.x : &shp_i.x;
+      if (acc.tensor == 1) {
+        ci = run(code, acc.idx_off[0], dom);
+        continue;
+      }
+      int64_t lin = 0;
+      bool inb = true;
+      for (int k = 0; k < acc.rank; ++k) {
+        const int64_t v = run(code, acc.idx_off[k], dom);
+        if (v < 0 || v >= dims[k]) inb = false;
+        lin = lin * dims[k] + v;
+      }
+      o_lin = inb ? lin : -1;
+    }
+    if (o_lin < 0) continue;
+    atomicMin(ci_lo + o_lin, int(ci));
+    atomicMax(ci_hi + o_lin, int(ci));
+    atomicAdd(cnt + o_lin, 1ull);
+  }
+}
+
 int64_t numel(const int64_t* d, int rank) {
   int64_t n = 1;
   for (int i = 0; i < rank; ++i) n *= d[i];
   return n;
 }
 
-}  // namespace
-}  // namespace nb
-
-using namespace nb;
-
-extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int,
-                                     const void* in, const void* w, void* out) {
-  return guard([&] {
-    if (!ctx || !nest || !in || !w || !out) fail(NB_ERR_CONFIG, "null argument");
-    if (nest->out_rank > kMaxRank || nest->in_rank > kMaxRank || nest->w_rank > kMaxRank)
-      fail(NB_ERR_UNSUPPORTED, "tensor rank above 4");
-    // flatten every program into one code array; each program starts with
-    // a (nops, 0) header
-    std::vector<int64_t> code;
+// The nest's statements as device descriptors over one flattened code
+// array of postfix programs (each program starts with a (nops, 0) header).
+void compile(const nb_nest* nest, std::vector<int64_t>& code, std::vector<DevStmt>& stmts,
+             std::vector<int64_t>& counts) {
     auto add = [&](const nb_nest_expr& e) {
       const int off = int(code.size() / 2);
       code.push_back(e.nops);
@@ -117,8 +148,6 @@ extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t i
       if (depth != 1 || maxd > kStack) fail(NB_ERR_UNSUPPORTED, "nest expression too deep");
       return off;
     };
-    std::vector<DevStmt> stmts;
-    std::vector<int64_t> counts;
     for (int64_t i = 0; i < nest->num_stmts; ++i) {
       const nb_nest_stmt& src = nest->stmts[i];
       if (src.depth > kMaxDepth || src.ndomain > kMaxDomain || src.naccess > kMaxAcc)
@@ -150,6 +179,23 @@ extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t i
       stmts.push_back(d);
       counts.push_back(cnt);
     }
+}
+
+}  // namespace
+}  // namespace nb
+
+using namespace nb;
+
+extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int,
+                                     const void* in, const void* w, void* out) {
+  return guard([&] {
+    if (!ctx || !nest || !in || !w || !out) fail(NB_ERR_CONFIG, "null argument");
+    if (nest->out_rank > kMaxRank || nest->in_rank > kMaxRank || nest->w_rank > kMaxRank)
+      fail(NB_ERR_UNSUPPORTED, "tensor rank above 4");
+    std::vector<int64_t> code;
+    std::vector<DevStmt> stmts;
+    std::vector<int64_t> counts;
+    compile(nest, code, stmts, counts);
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx_activate(ctx);
     cudaStream_t st = ctx->stream;
@@ -193,5 +239,49 @@ extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t i
     NB_CUDA(cudaStreamSynchronize(st));
     if (err == 1) fail(NB_ERR_GENERIC, "read outside a tensor");  // IndexOutOfRange
     if (err == 2) fail(NB_ERR_GENERIC, "accumulate outside the output");
+  });
+}
+
+extern "C" nb_status nb_nest_cells(nb_ctx* ctx, const nb_nest* nest, int32_t* ci_lo,
+                                   int32_t* ci_hi, int64_t* count) {
+  return guard([&] {
+    if (!ctx || !nest || !ci_lo || !ci_hi || !count) fail(NB_ERR_CONFIG, "null argument");
+    if (nest->out_rank > kMaxRank || nest->in_rank > kMaxRank || nest->w_rank > kMaxRank)
+      fail(NB_ERR_UNSUPPORTED, "tensor rank above 4");
+    std::vector<int64_t> code;
+    std::vector<DevStmt> stmts;
+    std::vector<int64_t> counts;
+    compile(nest, code, stmts, counts);
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx_activate(ctx);
+    cudaStream_t st = ctx->stream;
+    const int64_t no = numel(nest->out_shape, nest->out_rank);
+    // io: [code | ci_lo | ci_hi | count]
+    const size_t code_b = (code.size() * 8 + 255) & ~size_t(255);
+    const size_t cell_b = (size_t(no) * 4 + 255) & ~size_t(255);
+    ctx->io.ensure(code_b + 2 * cell_b + size_t(no) * 8);
+    char* base = static_cast<char*>(ctx->io.p);
+    int64_t* d_code = reinterpret_cast<int64_t*>(base);
+    int* d_lo = reinterpret_cast<int*>(base + code_b);
+    int* d_hi = reinterpret_cast<int*>(base + code_b + cell_b);
+    auto* d_cnt = reinterpret_cast<unsigned long long*>(base + code_b + 2 * cell_b);
+    NB_CUDA(cudaMemcpyAsync(d_code, code.data(), code.size() * 8, cudaMemcpyHostToDevice, st));
+    NB_CUDA(cudaMemsetAsync(d_lo, 0x7f, size_t(no) * 4, st));  // ~INT_MAX
+    NB_CUDA(cudaMemsetAsync(d_hi, 0xff, size_t(no) * 4, st));  // -1
+    NB_CUDA(cudaMemsetAsync(d_cnt, 0, size_t(no) * 8, st));
+    auto shp = [](const int64_t* d) { return make_longlong4(d[0], d[1], d[2], d[3]); };
+    for (size_t i = 0; i < stmts.size(); ++i) {
+      if (counts[i] == 0) continue;
+      const int64_t blocks = std::min<int64_t>((counts[i] + 255) / 256, int64_t(ctx->num_sms) * 64);
+      k_nest_cells<<<unsigned(blocks), 256, 0, st>>>(stmts[i], counts[i], d_code,
+                                                     shp(nest->out_shape), shp(nest->in_shape),
+                                                     shp(nest->w_shape), d_lo, d_hi, d_cnt);
+      ctx->launches++;
+    }
+    NB_CUDA(cudaMemcpyAsync(ci_lo, d_lo, size_t(no) * 4, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaMemcpyAsync(ci_hi, d_hi, size_t(no) * 4, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaMemcpyAsync(count, d_cnt, size_t(no) * 8, cudaMemcpyDeviceToHost, st));
+    NB_CUDA(cudaGetLastError());
+    NB_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -36,6 +36,11 @@ def load() -> C.CDLL:
                                        C.POINTER(C.c_void_p)]
         lib.nbi_near_threshold.restype = C.c_int
         lib.nbi_near_threshold.argtypes = [C.c_double, C.c_double, C.c_int]
+        lib.nbi_execute_boxes.restype = C.c_int
+        lib.nbi_execute_boxes.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_int,
+                                          C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                          C.POINTER(C.c_longlong)]
         lib.nbi_execute.restype = C.c_int
         lib.nbi_execute.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p,
                                     C.c_void_p]
@@ -182,3 +187,30 @@ def execute_gpu(spec, dsl: str, x, w):
     if rc != 0:
         raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
     return y
+
+
+def execute_boxes_gpu(spec, dsl: str, x, w, precision: int = None):
+    """The masked box executor (integration/nestopt_b200.hpp execute_boxes):
+    execute (I/interp.hpp:67-145) of conv_nest(spec) rewritten by `dsl` as
+    tensor-core implicit GEMMs over (output-channel range x row band x
+    input-channel range) boxes found by a GPU cell pass.  Integer inputs
+    come back as int64 (exact while sums stay small), floating ones as
+    float64 within the precision tier's tolerance.  Returns (y, stats) with
+    stats = {"boxes", "box_macs", "nest_macs"}; raises Unsupported for a
+    nest that does not decompose into boxes."""
+    import numpy as np
+    from .api import Precision
+    lib = load()
+    prec = Precision.FP32 if precision is None else precision
+    is_int = np.asarray(x).dtype.kind in "iu"
+    dt = np.int64 if is_int else np.float64
+    x = np.ascontiguousarray(x, dt)
+    w = np.ascontiguousarray(w, dt)
+    y = np.zeros(spec.output_shape(), dt)
+    nb_, bm, nm = C.c_longlong(), C.c_longlong(), C.c_longlong()
+    rc = lib.nbi_execute_boxes(json.dumps(spec.to_json()).encode(), dsl.encode(), int(is_int),
+                               x.ctypes.data, w.ctypes.data, y.ctypes.data, int(prec),
+                               C.byref(nb_), C.byref(bm), C.byref(nm))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.nbi_last_error().decode(errors="replace"))
+    return y, {"boxes": nb_.value, "box_macs": bm.value, "nest_macs": nm.value}

@@ -55,3 +55,43 @@ def test_gpu_execute_sequence1_structure():
     assert np.array_equal(y[:, 4:], dense[:, 4:])
     top = y[:, :4]
     assert (top == 0).any() and (top != 0).any()
+
+
+# ---- the masked box executor (execute_boxes) ----------------
+
+@pytest.mark.gpu
+@NEEDS_LIB
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['seed']}-{c['dsl']}")
+def test_gpu_box_executor_matches_reference(case):
+    """Every golden nest (Sequence-1 forms included) on the tensor cores
+    through execute_boxes: int64 bit-exact against the reference's execute;
+    fp64 inputs within the FP32 tier's conv tolerance (relative to the
+    output's scale); the boxes cover exactly the nest's MACs."""
+    import paper_2102_06599_b200 as nb
+    spec = ConvSpec.from_json(case["spec"])
+    rng = np.random.default_rng(case["seed"])
+    x = rng.integers(-3, 4, size=(spec.ci, spec.h, spec.w)).astype(np.int64)
+    w = rng.integers(-3, 4, size=(spec.co_eff(), spec.ci, spec.kh, spec.kw)).astype(np.int64)
+    y, st = S.execute_boxes_gpu(spec, case["dsl"], x, w)
+    assert y.ravel().tolist() == case["out_int"]
+    assert st["box_macs"] == st["nest_macs"] == case["macs"] and st["boxes"] >= 1
+    yf, _ = S.execute_boxes_gpu(spec, case["dsl"], x * 0.37, w * 1.3)
+    ref = np.asarray(case["out_f64"])
+    scale = np.abs(ref).max() or 1.0
+    tol = nb.TOLERANCE[nb.Precision.FP32]["conv"]
+    assert np.abs(yf.ravel() - ref).max() <= tol * scale * spec.ci * spec.kh * spec.kw
+
+
+@pytest.mark.gpu
+@NEEDS_LIB
+def test_gpu_box_executor_sequence1_boxes():
+    """Sequence 1 (arity 2, G 2) decomposes into one box per top row block
+    (its output-channel block) and one dense box over the bottom half --
+    G + 1 boxes, no MAC computed twice, none skipped."""
+    spec = ConvSpec(8, 16, 8, 8, 3, 3, 1, 1)
+    rng = np.random.default_rng(3)
+    x = rng.integers(-3, 4, size=(8, 8, 8)).astype(np.int64)
+    w = rng.integers(-3, 4, size=(16, 8, 3, 3)).astype(np.int64)
+    y, st = S.execute_boxes_gpu(spec, "sequence1(2,2)", x, w)
+    assert st["boxes"] == 3 and st["box_macs"] == st["nest_macs"]
+    assert np.array_equal(y, S.execute_gpu(spec, "sequence1(2,2)", x, w))
