@@ -353,7 +353,7 @@ def main():
     # single-process multi-GPU: one rank drives every GPU (sessions on each)
     devs = list(range(args.gpus)) if (args.single_process and world == 1) else [local]
     ngpu = world * len(devs)
-    origin_j, warm_j, timed_j, _ = timed_pool(args.steps, args.warmup, ngpu)
+    origin_j, warm_j, timed_j, spare_j = timed_pool(args.steps, args.warmup, ngpu)
     origin = nb.Network.from_json(origin_j)
     warm_pool = [nb.Network.from_json(n) for n in warm_j]
     timed = [nb.Network.from_json(n) for n in timed_j]
@@ -453,11 +453,23 @@ def main():
     d2h = sum(8 * (sum(l.spec.co_eff() for l in n.layers) + len(n.layers) + 2 +
                    N_BATCH * n.num_classes) for n in mine) / args.steps
 
-    # ---- transformed-net inference: forward of the best-ranked survivor
-    # (rank_survivors: macs ascending, fisher descending, I/search.hpp:338)
-    surv = [(nb.network_macs(n), -r.total, i) for i, (n, r) in enumerate(zip(mine, reps))
+    # ---- transformed-net inference: forward of the search's choice, i.e.
+    # survivors_ranked.front() over the whole pool (every candidate of the
+    # reference's per-layer search scored by the scheduler, outside the
+    # timed regions; fisher_accepts >= the origin, rank_survivors: macs
+    # ascending, fisher descending, I/search.hpp:338-349, 381)
+    full = [nb.Network.from_json(n) for n in warm_j + timed_j + spare_j]
+    full_reps, _ = nb.evaluate(sessions, full, prec)
+    surv = [(nb.network_macs(n), -r.total, i) for i, (n, r) in enumerate(zip(full, full_reps))
             if r.total >= origin_rep.total]
-    best = mine[min(surv)[2]] if surv else origin
+    bi = min(surv)[2] if surv else -1
+    best = full[bi] if surv else origin
+    best_info = {"pool": len(full), "survivors": len(surv),
+                 "macs": nb.network_macs(best), "origin_macs": nb.network_macs(origin),
+                 "fisher_total": full_reps[bi].total if surv else origin_rep.total,
+                 "origin_fisher_total": origin_rep.total,
+                 "changed_layer": next((l for l, (a, b) in enumerate(zip(best.layers, origin.layers))
+                                        if a.spec != b.spec), None)}
     for _ in range(3):
         sessions[0].forward(best, prec)
     inf_ms, _ = timed_region(lambda: [sessions[0].forward(best, prec) for _ in range(10)])
@@ -556,6 +568,7 @@ def main():
             "other_precisions": modes,
             "inference_ms": inf_ms / 10, "inference_origin_ms": inf_o_ms / 10,
             "inference_net_macs": nb.network_macs(best),
+            "inference_network": best_info,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),

@@ -241,7 +241,7 @@ int pick_pair_bn(int n, int m_tiles, bool split3, bool bf3 = false) {
 // one N tile share every B stage (each loads half, multicast to both), which
 // halves the weight operand's L2 -> SM traffic.  NB_TC_MC=0 disables it.
 bool use_mc(int bn, int m_tiles, bool pair, bool kwf = false, bool bf3 = false) {
-  if (bf3) return false;
+  if (bf3 && split_h16() != 2) return false;  // (16-bit multicast: fp16 only)
   // NB_TC_MC: 0 (default) off, 1 every single-CTA plan, 2 kw-fused plans only
   // (their B stage is 3x wider, 48 KB, the same for every CTA; measured: the
   // stage period drops 7% but the evaluation time does not)

@@ -667,9 +667,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           if (MC) {
             // this CTA's half of the B rows, into both CTAs' stage buffers
             const int half = int(rank) * (NM / 2);
-            if (ld_b) tma_load_2d_mc(b_hi(stage) + half * 128, &mapBh, &full[stage], kcoord, row + half, 3);
+            constexpr int rb = BF ? 64 : 128;  // bytes per B row
+            if (ld_b) tma_load_2d_mc(b_hi(stage) + half * rb, &mapBh, &full[stage], kcoord, row + half, 3);
             if (SPLIT3 && ld_b)
-              tma_load_2d_mc(b_lo(stage) + half * 128, &mapBl, &full[stage], kcoord, row + half, 3);
+              tma_load_2d_mc(b_lo(stage) + half * rb, &mapBl, &full[stage], kcoord, row + half, 3);
           } else {
             if (ld_b) tma_load_2d(b_hi(stage), &mapBh, &full[stage], kcoord, row);
             if (SPLIT3 && ld_b) tma_load_2d(b_lo(stage), &mapBl, &full[stage], kcoord, row);
@@ -1607,8 +1608,17 @@ bool make_maps(TcLaunch& L, const float* A, int AC, int AW, int AH, int AN, cons
 }
 
 cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
-  if (L.bf) {  // 16-bit split: single-CTA plans only
-    if (!L.split3 || L.pair || L.mc) return cudaErrorInvalidValue;
+  if (L.bf) {  // 16-bit split: single-CTA plans, or multicast-B clusters (fp16)
+    if (!L.split3 || L.pair) return cudaErrorInvalidValue;
+    if (L.mc) {
+      if (!L.args.h16_f16) return cudaErrorInvalidValue;
+      if (L.kwf) return L.bn == 64 ? launch_t<64, true, 2, true, 2>(L, st) : cudaErrorInvalidValue;
+      switch (L.bn) {
+        case 64: return launch_t<64, true, 2, false, 2>(L, st);
+        case 128: return launch_t<128, true, 2, false, 2>(L, st);
+      }
+      return cudaErrorInvalidValue;
+    }
     if (L.args.h16_f16) {
       if (L.kwf) return L.bn == 64 ? launch_t<64, true, 0, true, 2>(L, st) : cudaErrorInvalidValue;
       switch (L.bn) {
