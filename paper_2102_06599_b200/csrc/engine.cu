@@ -145,7 +145,7 @@ int pick_bn(int n_per_group, bool split3) {
     const char* e = std::getenv("NB_TC_BN3");
     return e && std::atoi(e) >= 256;
   }();
-  if (split3 && wide3 && !split_bf16() && n_per_group % 256 == 0) return 256;
+  if (split3 && wide3 && split_h16() != 1 && n_per_group % 256 == 0) return 256;
   static const int o3[] = {128, 64, 32};
   static const int o1[] = {256, 128, 64, 32};
   const int* o = split3 ? o3 : o1;

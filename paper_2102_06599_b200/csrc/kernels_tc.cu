@@ -1625,6 +1625,7 @@ cudaError_t launch(const TcLaunch& L, cudaStream_t st) {
         case 32: return launch_t<32, true, 0, false, 2>(L, st);
         case 64: return launch_t<64, true, 0, false, 2>(L, st);
         case 128: return launch_t<128, true, 0, false, 2>(L, st);
+        case 256: return launch_t<256, true, 0, false, 2>(L, st);  // (NB_TC_BN3=256)
       }
     } else {
       if (L.kwf) return L.bn == 64 ? launch_t<64, true, 0, true, 1>(L, st) : cudaErrorInvalidValue;

@@ -1,7 +1,8 @@
 """The tcgen05 kernel's experimental launch modes (environment switches read
 once per process, so each runs in a subprocess with a deadline): CTA pairs,
-multicast-B clusters, converter stage alternation, no split-K, no PDL, and
-the kw-fused plans switched off.  Each must reproduce reference_conv<int64>
+multicast-B clusters, converter stage alternation, no split-K, no PDL, the
+kw-fused plans switched off, the 3xTF32 / 3xBF16 splits, the halo-tile A
+operand and the 256-wide single-accumulator tile.  Each must reproduce reference_conv<int64>
 bit for bit on tensor-core-shaped layers (including a kw-fused shape) and
 finish -- a hang here is a barrier-count bug."""
 import os
@@ -21,7 +22,8 @@ from oracle.oracle import Restatement
 O = Restatement()
 ctx = nb.Context(0)
 specs = [ConvSpec(64, 128, 8, 8, 3, 3, 1, 1), ConvSpec(128, 128, 4, 4, 3, 3, 1, 1),
-         ConvSpec(64, 64, 32, 32, 3, 3, 1, 1), ConvSpec(64, 128, 9, 9, 3, 3, 2, 1)]
+         ConvSpec(64, 64, 32, 32, 3, 3, 1, 1), ConvSpec(64, 128, 9, 9, 3, 3, 2, 1),
+         ConvSpec(256, 256, 8, 8, 3, 3, 1, 1)]
 rng = np.random.default_rng(3)
 for prec in (Precision.FP32, Precision.TF32):
     for s in specs:
@@ -36,15 +38,19 @@ for prec in (Precision.FP32, Precision.TF32):
 print("ok")
 """ % ROOT
 
-MODES = ["NB_TC_PAIR=1", "NB_TC_PAIR=2", "NB_TC_MC=1", "NB_TC_MC=2", "NB_TC_CONVH=0",
-         "NB_TC_CONVH=2", "NB_TC_KSPLIT=0", "NB_TC_PDL=0", "NB_TC_KWF=0"]
+# comma-separated environment assignments; the CTA-pair modes run under the
+# 3xTF32 split (the 16-bit splits plan single-CTA or multicast launches only)
+MODES = ["NB_TC_SPLIT=tf32,NB_TC_PAIR=1", "NB_TC_SPLIT=tf32,NB_TC_PAIR=2", "NB_TC_MC=1",
+         "NB_TC_MC=2", "NB_TC_SPLIT=tf32,NB_TC_MC=1", "NB_TC_CONVH=0", "NB_TC_CONVH=1",
+         "NB_TC_CONVH=2", "NB_TC_KSPLIT=0", "NB_TC_PDL=0", "NB_TC_KWF=0", "NB_TC_SPLIT=tf32",
+         "NB_TC_SPLIT=bf16", "NB_TC_HALO=1", "NB_TC_HALO=1,NB_TC_CONVH=1",
+         "NB_TC_HALO=1,NB_TC_SPLIT=tf32", "NB_TC_BN3=256", "NB_TC_SPLIT=tf32,NB_TC_BN3=256"]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", MODES)
 def test_tc_mode_exact_and_terminates(mode):
-    k, v = mode.split("=")
-    env = dict(os.environ, **{k: v})
+    env = dict(os.environ, **dict(kv.split("=") for kv in mode.split(",")))
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True,
                        timeout=240, cwd=ROOT)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (mode, r.stdout[-2000:],
