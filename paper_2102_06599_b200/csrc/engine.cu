@@ -748,7 +748,7 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
     return e && std::atoi(e) != 0;
   }();
   L.args.halo = 0;
-  if (halo_on && split3 && !tp.pair && !tp.mc && args.S == 1) {
+  if (halo_on && split3 && !tp.pair && args.S == 1) {
     int span_h = 0, span_w = 0, most = 0;
     for (int ph = 0; ph < args.nphase; ++ph) {
       int h0 = 0, h1 = 0, w0 = 0, w1 = 0;

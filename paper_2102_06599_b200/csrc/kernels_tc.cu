@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   // blocks run chunk-major (all taps of a chunk back to back) and the
   // converters form each tap's shifted A rows from the halo while splitting
   // them -- one A load per chunk instead of one per (tap, chunk).
-  const bool halo = kSplitA && !MC && a.halo;
+  const bool halo = kSplitA && a.halo;
   // channel-halves conversion (two groups per stage) needs exactly two groups
   // (two alternating groups need even rings: an odd ring converts by halves)
   const bool halves_on = SPLIT3 && C::kConvGroups == 2 && (a.conv_halves != 0 || (S & 1) || (ST & 1));
@@ -627,7 +627,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   // init, TMEM allocation, descriptor prefetch) overlapped the previous
   // kernel's tail.  Every global read and write below waits for that kernel.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Experiment (NB_TC_DEBUG bit 16384): the producer lane of a single-CTA
+  // split-converter launch first issues its first tile's B stages (packed
+  // weights, written before any conv of the run started) and waits for the
+  // previous kernel only then.  Measured 2% slower (the early loads compete
+  // with the previous kernel's tail, profiles/r02_kernels.md), so off.
+  const bool early_b = kSplitA && !MC && warp == 0 && lane == 0 && (a.debug & 16384);
+  if (!early_b) asm volatile("griddepcontrol.wait;" ::: "memory");
   // trace: per-CTA %globaltimer at start (after the grid dependency) and at
   // the end, slots [5*kTraceStages + 4*cta + {0: launch, 1: start, 2: mma done, 3: end}]
   if (a.trace && threadIdx.x == 0) {
@@ -651,6 +657,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       int stage = 0, pit = 0, hidx = 0;
       uint32_t phase = 0;
       const uint32_t halo_bytes = uint32_t(a.halo_w) * a.halo_h * a.BNI * 128;
+      int b_pre = 0;  // leading B stages of the first tile issued before the grid dependency
+      if (early_b) {
+        if (unit0 < num_units && !(a.debug & 8)) {
+          const Tile d = decode<CLUSTER>(a, unit0, int(rank));
+          const int g = d.nt / a.n_tiles_per_group, nn = d.nt % a.n_tiles_per_group;
+          const int row = a.b_row_base + g * a.b_row_per_group + nn * BN;
+          const int ntp = a.ntaps[d.ph];
+          b_pre = min(S, d.kb1 - d.kb0);
+          for (int i = 0; i < b_pre; ++i) {
+            const int kb = d.kb0 + i;
+            const int32_t tp = a.taps[d.ph][halo ? kb % ntp : kb / a.a_cblocks];
+            const int cb = halo ? kb / ntp : kb % a.a_cblocks;
+            const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
+            mbar_expect_tx(&full[i], uint32_t(C::kBBytes) * 2);  // (stage i: fresh ring)
+            tma_load_2d(b_hi(i), &mapBh, &full[i], kcoord, row);
+            tma_load_2d(b_lo(i), &mapBl, &full[i], kcoord, row);
+          }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+      }
       for (int u = unit0; u < num_units; u += ustep) {
         const Tile d = decode<CLUSTER>(a, u, int(rank));
         const int m = d.m, nt = d.nt;
@@ -661,9 +687,17 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         // (oh_base: a band of output rows starting there, fprop only)
         const int w0 = wb * a.BW * a.S, h0 = (hb * a.BH + a.oh_base) * a.S, n0 = nb * a.BNI;
         const bool ld_a = !(a.debug & 4), ld_b = !(a.debug & 8);  // experiments
-        // B of K block (tap tp, chunk cb) into the stage
-        auto load_b = [&](int32_t tp, int cb) {
+        // B of K block (tap tp, chunk cb) into the stage (issue == false: the
+        // stage's B was issued ahead of the grid dependency; advance only)
+        auto load_b = [&](int32_t tp, int cb, bool issue = true) {
           const int kcoord = tap_kidx(tp) * a.b_k_per_tap + cb * 32;
+          if (!issue) {
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            return;
+          }
           if (MC) {
             // this CTA's half of the B rows, into both CTAs' stage buffers
             const int half = int(rank) * (NM / 2);
@@ -696,8 +730,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             }
             mbar_wait(&empty[stage], phase ^ 1);
             trace(a, 0, pit++);
-            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
-            load_b(a.taps[d.ph][t], cb);
+            const bool pre = b_pre > 0;
+            if (pre) --b_pre;
+            else mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
+            load_b(a.taps[d.ph][t], cb, !pre);
             if (++t == ntp) {
               t = 0;
               ++cb;
@@ -712,16 +748,18 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           const int ah = h0 + tap_dh(tp), aw = w0 + tap_dw(tp);
           mbar_wait(&empty[stage], phase ^ 1);
           trace(a, 0, pit++);
+          const bool pre = b_pre > 0;
+          if (pre) --b_pre;
           if (kSplitA) {
             mbar_expect_tx(&fulla[stage], ld_a ? a_box_bytes : 0u);
             if (ld_a) tma_load_4d(a_hi(stage), &mapA, &fulla[stage], c_base + cb * 32, aw, ah, n0);
-            mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
+            if (!pre) mbar_expect_tx(&full[stage], ld_b ? uint32_t(C::kBBytes) * 2 : 0u);
           } else {
             mbar_expect_tx(&full[stage], (ld_a ? a_box_bytes : 0u) +
                                              (ld_b ? uint32_t(C::kBBytes) * (SPLIT3 ? 2 : 1) : 0u));
             if (ld_a) tma_load_4d(a_hi(stage), &mapA, &full[stage], c_base + cb * 32, aw, ah, n0);
           }
-          load_b(tp, cb);
+          load_b(tp, cb, !pre);
         }
       }
     }
@@ -1562,7 +1600,7 @@ int halo_cap_t() {
 }  // namespace
 
 int halo_capacity(const TcLaunch& L) {
-  if (!L.split3 || L.pair || L.mc) return 0;
+  if (!L.split3 || L.pair) return 0;
   if (L.kwf) return L.bn == 64 ? (L.bf ? halo_cap_t<64, true, true>() : halo_cap_t<64, true, false>()) : 0;
   switch (L.bn) {
     case 32: return L.bf ? halo_cap_t<32, false, true>() : halo_cap_t<32, false, false>();

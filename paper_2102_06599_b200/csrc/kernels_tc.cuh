@@ -99,7 +99,8 @@ struct TcArgs {
   // garbage results): 2 = no MMAs, 4 = no A loads, 8 = no B loads, 16 = no
   // epilogue, 32 = no split conversion, 64 = no tiles at all, 128 = MMAs
   // read stage 0's TMEM columns only, 2048 = no A_prev loads, 4096 = no
-  // Fisher reduction, 8192 = no dpre stores; bits 16..19 cap the ring depth
+  // Fisher reduction, 8192 = no dpre stores, 16384 = B prefetch before the
+  // grid dependency (a correct variant, not garbage); bits 16..19 cap the ring depth
   // (0 = the configured stage count)
   int debug;
   // experiments only (NB_TC_TRACE): CTA 0 records clock64() stamps of its

@@ -44,7 +44,8 @@ MODES = ["NB_TC_SPLIT=tf32,NB_TC_PAIR=1", "NB_TC_SPLIT=tf32,NB_TC_PAIR=2", "NB_T
          "NB_TC_MC=2", "NB_TC_SPLIT=tf32,NB_TC_MC=1", "NB_TC_CONVH=0", "NB_TC_CONVH=1",
          "NB_TC_CONVH=2", "NB_TC_KSPLIT=0", "NB_TC_PDL=0", "NB_TC_KWF=0", "NB_TC_SPLIT=tf32",
          "NB_TC_SPLIT=bf16", "NB_TC_HALO=1", "NB_TC_HALO=1,NB_TC_CONVH=1",
-         "NB_TC_HALO=1,NB_TC_SPLIT=tf32", "NB_TC_BN3=256", "NB_TC_SPLIT=tf32,NB_TC_BN3=256"]
+         "NB_TC_HALO=1,NB_TC_SPLIT=tf32", "NB_TC_BN3=256", "NB_TC_SPLIT=tf32,NB_TC_BN3=256",
+         "NB_TC_HALO=1,NB_TC_MC=1", "NB_TC_DEBUG=16384", "NB_TC_DEBUG=16384,NB_TC_HALO=1"]
 
 
 @pytest.mark.gpu
