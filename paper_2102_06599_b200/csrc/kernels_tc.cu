@@ -921,6 +921,33 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       const bool empty_phase = a.ntaps[ph] == 0;
       const int tile_in_img = ph * part_per_phase + (a.BNI == 1 ? hb * a.tiles_w + wb : 0);
       const bool tile_real = m < a.m_tiles;
+      // Fused dgrad epilogue of the Fisher pipeline (each warp's 32 rows in
+      // one image): A_prev in / dpre out move through a per-warp transpose
+      // tile (lane l moves 16 B of row 8k + l/4, column quad l%4 -- 8 rows x
+      // 64 B per warp instruction instead of 32 rows x 16 B).  A_prev of the
+      // first two 16-column chunks is requested before waiting for the
+      // accumulator (it does not depend on it), then two chunks ahead.
+      const bool fast_dgrad = a.mode == 1 && a.ksplit == 1 && a.partial && a.a_prev &&
+                              rows_per_img % 32 == 0 && !(a.debug & 16);
+      const int64_t rbase = pix * a.out_ld + col0;
+      long long rp[4];
+      float4 apn[2][4];
+      if (fast_dgrad) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int src = 8 * k + (lane >> 2);
+          const long long b = __shfl_sync(0xffffffffu, (long long)rbase, src);
+          const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
+          rp[k] = ok ? b + 4 * (lane & 3) : -1ll;
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            apn[j][k] = rp[k] >= 0 && 16 * j < nlim && 16 * j < BN
+                            ? *reinterpret_cast<const float4*>(a.a_prev + rp[k] + 16 * j)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * NM);
@@ -962,40 +989,16 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           for (int i = 0; i < 16; ++i) v[i] = (v[i] * inv_a) * a.b_inv;
         }
       };
-      // Fused dgrad epilogue of the Fisher pipeline (each warp's 32 rows in one
-      // image): the next chunk's A_prev is loaded while this one is processed,
-      // a 31-shuffle reduce-scatter leaves lane l with the warp's sum of column
-      // l of the chunk, and the image's warps are combined once per tile.
-      const bool fast_dgrad = a.mode == 1 && a.ksplit == 1 && a.partial && a.a_prev &&
-                              rows_per_img % 32 == 0 && !(a.debug & 16);
       if (fast_dgrad) {
-        const int64_t rbase = pix * a.out_ld + col0;
-        // A_prev in / dpre out through a per-warp transpose tile: lane l moves
-        // 16 B of row 8k + l/4 (column quad l%4) -- 8 rows x 64 B per warp
-        // instruction instead of 32 rows x 16 B
         float* xp = red + 128 * 17 + q * (32 * 20);
         const float* aprev = a.a_prev;
-        auto row_ptr = [&](int k) {  // this lane's transposed row k: base offset, valid
-          const int src = 8 * k + (lane >> 2);
-          const long long b = __shfl_sync(0xffffffffu, (long long)rbase, src);
-          const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
-          return ok ? b + 4 * (lane & 3) : -1ll;
-        };
-        long long rp[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rp[k] = row_ptr(k);
-        float4 apn[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          apn[k] = rp[k] >= 0 ? *reinterpret_cast<const float4*>(aprev + rp[k])
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
           if (c >= nlim) break;
           // transpose this chunk's A_prev rows into registers (own row)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3)) = apn[k];
+            *reinterpret_cast<float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3)) = apn[0][k];
           __syncwarp();
           float av[16];
 #pragma unroll
@@ -1007,10 +1010,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             av[4 * i + 3] = t.w;
           }
           __syncwarp();
-          if (c + 16 < BN && c + 16 < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) apn[0][k] = apn[1][k];
+          if (c + 32 < BN && c + 32 < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (rp[k] >= 0) apn[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 16);
+              if (rp[k] >= 0) apn[1][k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 32);
           }
           float v[16];
           acc_ld16(c, v);
@@ -1361,8 +1366,14 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
                 tmem_st8(ta + 8 * cg, hi);
                 tmem_st8(ta + 16 + 8 * cg, lo);
               } else {
-                tmem_st16(ta, hi);
-                tmem_st16(ta + 16, lo);
+                // hi and lo are adjacent: one 32-column store
+                uint32_t hl[32];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  hl[i] = hi[i];
+                  hl[16 + i] = lo[i];
+                }
+                tmem_st32(ta, hl);
               }
             } else if (halves) {
               uint32_t hi[16], lo[16];

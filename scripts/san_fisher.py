@@ -13,6 +13,7 @@ net = Network([
     Layer(ConvSpec(64, 64, 8, 8, 3, 3, 1, 1, spatial_div_h=2, spatial_div_w=2)),
     Layer(ConvSpec(64, 64, 4, 4, 3, 3, 1, 1, groups=64)),
     Layer(ConvSpec(64, 64, 4, 4, 3, 3, 1, 1)),
+    Layer(ConvSpec(64, 64, 4, 4, 3, 3, 1, 1, groups=16)),
 ], num_classes=10, seed=42)
 ctx = nb.Context(0)
 batch = nb.make_batch(net, 4, 1)
