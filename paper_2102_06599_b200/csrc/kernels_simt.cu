@@ -903,11 +903,30 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
   float contrib[4] = {0.f, 0.f, 0.f, 0.f};
   float mx = 0.f;  // max |stored value| for the next fp16-split GEMM (image n)
   if (c < e.C) {
+    // the partials and A_prev are read-only here: every load of a pixel is
+    // issued (non-coherent path) before its sums, and two splits at a time
+#pragma unroll 2
     for (int p = int(blockIdx.z) * cs + threadIdx.y; p < pend; p += 8) {
       const int64_t idx = (n * e.HW + p) * e.ld + e.c0 + c;
+      const float4* wsp = reinterpret_cast<const float4*>(e.ws + idx);
+      const int64_t wst = e.ws_stride / 4;
+      const float4 w0 = __ldg(wsp);
+      const float4 w1 = e.ksplit > 1 ? __ldg(wsp + wst) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 a = e.mode == 1 && e.a_prev ? __ldg(reinterpret_cast<const float4*>(e.a_prev + idx))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int k = 0; k < e.ksplit; ++k) {
-        const float4 w = *reinterpret_cast<const float4*>(e.ws + k * e.ws_stride + idx);
+      v.x += w0.x;
+      v.y += w0.y;
+      v.z += w0.z;
+      v.w += w0.w;
+      if (e.ksplit > 1) {
+        v.x += w1.x;
+        v.y += w1.y;
+        v.z += w1.z;
+        v.w += w1.w;
+      }
+      for (int k = 2; k < e.ksplit; ++k) {
+        const float4 w = __ldg(wsp + k * wst);
         v.x += w.x;
         v.y += w.y;
         v.z += w.z;
@@ -925,7 +944,6 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue4(SplitEpi e) {
       } else {
         if (e.g_out) *reinterpret_cast<float4*>(e.g_out + idx) = v;
         if (e.a_prev) {
-          const float4 a = *reinterpret_cast<const float4*>(e.a_prev + idx);
           contrib[0] = fmaf(a.x, v.x, contrib[0]);
           contrib[1] = fmaf(a.y, v.y, contrib[1]);
           contrib[2] = fmaf(a.z, v.z, contrib[2]);
