@@ -1057,15 +1057,11 @@ bool grouped_smem_ok(const ConvGeom& g, const RangeDesc& r) {
   return size_t(IH) * IW * cic * 4 <= 96 * 1024;
 }
 
-// Depthwise 3x3 stride-1 pad-1 fprop as a register sliding window (NHWC,
-// channel pairs): thread (pair, column) walks a strip of kDwStrip output
-// rows keeping its 3x3 window in registers; each step prefetches the next
-// input row's three pairs (the side columns are the neighbouring threads'
-// centres: L1 hits), runs 18 FMAs and stores one output pair (coalesced
-// across the pairs).  Pairs rather than quads keep the state at ~60
-// registers, so four 256-thread blocks share an SM: the strip loops need
-// warps, not barriers, to keep DRAM busy.  DRAM sees each input and output
-// once (plus the strips' halo rows).
+// Depthwise 3x3 stride-1 pad-1 fprop as a register sliding window (NHWC).
+// DRAM sees each input and output once (plus the strips' halo rows); with
+// one output column per thread every input pixel also crossed L1 three times
+// and the loop was load-instruction bound (47% of HBM on 64@56, N=256); eight
+// columns per thread load each pixel once per column block: 65% (profiles/).
 constexpr int kDwStrip = 16;
 
 // V = channels per thread (1 or 2): vector type and its lanes
@@ -1084,20 +1080,27 @@ struct DwVec<2> {
   __device__ static float& at(float2& v, int i) { return i ? v.y : v.x; }
 };
 
-template <int V>
-__global__ void __launch_bounds__(256, V == 1 ? 8 : 4)
+// Thread = V adjacent channels x OWB adjacent output columns of a
+// `strip`-row strip; a register window of 3
+// input rows x (OWB + 2) columns slides down the strip (each input pixel is
+// loaded once per thread column block, the next row is in flight while the
+// current one computes).  A warp covers 32 channel groups of one column
+// block: its loads and stores are contiguous channel runs.
+template <int V, int OWB>
+__global__ void __launch_bounds__(256, OWB == 1 ? (V == 1 ? 8 : 4) : (OWB == 2 ? 3 : 2))
     k_dw3_nhwc(ConvGeom g, int ri, const float* __restrict__ x, const float* __restrict__ wbase,
-               float* __restrict__ y, bool relu) {
+               float* __restrict__ y, bool relu, int strip) {
   using DV = DwVec<V>;
   using T = typename DV::T;
+  constexpr int WW = OWB + 2;
   const RangeDesc r = g.r[ri];
   const int np = r.len / V;
   const int p = blockIdx.z * blockDim.x + threadIdx.x;  // channel group (range-local)
-  const int ow = blockIdx.x * blockDim.y + threadIdx.y;
-  const int strips = (g.OH + kDwStrip - 1) / kDwStrip;
+  const int ow0 = (blockIdx.x * blockDim.y + threadIdx.y) * OWB;
+  const int strips = (g.OH + strip - 1) / strip;
   const int64_t n = blockIdx.y / strips;
-  const int oh0 = int(blockIdx.y % strips) * kDwStrip, oh1 = min(g.OH, oh0 + kDwStrip);
-  if (p >= np || ow >= g.OW) return;
+  const int oh0 = int(blockIdx.y % strips) * strip, oh1 = min(g.OH, oh0 + strip);
+  if (p >= np || ow0 >= g.OW) return;
   const int c = V * p;  // depthwise: input channel == range-local output channel
   const float* __restrict__ wf = wbase + r.wf_off;  // Wf[tap][0][co]
   T w[9];
@@ -1110,33 +1113,37 @@ __global__ void __launch_bounds__(256, V == 1 ? 8 : 4)
                ? __ldg(reinterpret_cast<const T*>(xn + ih * row + int64_t(iw) * g.Ci))
                : DV::zero();
   };
-  T win[3][3];  // [input row - (oh - 1)][kw]
+  T win[3][WW];  // [input row - (oh - 1)][input column - (ow0 - 1)]
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int kw = 0; kw < 3; ++kw) win[i][kw] = ld(oh0 - 1 + i, ow - 1 + kw);
-  float* __restrict__ yp = y + (n * g.OH * g.OW + ow) * int64_t(g.Co) + r.b + c;
+    for (int j = 0; j < WW; ++j) win[i][j] = ld(oh0 - 1 + i, ow0 - 1 + j);
+  float* __restrict__ yp = y + (n * g.OH * g.OW + ow0) * int64_t(g.Co) + r.b + c;
   for (int oh = oh0; oh < oh1; ++oh) {
-    T nxt[3];  // the next step's input row, in flight while this one computes
+    T nxt[WW];  // the next step's input row, in flight while this one computes
 #pragma unroll
-    for (int kw = 0; kw < 3; ++kw) nxt[kw] = oh + 1 < oh1 ? ld(oh + 2, ow - 1 + kw) : DV::zero();
-    T a = DV::zero();
+    for (int j = 0; j < WW; ++j) nxt[j] = oh + 1 < oh1 ? ld(oh + 2, ow0 - 1 + j) : DV::zero();
 #pragma unroll
-    for (int kh = 0; kh < 3; ++kh)
+    for (int o = 0; o < OWB; ++o) {
+      T a = DV::zero();
 #pragma unroll
-      for (int kw = 0; kw < 3; ++kw)
+      for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
-        for (int i = 0; i < V; ++i)
-          DV::at(a, i) = fmaf(DV::at(win[kh][kw], i), DV::at(w[kh * 3 + kw], i), DV::at(a, i));
-    if (relu)
+        for (int kw = 0; kw < 3; ++kw)
 #pragma unroll
-      for (int i = 0; i < V; ++i) DV::at(a, i) = DV::at(a, i) > 0.f ? DV::at(a, i) : 0.f;
-    *reinterpret_cast<T*>(yp + int64_t(oh) * g.OW * g.Co) = a;
+          for (int i = 0; i < V; ++i)
+            DV::at(a, i) = fmaf(DV::at(win[kh][o + kw], i), DV::at(w[kh * 3 + kw], i), DV::at(a, i));
+      if (relu)
 #pragma unroll
-    for (int kw = 0; kw < 3; ++kw) {
-      win[0][kw] = win[1][kw];
-      win[1][kw] = win[2][kw];
-      win[2][kw] = nxt[kw];
+        for (int i = 0; i < V; ++i) DV::at(a, i) = DV::at(a, i) > 0.f ? DV::at(a, i) : 0.f;
+      if (OWB == 1 || ow0 + o < g.OW)
+        *reinterpret_cast<T*>(yp + (int64_t(oh) * g.OW + o) * g.Co) = a;
+    }
+#pragma unroll
+    for (int j = 0; j < WW; ++j) {
+      win[0][j] = win[1][j];
+      win[1][j] = win[2][j];
+      win[2][j] = nxt[j];
     }
   }
 }
@@ -1161,16 +1168,34 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
       const char* e = std::getenv("NB_DW3_V");
       return e && std::atoi(e) == 1 ? 1 : 2;
     }();
+    // NB_DW3_OWB: output columns per thread (1, 2, 4 or 8 with V=2)
+    static const int OWB = [] {
+      const char* e = std::getenv("NB_DW3_OWB");
+      const int v = e ? std::atoi(e) : 8;
+      return v == 1 || v == 2 || v == 4 ? v : 8;
+    }();
     const int np = r.len / V;
-    const int tp = np < 32 ? np : 32, tw = std::max(1, std::min(256 / tp, g.OW));
+    const int ncb = (g.OW + OWB - 1) / OWB;  // column blocks
+    const int tp = np < 32 ? np : 32;
+    int tw = std::max(1, std::min(256 / tp, ncb));
+    const int gx = (ncb + tw - 1) / tw;
+    tw = (ncb + gx - 1) / gx;  // balance the column blocks over the grid
+    // strip rows (shorter strips for small images measured slower: each
+    // re-reads two halo rows and refills the window)
+    const int strip = kDwStrip;
     dim3 block(tp, tw);
-    dim3 grid(unsigned((g.OW + tw - 1) / tw),
-              unsigned(int64_t(g.N) * ((g.OH + kDwStrip - 1) / kDwStrip)),
+    dim3 grid(unsigned(gx), unsigned(int64_t(g.N) * ((g.OH + strip - 1) / strip)),
               unsigned((np + tp - 1) / tp));
+    auto go = [&](auto kern) { kern<<<grid, block, 0, st>>>(g, range, x, wbase, y, relu, strip); };
     if (V == 2) {
-      k_dw3_nhwc<2><<<grid, block, 0, st>>>(g, range, x, wbase, y, relu);
+      if (OWB == 8) go(k_dw3_nhwc<2, 8>);
+      else if (OWB == 4) go(k_dw3_nhwc<2, 4>);
+      else if (OWB == 2) go(k_dw3_nhwc<2, 2>);
+      else go(k_dw3_nhwc<2, 1>);
     } else {
-      k_dw3_nhwc<1><<<grid, block, 0, st>>>(g, range, x, wbase, y, relu);
+      if (OWB == 4) go(k_dw3_nhwc<1, 4>);
+      else if (OWB == 2) go(k_dw3_nhwc<1, 2>);
+      else go(k_dw3_nhwc<1, 1>);
     }
     return;
   }

@@ -22,7 +22,8 @@ rows = []
 for c, hw in [(64, 56), (128, 28), (256, 14), (512, 7)]:
     shape = Network([Layer(ConvSpec(c, c, hw, hw, 3, 3, 1, 1))], num_classes=10, seed=42)
     sess = nb.Session(shape, nb.make_batch(shape, N, 1), ctx=ctx)
-    for g in sorted({1, 2, 4, 8, 32, c}):
+    # SWEEP_GROUPS=dw: the depthwise points only
+    for g in ([c] if os.environ.get("SWEEP_GROUPS") == "dw" else sorted({1, 2, 4, 8, 32, c})):
         net = Network([Layer(ConvSpec(c, c, hw, hw, 3, 3, 1, 1, groups=g))], num_classes=10, seed=42)
         macs = nb.count_macs(net.layers[0].spec)
         flops = 2.0 * N * macs
