@@ -1148,6 +1148,143 @@ __global__ void __launch_bounds__(256, OWB == 1 ? (V == 1 ? 8 : 4) : (OWB == 2 ?
   }
 }
 
+// dgrad of a depthwise 3x3 stride-1 pad-1 layer on the same register window
+// (thread = a channel pair x OWB input columns of a strip of input rows):
+// g[ih, iw] = sum_{kh,kw} W[kh,kw] * dpre[ih + 1 - kh, iw + 1 - kw], with the
+// fused epilogue of k_dgrad_grouped3 (g_out, the ReLU-masked dpre of the
+// previous layer, A*g partials).  Partials: one per (image, tile, channel),
+// tile = (strip, column-block group); the block's column blocks are summed
+// in threadIdx.y order (deterministic).
+template <int OWB>
+__global__ void __launch_bounds__(256, 2)
+    k_dgrad_dw3(ConvGeom g, const float* __restrict__ dpre, const float* __restrict__ wbase,
+                const float* __restrict__ a_prev, bool relu_prev, float* __restrict__ dpre_out,
+                float* __restrict__ g_out, double* __restrict__ partial, int strip) {
+  constexpr int WW = OWB + 2;
+  __shared__ float2 red[256];
+  const RangeDesc r = g.r[0];
+  const int np = g.Ci / 2;
+  const int p = blockIdx.z * blockDim.x + threadIdx.x;  // channel pair
+  const int iw0 = (blockIdx.x * blockDim.y + threadIdx.y) * OWB;
+  const int strips = (g.H + strip - 1) / strip;
+  const int64_t n = blockIdx.y / strips;
+  const int sidx = int(blockIdx.y % strips);
+  const int ih0 = sidx * strip, ih1 = min(g.H, ih0 + strip);
+  const int c = 2 * p;
+  float2 contrib = make_float2(0.f, 0.f);
+  if (p < np && iw0 < g.W) {
+    const float* __restrict__ wd = wbase + r.wd_off;  // Wd[tap][ci]
+    float2 w[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) w[t] = __ldg(reinterpret_cast<const float2*>(wd + int64_t(t) * g.Ci + c));
+    const int64_t drow = int64_t(g.OW) * g.Co;
+    const float* __restrict__ dn = dpre + n * g.OH * drow + r.b + c;
+    auto ld = [&](int oh, int ow) {
+      return (oh >= 0 && oh < g.OH && ow >= 0 && ow < g.OW)
+                 ? __ldg(reinterpret_cast<const float2*>(dn + oh * drow + int64_t(ow) * g.Co))
+                 : make_float2(0.f, 0.f);
+    };
+    float2 win[3][WW];  // [dpre row - (ih - 1)][dpre column - (iw0 - 1)]
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < WW; ++j) win[i][j] = ld(ih0 - 1 + i, iw0 - 1 + j);
+    for (int ih = ih0; ih < ih1; ++ih) {
+      const int64_t rowi = ((n * g.H + ih) * g.W + iw0) * int64_t(g.Ci) + c;
+      float2 nxt[WW], av[OWB];
+#pragma unroll
+      for (int j = 0; j < WW; ++j) nxt[j] = ih + 1 < ih1 ? ld(ih + 2, iw0 - 1 + j) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < OWB; ++o)
+        av[o] = a_prev && iw0 + o < g.W
+                    ? __ldg(reinterpret_cast<const float2*>(a_prev + rowi + int64_t(o) * g.Ci))
+                    : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < OWB; ++o) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const float2 wv = w[(2 - i) * 3 + (2 - j)];
+            acc.x = fmaf(win[i][o + j].x, wv.x, acc.x);
+            acc.y = fmaf(win[i][o + j].y, wv.y, acc.y);
+          }
+        if (iw0 + o >= g.W) continue;
+        const int64_t idx = rowi + int64_t(o) * g.Ci;
+        if (g_out) *reinterpret_cast<float2*>(g_out + idx) = acc;
+        if (a_prev) {
+          contrib.x = fmaf(av[o].x, acc.x, contrib.x);
+          contrib.y = fmaf(av[o].y, acc.y, contrib.y);
+          if (dpre_out)  // I/nnet.hpp:229-233
+            *reinterpret_cast<float2*>(dpre_out + idx) =
+                make_float2((relu_prev && !(av[o].x > 0.f)) ? 0.f : acc.x,
+                            (relu_prev && !(av[o].y > 0.f)) ? 0.f : acc.y);
+        } else if (dpre_out) {
+          *reinterpret_cast<float2*>(dpre_out + idx) = acc;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < WW; ++j) {
+        win[0][j] = win[1][j];
+        win[1][j] = win[2][j];
+        win[2][j] = nxt[j];
+      }
+    }
+  }
+  if (!partial) return;
+  red[threadIdx.y * blockDim.x + threadIdx.x] = contrib;
+  __syncthreads();
+  if (threadIdx.y == 0 && p < np) {
+    float2 sum = make_float2(0.f, 0.f);
+    for (int k = 0; k < int(blockDim.y); ++k) {
+      sum.x += red[k * blockDim.x + threadIdx.x].x;
+      sum.y += red[k * blockDim.x + threadIdx.x].y;
+    }
+    const int64_t tile = int64_t(sidx) * gridDim.x + blockIdx.x;
+    double* dst = partial + (n * int64_t(strips) * gridDim.x + tile) * g.Ci + c;
+    dst[0] = double(sum.x);
+    dst[1] = double(sum.y);
+  }
+}
+
+// launch shape of the depthwise register-window kernels: channel-group
+// threads x column-block threads, grid (column-block groups, N x strips,
+// channel blocks)
+struct DwShape {
+  dim3 block, grid;
+  int strip, strips, owb;
+};
+DwShape dw3_shape(int64_t N, int OH, int OW, int np, int owb) {
+  DwShape d;
+  const int ncb = (OW + owb - 1) / owb;  // column blocks
+  const int tp = np < 32 ? np : 32;
+  int tw = std::max(1, std::min(256 / tp, ncb));
+  const int gx = (ncb + tw - 1) / tw;
+  tw = (ncb + gx - 1) / gx;  // balance the column blocks over the grid
+  // strip rows (shorter strips for small images measured slower: each
+  // re-reads two halo rows and refills the window)
+  d.strip = kDwStrip;
+  d.strips = (OH + d.strip - 1) / d.strip;
+  d.block = dim3(tp, tw);
+  d.grid = dim3(unsigned(gx), unsigned(N * d.strips), unsigned((np + tp - 1) / tp));
+  d.owb = owb;
+  return d;
+}
+
+bool dw3_dgrad_ok(const ConvGeom& g) {
+  static const bool on = [] {  // NB_DW3_DGRAD=0: the shared-memory halo kernel instead
+    const char* e = std::getenv("NB_DW3_DGRAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || g.nranges != 1) return false;
+  const RangeDesc& r = g.r[0];
+  return r.b == 0 && r.len == g.Co && g.Ci == g.Co && r.groups == r.len && r.slice_ci == 1 &&
+         r.slice_co == 1 && g.KH == 3 && g.KW == 3 && g.S == 1 && g.P == 1 && g.Ci % 2 == 0 &&
+         g.H == g.OH && g.W == g.OW;
+}
+constexpr int kDwDgradOwb = 4;
+
 bool dw3_ok(const ConvGeom& g, const RangeDesc& r) {
   static const bool on = [] {  // NB_DW3=0: the shared-memory halo kernel instead
     const char* e = std::getenv("NB_DW3");
@@ -1174,19 +1311,8 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
       const int v = e ? std::atoi(e) : 8;
       return v == 1 || v == 2 || v == 4 ? v : 8;
     }();
-    const int np = r.len / V;
-    const int ncb = (g.OW + OWB - 1) / OWB;  // column blocks
-    const int tp = np < 32 ? np : 32;
-    int tw = std::max(1, std::min(256 / tp, ncb));
-    const int gx = (ncb + tw - 1) / tw;
-    tw = (ncb + gx - 1) / gx;  // balance the column blocks over the grid
-    // strip rows (shorter strips for small images measured slower: each
-    // re-reads two halo rows and refills the window)
-    const int strip = kDwStrip;
-    dim3 block(tp, tw);
-    dim3 grid(unsigned(gx), unsigned(int64_t(g.N) * ((g.OH + strip - 1) / strip)),
-              unsigned((np + tp - 1) / tp));
-    auto go = [&](auto kern) { kern<<<grid, block, 0, st>>>(g, range, x, wbase, y, relu, strip); };
+    const DwShape d = dw3_shape(g.N, g.OH, g.OW, r.len / V, OWB);
+    auto go = [&](auto kern) { kern<<<d.grid, d.block, 0, st>>>(g, range, x, wbase, y, relu, d.strip); };
     if (V == 2) {
       if (OWB == 8) go(k_dw3_nhwc<2, 8>);
       else if (OWB == 4) go(k_dw3_nhwc<2, 4>);
@@ -1271,6 +1397,10 @@ bool dgrad_grouped3_ok(const ConvGeom& g) {
 }
 
 int direct_dgrad_tiles(const ConvGeom& g) {
+  if (dw3_dgrad_ok(g)) {
+    const DwShape d = dw3_shape(g.N, g.H, g.W, g.Ci / 2, kDwDgradOwb);
+    return d.strips * int(d.grid.x);
+  }
   if (dgrad_grouped3_ok(g)) {
     const GTile T = gtile(g.H, g.W);
     return ((g.H + T.th - 1) / T.th) * ((g.W + T.tw - 1) / T.tw);
@@ -1281,6 +1411,12 @@ int direct_dgrad_tiles(const ConvGeom& g) {
 void launch_dgrad_direct(const ConvGeom& g, const float* dpre, const float* wbase,
                          const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                          double* partial, cudaStream_t st) {
+  if (dw3_dgrad_ok(g)) {
+    const DwShape d = dw3_shape(g.N, g.H, g.W, g.Ci / 2, kDwDgradOwb);
+    k_dgrad_dw3<kDwDgradOwb><<<d.grid, d.block, 0, st>>>(g, dpre, wbase, a_prev, relu_prev,
+                                                         dpre_out, g_out, partial, d.strip);
+    return;
+  }
   if (dgrad_grouped3_ok(g)) {
     const size_t smem = dgrad_grouped3_smem(g);
     dim3 grid(direct_dgrad_tiles(g), g.N, (g.Ci + 31) / 32);
