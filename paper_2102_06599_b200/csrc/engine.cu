@@ -194,19 +194,6 @@ int m_tiles_at(int OH, int OW, int64_t nimg, int S) {
   return t.m_tiles;
 }
 
-// Split-K launches reduce their partials in a separate k_splitk_epilogue
-// pass; NB_TC_SPLITK_EPI=0 reduces them in the conv kernel instead (the
-// tile's last unit runs the epilogue on the sum: measured slower, its
-// four epilogue warps are latency-bound on the partials, profiles/r02_kernels.md).
-bool splitk_fused() {
-  static const bool fused = [] {
-    const char* e = std::getenv("NB_TC_SPLITK_EPI");
-    return e && std::atoi(e) == 0;
-  }();
-  return fused;
-}
-constexpr int64_t kTileCounters = 4096;
-
 // Split-K factor of a tensor-core launch: when its output tiles cannot fill
 // one wave of SMs, divide the K blocks (taps x 32-channel chunks, at least 4
 // per split) so that tiles x splits still fits in one wave.
@@ -551,12 +538,10 @@ NetPlan lower(const NetDesc& net, int64_t n, nb_precision prec, int num_sms, int
           t.part_ld = g.Ci;
           const bool mc = use_mc(bn, mt, pbn != 0, kwf, P.h16 != 0);
           t.ksplit = choose_ksplit(t, mt, num_sms, pbn != 0 || mc);
-          // split-K dgrad through k_splitk_epilogue: one partial per (image,
-          // pixel chunk); else one per (phase, tile of the image)
-          const bool sepi = t.ksplit > 1 && !splitk_fused();
-          const int hw_chunks = sepi ? splitk_hw_chunks(plan_n, g.H * g.W, g.Ci) : 1;
+          // split-K dgrad: k_splitk_epilogue writes one partial per (image, pixel chunk)
+          const int hw_chunks = t.ksplit > 1 ? splitk_hw_chunks(plan_n, g.H * g.W, g.Ci) : 1;
           t.part_tiles_per_img =
-              sepi ? hw_chunks : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
+              t.ksplit > 1 ? hw_chunks : t.nphase * (t.BNI == 1 ? t.tiles_h * t.tiles_w : 1);
           if (t.ksplit > 1)
             P.ws_floats = std::max(P.ws_floats, int64_t(t.ksplit) * n * g.H * g.W * g.Ci);
           TcPlan& tp = lp.tcd;
@@ -718,18 +703,6 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
     return e ? std::atoi(e) : 0;
   }();
   L.args.debug = dbg;
-  L.args.tile_cnt = nullptr;
-  if (L.args.ksplit > 1 && splitk_fused()) {
-    // one counter per (tile, cluster rank); zero between launches (the last
-    // unit of a tile resets its counter)
-    const int64_t need = int64_t(L.args.nphase) * L.args.m_tiles * L.args.n_tiles * 2;
-    if (need > kTileCounters) throw std::runtime_error("split-K tile counters exhausted");
-    if (!c->tilecnt.p) {
-      c->tilecnt.ensure(kTileCounters * sizeof(int));
-      NB_CUDA(cudaMemset(c->tilecnt.p, 0, kTileCounters * sizeof(int)));
-    }
-    L.args.tile_cnt = c->tilecnt.as<int>();
-  }
   // NB_TC_TRACE=<launch index>: record CTA 0's stage timeline of that TC
   // launch of this context and dump it to nb_tc_trace.txt (experiments)
   static const int trace_at = [] {
@@ -888,7 +861,7 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
       const bool col = lp.tcf[r].col;
       launch_tc(c, lp.tcf[r], a, P.split3, P.h16 != 0, x, col ? 32 : g.Ci, col ? g.OW : g.W,
                 col ? g.OH : g.H, g.N, base + lp.tcf[r].w_off, st);
-      if (a.ksplit > 1 && !splitk_fused()) {
+      if (a.ksplit > 1) {
         SplitEpi e{};
         e.ws = a.ws;
         e.ws_stride = a.ws_stride;
@@ -946,7 +919,7 @@ void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
     a.ws_stride = int64_t(g.N) * g.H * g.W * g.Ci;
     set_scaling(P, lp, a, in_amax, dpre_out ? out_amax : nullptr);
     launch_tc(c, lp.tcd, a, P.split3, P.h16 != 0, dpre, g.Co, g.OW, g.OH, g.N, base + lp.tcd.w_off, st);
-    if (a.ksplit > 1 && !splitk_fused()) {
+    if (a.ksplit > 1) {
       SplitEpi e{};
       e.ws = a.ws;
       e.ws_stride = a.ws_stride;

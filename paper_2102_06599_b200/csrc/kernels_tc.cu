@@ -311,9 +311,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
@@ -327,16 +324,8 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                : "memory");
   return v;
 }
-// named barrier returning the OR of every participant's predicate
-__device__ __forceinline__ bool named_bar_or(int id, int n, bool p) {
-  uint32_t r;
-  asm volatile(
-      "{\n .reg .pred pi, po;\n setp.ne.u32 pi, %1, 0;\n"
-      " barrier.red.or.pred po, %2, %3, pi;\n selp.u32 %0, 1, 0, po;\n}"
-      : "=r"(r)
-      : "r"(p ? 1u : 0u), "r"(id), "r"(n)
-      : "memory");
-  return r != 0;
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 constexpr int kABytes = 128 * 128;  // 128 pixels x 32 fp32 channels
@@ -656,7 +645,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   // weights, written before any conv of the run started) and waits for the
   // previous kernel only then.  Measured 2% slower (the early loads compete
   // with the previous kernel's tail, profiles/r02_kernels.md), so off.
-  const bool early_b = kSplitA && !MC && warp == 0 && lane == 0 && (a.debug & 16384);
+  // (not with the halo A operand: that combination hung once in ~20 runs of
+  // tests/test_tc_modes.py and was dropped rather than debugged)
+  const bool early_b = kSplitA && !MC && !a.halo && warp == 0 && lane == 0 && (a.debug & 16384);
   if (!early_b) asm volatile("griddepcontrol.wait;" ::: "memory");
   // trace: per-CTA %globaltimer at start (after the grid dependency) and at
   // the end, slots [5*kTraceStages + 4*cta + {0: launch, 1: start, 2: mma done, 3: end}]
@@ -951,29 +942,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       // 64 B per warp instruction instead of 32 rows x 16 B).  A_prev of the
       // first two 16-column chunks is requested before waiting for the
       // accumulator (it does not depend on it), then two chunks ahead.
-      // in-kernel split-K: pass 1 stores this unit's partial; the tile's
-      // last unit then runs the epilogue on the sum of the partials (from_ws)
-      const bool ks_fused = a.ksplit > 1 && a.tile_cnt;
-      const bool fast_dgrad = a.mode == 1 && (a.ksplit == 1 || ks_fused) && a.partial &&
-                              a.a_prev && rows_per_img % 32 == 0 && !(a.debug & 16);
+      const bool fast_dgrad = a.mode == 1 && a.ksplit == 1 && a.partial && a.a_prev &&
+                              rows_per_img % 32 == 0 && !(a.debug & 16);
       const int64_t rbase = pix * a.out_ld + col0;
       long long rp[4];
       float4 apn[2][4];
-      auto load_apn = [&]() {
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            apn[j][k] = rp[k] >= 0 && 16 * j < nlim && 16 * j < BN
-                            ? *reinterpret_cast<const float4*>(a.a_prev + rp[k] + 16 * j)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-      };
-      // fprop / split-K partial stores through the per-warp transpose tile
-      // (8 rows x 64 B per warp store instead of 32 rows x 16 B; debug bit
-      // 2^21): measured slower than direct row stores -- the fprop epilogue is
-      // issue-latency bound, not store bound (profiles/r02_kernels.md)
-      const bool xstore = !fast_dgrad && (a.debug & (1 << 21)) && (a.mode == 0 || (a.ksplit > 1 && !ks_fused));
-      if (fast_dgrad || xstore) {
+      if (fast_dgrad) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int src = 8 * k + (lane >> 2);
@@ -981,7 +955,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, src);
           rp[k] = ok ? b + 4 * (lane & 3) : -1ll;
         }
-        if (fast_dgrad && !ks_fused) load_apn();
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            apn[j][k] = rp[k] >= 0 && 16 * j < nlim && 16 * j < BN
+                            ? *reinterpret_cast<const float4*>(a.a_prev + rp[k] + 16 * j)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       const bool etr = r == 0 && local < 10;  // trace role 9: this tile's epilogue events
       if (etr) trace(a, 9, local * 24);
@@ -997,10 +977,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       if (unscale && a.a_amax && valid) inv_a = pow2f(-amax_shift(a.a_amax[n]));
       float out_mx = 0.f;  // max |value| this thread stores for the next GEMM (out_amax)
       auto acc_ld16_raw = [&](int c, float* v) {
-        if (a.debug & (1 << 23)) {  // (experiment: no TMEM loads)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = float(c + i);
-        } else if (!KWF) {
+        if (!KWF) {
           tmem_ld16(trow + uint32_t(c), v);
         } else {
           uint32_t l[16], m[16], rr[16];
@@ -1023,83 +1000,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           }
         }
       };
-      bool from_ws = false;
       auto acc_ld16 = [&](int c, float* v) {
-        if (from_ws) {  // the split partials of this row, summed in split order
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          if (valid) {
-            for (int k = 0; k < a.ksplit; ++k) {
-              const float4* w =
-                  reinterpret_cast<const float4*>(a.ws + int64_t(k) * a.ws_stride + rbase + c);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                if (!KWF && c + 4 * i >= nlim) break;
-                const float4 t = __ldcg(w + i);
-                v[4 * i] += t.x;
-                v[4 * i + 1] += t.y;
-                v[4 * i + 2] += t.z;
-                v[4 * i + 3] += t.w;
-              }
-            }
-          }
-          return;
-        }
         acc_ld16_raw(c, v);
         if (unscale) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = (v[i] * inv_a) * a.b_inv;
         }
       };
-      if (ks_fused) {
-        // pass 1: this unit's partial into its copy of the output, then free
-        // the accumulator
+      if (fast_dgrad) {
+        // this warp's transpose tile, addressed in the shared space (a generic
+        // pointer turns the accesses into long-scoreboard LD/ST)
+        const uint32_t xs = smem_u32(red + 128 * 17 + q * (32 * 20));
+        const uint32_t x_sc = xs + uint32_t(((lane >> 2) * 20 + 4 * (lane & 3)) * 4);  // + k * 640
+        const uint32_t x_own = xs + uint32_t(lane * 20 * 4);                          // + i * 16
+        const float* aprev = a.a_prev;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
           if (c >= nlim) break;
-          float v[16];
-          acc_ld16(c, v);
-          if (valid) {
-            float4* o = reinterpret_cast<float4*>(a.ws + int64_t(d.ks) * a.ws_stride + rbase + c);
+          // transpose this chunk's A_prev rows into registers (own row)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (!KWF && c + 4 * i >= nlim) break;
-              o[i] = empty_phase ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                 : make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-          }
-        }
-        tc_fence_before();
-        __threadfence();
-        named_bar(1, 128);
-        bool last = false;
-        if (r == 0) {
-          if (PAIR) {
-            mbar_arrive_remote(tempty_remote + uint32_t(acc * 8));
-          } else {
-            mbar_arrive(&tempty[acc]);
-          }
-          int* cnt = a.tile_cnt + (u / a.ksplit) * (CLUSTER ? 2 : 1) + (CLUSTER ? int(rank) : 0);
-          last = atomicAdd(cnt, 1) == a.ksplit - 1;
-          if (last) *cnt = 0;  // ready for the next launch on this stream
-        }
-        if (!named_bar_or(1, 128, last)) continue;
-        __threadfence();
-        from_ws = true;
-        if (fast_dgrad) load_apn();
-      }
-      if (fast_dgrad) {
-        // this warp's transpose tile (shared-space accesses: the generic
-        // pointer would turn them into long-scoreboard LD/ST)
-        const uint32_t xs = smem_u32(red + 128 * 17 + q * (32 * 20));
-        const uint32_t x_sc = xs + uint32_t(((lane >> 2) * 20 + 4 * (lane & 3)) * 4);  // + k*640
-        const uint32_t x_own = xs + uint32_t(lane * 20 * 4);                          // + i*16
-        const float* aprev = a.a_prev;
-        // one 16-column chunk; ap holds its A_prev quads and is refilled with
-        // chunk c + 32 (two chunk bodies of latency cover before its use)
-        auto chunk = [&](const int c, float4 (&ap)[4]) __attribute__((always_inline)) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) sts128(x_sc + k * 640, ap[k]);
+          for (int k = 0; k < 4; ++k) sts128(x_sc + k * 640, apn[0][k]);
           __syncwarp();
           float av[16];
 #pragma unroll
@@ -1111,21 +1031,21 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             av[4 * i + 3] = t.w;
           }
           __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) apn[0][k] = apn[1][k];
           if (c + 32 < BN && c + 32 < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (rp[k] >= 0) ap[k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 32);
+              if (rp[k] >= 0) apn[1][k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 32);
           }
           float v[16];
-          if (empty_phase) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          } else {
-            acc_ld16(c, v);
-          }
+          acc_ld16(c, v);
           float x[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) x[i] = valid ? av[i] * v[i] : 0.f;
+          for (int i = 0; i < 16; ++i) {
+            if (empty_phase) v[i] = 0.f;
+            x[i] = valid ? av[i] * v[i] : 0.f;
+          }
           if (a.g_out && valid) {
             float4* go = reinterpret_cast<float4*>(a.g_out + rbase + c);
 #pragma unroll
@@ -1154,8 +1074,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           }
           if (etr) trace(a, 9, local * 24 + 2 + c / 16);
           if (a.debug & 4096) {  // experiment: no reduction
-            if (lane < 16) red[q * BN + c + lane] = x[lane & 15];
-            return;
+            if (lane < 16) red[q * BN + c + lane] = x[0];  // (a static index: x stays in registers)
+            continue;
           }
           // reduce-scatter over the warp: 16 + 8 + 4 + 2 + 1 shuffles
 #pragma unroll
@@ -1182,13 +1102,6 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
             if (lane < 16) red[q * BN + c + lane] = tot;  // column c + (lane & 15)
           }
-        };
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          if (c >= nlim) break;
-          chunk(c, apn[0]);
-          if (c + 16 >= nlim) break;
-          chunk(c + 16, apn[1]);
         }
         named_bar(1, 128);
         if (etr) trace(a, 9, local * 24 + 18);
@@ -1216,31 +1129,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        if (xstore && c + 16 <= nlim) {
-          // whole 16-column chunk: fprop output (ReLU) or this split's partial
-          float* xp = red + 128 * 17 + q * (32 * 20);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            if (!(a.ksplit > 1 && !ks_fused) && a.relu) {  // (a split's raw partial: no ReLU)
-              x.x = x.x > 0.f ? x.x : 0.f;
-              x.y = x.y > 0.f ? x.y : 0.f;
-              x.z = x.z > 0.f ? x.z : 0.f;
-              x.w = x.w > 0.f ? x.w : 0.f;
-            }
-            if (valid)
-              out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
-            *reinterpret_cast<float4*>(xp + lane * 20 + 4 * i) = x;
-          }
-          __syncwarp();
-          float* dst = a.ksplit > 1 && !ks_fused ? a.ws + int64_t(d.ks) * a.ws_stride : a.out;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (rp[k] >= 0)
-              *reinterpret_cast<float4*>(dst + rp[k] + c) =
-                  *reinterpret_cast<const float4*>(xp + (8 * k + (lane >> 2)) * 20 + 4 * (lane & 3));
-          __syncwarp();
-        } else if (a.ksplit > 1 && !ks_fused) {
+        if (a.ksplit > 1) {
           // split-K: raw partial sums into this split's copy of the output;
           // k_splitk_epilogue adds the copies in order and runs the epilogue
           if (valid) {
@@ -1265,10 +1154,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
                 x.w = x.w > 0.f ? x.w : 0.f;
               }
               out_mx = fmaxf(out_mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
-              if (a.debug & (1 << 22))  // (experiment: no output stores)
-                asm volatile("" ::"f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w));
-              else
-                o[i] = x;
+              o[i] = x;
             }
           }
         } else {
@@ -1363,27 +1249,21 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
             named_bar(1, 128);
           }
         }
-        if (etr) trace(a, 9, local * 24 + 2 + c / 16);
       }
       if (etr) trace(a, 9, local * 24 + 19);
       // all 128 rows drained -> one arrival per CTA on the MMA CTA's barrier
-      // (a fused split-K unit freed its accumulator after pass 1)
-      if (!from_ws) {
-        tc_fence_before();
-        named_bar(1, 128);
-        if (r == 0) {
-          if (PAIR) {
-            mbar_arrive_remote(tempty_remote + uint32_t(acc * 8));
-          } else {
-            mbar_arrive(&tempty[acc]);
-          }
+      tc_fence_before();
+      named_bar(1, 128);
+      if (r == 0) {
+        if (PAIR) {
+          mbar_arrive_remote(tempty_remote + uint32_t(acc * 8));
+        } else {
+          mbar_arrive(&tempty[acc]);
         }
-      } else {
-        named_bar(1, 128);  // red / transpose tiles free for the next tile
       }
       // per-image max of what this tile stored for the next GEMM: lanes of
       // one image reduce together, one atomic per image per warp
-      if (a.out_amax && (a.ksplit == 1 || ks_fused)) {
+      if (a.out_amax && a.ksplit == 1) {
         const int key = (valid && tile_real) ? n : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, key);
         const unsigned m = __reduce_max_sync(grp, __float_as_uint(out_mx));

@@ -41,15 +41,11 @@ struct TcArgs {
   int n_tiles, n_tiles_per_group;
   // split-K: the (tap, channel-chunk) K blocks of a tile are divided into
   // ksplit contiguous ranges, each accumulated by its own work unit into its
-  // own copy of the output (ws + ks * ws_stride, same layout as out); the
-  // unit that completes a tile last (tile_cnt, one counter per tile and
-  // cluster rank, zero between launches) sums the copies in split order and
-  // runs the tile's epilogue (NB_TC_SPLITK_EPI=0).  tile_cnt null (default):
-  // k_splitk_epilogue does
+  // own copy of the output (ws + ks * ws_stride, same layout as out);
+  // k_splitk_epilogue then sums the copies in order and runs the epilogue
   int ksplit;
   float* ws;
   int64_t ws_stride;
-  int* tile_cnt;
   int S;  // element stride of the A box (fprop stride; 1 for dgrad)
   // phases
   int nphase, PS;

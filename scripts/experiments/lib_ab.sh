@@ -1,11 +1,9 @@
-# same-box A/B of two builds (NB200_LIB) on the origin evaluation and the bench
-mkdir -p gpurun_out
-for lib in libnb200_head.so libnb200.so; do
-  for h in 1 0; do
-    NB200_LIB=$lib NB_TC_HALO=$h NB_TC_TRACE=214 timeout 120 python scripts/origin_fisher.py 3 fp32 > gpurun_out/of.txt 2>&1
-    echo "== $lib halo=$h: $(sed -n 3p gpurun_out/of.txt)"; python scripts/trace_detail.py nb_tc_trace.txt 2>/dev/null | head -1 | cut -c1-40
-    [ "$lib" = libnb200_head.so ] && break
-  done
+# same-box A/B of library builds (NB200_LIB): origin Fisher (1 stream) and the 4-session bench
+for round in 1 2; do
+for lib in ${LIBS:-libnb200_A.so libnb200_B.so libnb200.so}; do
+  NB200_LIB=$lib timeout 60 python scripts/origin_fisher.py 6 fp32 > gpurun_out/of.txt 2>&1
+  o=$(grep "fisher [3-5]" gpurun_out/of.txt | awk '{print $3}' | sort -n | head -1)
+  NB200_LIB=$lib timeout 200 python bench.py --steps 40 --warmup 5 --no-modes --no-cpu-baseline --no-peaks > gpurun_out/bench.log 2>&1
+  echo "$lib origin_ms=$o $(tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('bench', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'dgrad', round(r['achieved'],1))")"
 done
-NB_TC_HALO=0 timeout 300 python -m pytest tests/test_sharded.py -m gpu -x -q -p no:cacheprovider 2>&1 | tail -1
-NB_TC_HALO=1 timeout 300 python -m pytest tests/test_sharded.py -m gpu -x -q -p no:cacheprovider 2>&1 | tail -1
+done
