@@ -190,6 +190,23 @@ __device__ __forceinline__ void split_f16x2(uint32_t x0, uint32_t x1, float sA, 
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "r"(l1), "r"(l0));
 }
 
+// packed fp32x2 arithmetic (same rounding as the scalar instructions)
+__device__ __forceinline__ void mul2s(float& a, float& b, float s) {
+  asm("{\n\t.reg .b64 xx, ss;\n\tmov.b64 xx, {%0, %1};\n\tmov.b64 ss, {%2, %2};\n\t"
+      "mul.rn.f32x2 xx, xx, ss;\n\tmov.b64 {%0, %1}, xx;\n\t}"
+      : "+f"(a), "+f"(b) : "f"(s));
+}
+__device__ __forceinline__ void mul2(float& a, float& b, float c, float d) {
+  asm("{\n\t.reg .b64 xx, yy;\n\tmov.b64 xx, {%0, %1};\n\tmov.b64 yy, {%2, %3};\n\t"
+      "mul.rn.f32x2 xx, xx, yy;\n\tmov.b64 {%0, %1}, xx;\n\t}"
+      : "+f"(a), "+f"(b) : "f"(c), "f"(d));
+}
+__device__ __forceinline__ void add2(float& a, float& b, float c, float d) {
+  asm("{\n\t.reg .b64 xx, yy;\n\tmov.b64 xx, {%0, %1};\n\tmov.b64 yy, {%2, %3};\n\t"
+      "add.rn.f32x2 xx, xx, yy;\n\tmov.b64 {%0, %1}, xx;\n\t}"
+      : "+f"(a), "+f"(b) : "f"(c), "f"(d));
+}
+
 // The fp16 split's per-image scale 2^k, k = 14 - e (e = exponent of the
 // image's max |A|, so |A 2^k| < 2^15), and its inverse; 1 when the max is 0
 // or absent.
@@ -975,15 +992,19 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       constexpr bool unscale = F16;
       float inv_a = 1.f;
       if (unscale && a.a_amax && valid) inv_a = pow2f(-amax_shift(a.a_amax[n]));
+      const float unsc = inv_a * a.b_inv;  // both powers of two: one exact scale
+      const bool warp_valid = __all_sync(0xffffffffu, valid);  // (the common case: no selects)
       float out_mx = 0.f;  // max |value| this thread stores for the next GEMM (out_amax)
       auto acc_ld16_raw = [&](int c, float* v) {
         if (!KWF) {
           tmem_ld16(trow + uint32_t(c), v);
         } else {
+          // the neighbours' column blocks chosen by TMEM address (no per-value selects)
           uint32_t l[16], m[16], rr[16];
-          tmem_ld16_nw(trow + uint32_t(c), l);
+          const bool fwd0 = a.kwf_sgn > 0;
+          tmem_ld16_nw(trow + uint32_t((fwd0 ? 0 : 2 * BN) + c), l);
           tmem_ld16_nw(trow + uint32_t(BN + c), m);
-          tmem_ld16_nw(trow + uint32_t(2 * BN + c), rr);
+          tmem_ld16_nw(trow + uint32_t((fwd0 ? 2 * BN : 0) + c), rr);
           tmem_wait_ld();
           // fprop (sgn +1): out(w) = D0(w-1) + D1(w) + D2(w+1); dgrad: D0(w+1) + D1(w) + D2(w-1);
           // w = the lane's position in its image-row segment of kwf_w lanes
@@ -991,8 +1012,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           const int kw_lane = lane & (a.kwf_w - 1);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float left_src = __uint_as_float(fwd ? l[i] : rr[i]);
-            const float right_src = __uint_as_float(fwd ? rr[i] : l[i]);
+            const float left_src = __uint_as_float(l[i]);
+            const float right_src = __uint_as_float(rr[i]);
             const float from_left = __shfl_up_sync(0xffffffffu, left_src, 1, a.kwf_w);
             const float from_right = __shfl_down_sync(0xffffffffu, right_src, 1, a.kwf_w);
             v[i] = __uint_as_float(m[i]) + (kw_lane > 0 ? from_left : 0.f) +
@@ -1004,7 +1025,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         acc_ld16_raw(c, v);
         if (unscale) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (v[i] * inv_a) * a.b_inv;
+          for (int i = 0; i < 16; i += 2) mul2s(v[i], v[i + 1], unsc);
         }
       };
       if (fast_dgrad) {
@@ -1042,9 +1063,17 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           acc_ld16(c, v);
           float x[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 16; ++i)
             if (empty_phase) v[i] = 0.f;
-            x[i] = valid ? av[i] * v[i] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            x[i] = av[i];
+            x[i + 1] = av[i + 1];
+            mul2(x[i], x[i + 1], v[i], v[i + 1]);
+          }
+          if (!warp_valid) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = valid ? x[i] : 0.f;
           }
           if (a.g_out && valid) {
             float4* go = reinterpret_cast<float4*>(a.g_out + rbase + c);
