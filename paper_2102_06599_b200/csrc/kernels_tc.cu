@@ -478,7 +478,11 @@ struct Cfg {
   // float transpose tile per epilogue warp (coalesced A_prev / dpre rows)
   static constexpr int kXposeBytes = 4 * 32 * 20 * 4;
   static constexpr int kRedBytes = 128 * 17 * 4 + kXposeBytes;
-  static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes + 512;
+  // kw-fused 16-bit-split tiles: the MMA (N = 3 x BN) outlasts one converter
+  // group, and the epilogue (three accumulator blocks per chunk) outlasts the
+  // mainloop -- the second converter group runs a second epilogue column group
+  static constexpr int kEpiGroups = (SPLIT3 && KWF && BF && kConvGroups == 2) ? 2 : 1;
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + kRedBytes * kEpiGroups + 512;
   // halo buffer capacity (bytes) of halo mode (TcArgs::halo)
 #ifndef NB_TC_INTERLEAVED
   static constexpr int halo_cap() { return (kStages / 2) * kABytes; }
@@ -554,7 +558,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
 #endif
   auto halo_buf = [&](int h) { return smem + h * (C::kStages / 2) * kABytes; };
   float* red = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kRedBytes);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kRedBytes * C::kEpiGroups);
   uint64_t* full = bars;            // S: this CTA's TMA bytes landed
   uint64_t* ready = bars + S;       // ST: TMEM A slot ready for the MMA (split A in TMEM /
                                     //     both CTAs' data landed) -- MMA CTA's copy
@@ -579,7 +584,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
   const bool halo = kSplitA && a.halo;
   // channel-halves conversion (two groups per stage) needs exactly two groups
   // (two alternating groups need even rings: an odd ring converts by halves)
-  const bool halves_on = SPLIT3 && C::kConvGroups == 2 && (a.conv_halves != 0 || (S & 1) || (ST & 1));
+  // two epilogue column groups (kw-fused 16-bit splits; debug bit 2^21: off):
+  // one converter group converts every stage
+  // (dgrad only: the fprop epilogue is lighter than one converter group's
+  // mainloop and loses from it)
+  const bool epi2 = C::kEpiGroups == 2 && a.mode == 1 && !(a.debug & (1 << 21));
+  const bool halves_on = SPLIT3 && C::kConvGroups == 2 && !epi2 &&
+                         (a.conv_halves != 0 || (S & 1) || (ST & 1));
 
   // Role of each warp.  An SM sub-partition issues from its eligible warps
   // highest-warp-id first, so the single MMA-issuing thread sits in the
@@ -621,9 +632,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kCtas);
+      mbar_init(&tempty[i], kCtas * (epi2 ? 2 : 1));
       mbar_init(&halo_full[i], 1);
-      mbar_init(&halo_empty[i], G4);  // every converter warp releases every chunk
+      mbar_init(&halo_empty[i], epi2 ? 4 : G4);  // every converter warp releases every chunk
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -926,9 +937,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------- epilogue (TMEM lanes 32*(warp-4) .. +31)
-    const int q = warp - 4;
+  } else if ((warp >= 4 && warp < 8) || (epi2 && warp >= 12)) {
+    // ---------------- epilogue (TMEM lanes 32*(warp%4) .. +31); with epi2 the
+    // second converter group's warps are a second column group taking every
+    // other 16-column chunk (own scratch and named barrier; both release the
+    // accumulator)
+    const int gi = warp >= 12 ? 1 : 0, G = epi2 ? 2 : 1;
+    const int c0g = 16 * gi, cs = 16 * G, bid = 1 + gi;
+    float* const red_g = gi ? red + C::kRedBytes / 4 : red;
+    const int q = warp & 3;
     const int r = q * 32 + lane;  // accumulator row == TMEM lane
     const int rows_per_img = a.BW * a.BH;
     const int part_per_phase = a.BNI == 1 ? a.tiles_h * a.tiles_w : 1;
@@ -976,11 +993,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            apn[j][k] = rp[k] >= 0 && 16 * j < nlim && 16 * j < BN
-                            ? *reinterpret_cast<const float4*>(a.a_prev + rp[k] + 16 * j)
+            apn[j][k] = rp[k] >= 0 && c0g + cs * j < nlim && c0g + cs * j < BN
+                            ? *reinterpret_cast<const float4*>(a.a_prev + rp[k] + c0g + cs * j)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      const bool etr = r == 0 && local < 10;  // trace role 9: this tile's epilogue events
+      const bool etr = r == 0 && gi == 0 && local < 10;  // trace role 9: this tile's epilogue events
       if (etr) trace(a, 9, local * 24);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
@@ -1031,12 +1048,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
       if (fast_dgrad) {
         // this warp's transpose tile, addressed in the shared space (a generic
         // pointer turns the accesses into long-scoreboard LD/ST)
-        const uint32_t xs = smem_u32(red + 128 * 17 + q * (32 * 20));
+        const uint32_t xs = smem_u32(red_g + 128 * 17 + q * (32 * 20));
         const uint32_t x_sc = xs + uint32_t(((lane >> 2) * 20 + 4 * (lane & 3)) * 4);  // + k * 640
         const uint32_t x_own = xs + uint32_t(lane * 20 * 4);                          // + i * 16
         const float* aprev = a.a_prev;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
+        for (int c = c0g; c < BN; c += cs) {
           if (c >= nlim) break;
           // transpose this chunk's A_prev rows into registers (own row)
 #pragma unroll
@@ -1054,10 +1071,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           __syncwarp();
 #pragma unroll
           for (int k = 0; k < 4; ++k) apn[0][k] = apn[1][k];
-          if (c + 32 < BN && c + 32 < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
+          if (c + 2 * cs < BN && c + 2 * cs < nlim && !(a.debug & 2048)) {  // (debug 2048: no A_prev loads)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (rp[k] >= 0) apn[1][k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 32);
+              if (rp[k] >= 0) apn[1][k] = *reinterpret_cast<const float4*>(aprev + rp[k] + c + 2 * cs);
           }
           float v[16];
           acc_ld16(c, v);
@@ -1103,7 +1120,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           }
           if (etr) trace(a, 9, local * 24 + 2 + c / 16);
           if (a.debug & 4096) {  // experiment: no reduction
-            if (lane < 16) red[q * BN + c + lane] = x[0];  // (a static index: x stays in registers)
+            if (lane < 16) red_g[q * BN + c + lane] = x[0];  // (a static index: x stays in registers)
             continue;
           }
           // reduce-scatter over the warp: 16 + 8 + 4 + 2 + 1 shuffles
@@ -1129,28 +1146,29 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           {
             const float send = b0 ? w2[0] : w2[1], keep = b0 ? w2[1] : w2[0];
             const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-            if (lane < 16) red[q * BN + c + lane] = tot;  // column c + (lane & 15)
+            if (lane < 16) red_g[q * BN + c + lane] = tot;  // column c + (lane & 15)
           }
         }
-        named_bar(1, 128);
+        named_bar(bid, 128);
         if (etr) trace(a, 9, local * 24 + 18);
         if (tile_real) {
           const int wpi = rows_per_img / 32;
           for (int idx = r; idx < a.BNI * BN; idx += 128) {
             const int img = idx / BN, j = idx % BN;
+            if (((j >> 4) % G) != gi) continue;  // the other group's columns
             const int nimg = nb * a.BNI + img;
             if (nimg < a.nimg && j < nlim) {
               float sum = 0.f;
-              for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red[w * BN + j];
+              for (int w = img * wpi; w < (img + 1) * wpi; ++w) sum += red_g[w * BN + j];
               a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld + col0 +
                         j] = double(sum);
             }
           }
         }
-        named_bar(1, 128);
+        named_bar(bid, 128);
       }
 #pragma unroll 1
-      for (int c = 0; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += 16) {  // (debug 16: no epilogue)
+      for (int c = c0g; c < ((a.debug & 16) || fast_dgrad ? 0 : BN); c += cs) {  // (debug 16: no epilogue)
         if (c >= nlim) break;
         float v[16];
         acc_ld16(c, v);
@@ -1244,45 +1262,45 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
               for (int o = 16; o; o >>= 1) contrib[i] += __shfl_xor_sync(0xffffffffu, contrib[i], o);
             if (lane == 0) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) red[q * 17 + i] = contrib[i];
+              for (int i = 0; i < 16; ++i) red_g[q * 17 + i] = contrib[i];
             }
-            named_bar(1, 128);
+            named_bar(bid, 128);
             const int wpi = rows_per_img / 32;
             if (r < a.BNI * 16) {
               const int img = r / 16, j = r % 16;
               const int nimg = nb * a.BNI + img;
               if (nimg < a.nimg) {
                 float s = 0.f;
-                for (int w = img * wpi; w < (img + 1) * wpi; ++w) s += red[w * 17 + j];
+                for (int w = img * wpi; w < (img + 1) * wpi; ++w) s += red_g[w * 17 + j];
                 a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
                           col0 + c + j] = double(s);
               }
             }
-            named_bar(1, 128);
+            named_bar(bid, 128);
           } else if (a.partial && tile_real) {
             // small images (several per tile): serial sums over each image's rows
 #pragma unroll
-            for (int i = 0; i < 16; ++i) red[r * 17 + i] = contrib[i];
-            named_bar(1, 128);
+            for (int i = 0; i < 16; ++i) red_g[r * 17 + i] = contrib[i];
+            named_bar(bid, 128);
             for (int wi2 = r; wi2 < a.BNI * 16; wi2 += 128) {
               const int img = wi2 / 16, j = wi2 % 16;
               const int nimg = nb * a.BNI + img;
               if (nimg < a.nimg) {
                 float s = 0.f;
                 for (int rr = img * rows_per_img; rr < (img + 1) * rows_per_img; ++rr)
-                  s += red[rr * 17 + j];
+                  s += red_g[rr * 17 + j];
                 a.partial[(int64_t(nimg) * a.part_tiles_per_img + tile_in_img) * a.part_ld +
                           col0 + c + j] = double(s);
               }
             }
-            named_bar(1, 128);
+            named_bar(bid, 128);
           }
         }
       }
       if (etr) trace(a, 9, local * 24 + 19);
       // all 128 rows drained -> one arrival per CTA on the MMA CTA's barrier
       tc_fence_before();
-      named_bar(1, 128);
+      named_bar(bid, 128);
       if (r == 0) {
         if (PAIR) {
           mbar_arrive_remote(tempty_remote + uint32_t(acc * 8));
@@ -1493,7 +1511,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT3, CL == 1, KWF, H16 != 0>::kThre
           tslot = 0;
           tph ^= 1;
         }
-        if (++rot == C::kConvGroups) rot = 0;
+        if (++rot == (epi2 ? 1 : C::kConvGroups)) rot = 0;
         if (halo) {
           if (++htap == ntp) htap = 0;
           htp = a.taps[d.ph][htap];
