@@ -83,6 +83,8 @@ def parse():
     p.add_argument("--no-peaks", action="store_true", help="skip the peak microbenchmarks")
     p.add_argument("--no-modes", action="store_true",
                    help="skip the other precision tiers' figures")
+    p.add_argument("--no-inference", action="store_true",
+                   help="skip the whole-pool search behind the inference figure (profiling runs)")
     p.add_argument("--no-kernel-events", action="store_true",
                    help="skip the per-launch CUDA events (no roofline; overhead check)")
     return p.parse_args()
@@ -458,8 +460,8 @@ def main():
     # reference's per-layer search scored by the scheduler, outside the
     # timed regions; fisher_accepts >= the origin, rank_survivors: macs
     # ascending, fisher descending, I/search.hpp:338-349, 381)
-    full = [nb.Network.from_json(n) for n in warm_j + timed_j + spare_j]
-    full_reps, _ = nb.evaluate(sessions, full, prec)
+    full = [] if args.no_inference else [nb.Network.from_json(n) for n in warm_j + timed_j + spare_j]
+    full_reps, _ = nb.evaluate(sessions, full, prec) if full else ([], None)
     surv = [(nb.network_macs(n), -r.total, i) for i, (n, r) in enumerate(zip(full, full_reps))
             if r.total >= origin_rep.total]
     bi = min(surv)[2] if surv else -1

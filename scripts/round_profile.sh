@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench_default.log | cut -c1-300
 timeout 1500 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 12 --warmup 3 --streams 1 --no-cpu-baseline --no-modes --no-peaks \
+  --log-file gpurun_out/launches.csv python bench.py --steps 12 --warmup 3 --streams 1 --no-cpu-baseline --no-modes --no-peaks --no-inference \
   > gpurun_out/ncu_launch_bench.log 2>&1; echo "launches rc=$?"
 STEPS=12 bash scripts/ncu_traffic.sh
 rm -f gpurun_out/prof_r2_*.ncu-rep
