@@ -7,9 +7,21 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "nb200.h"
 
 namespace nb {
+
+// NVTX range over a scope (scheduler calls, evaluations, layers), for
+// Nsight Systems / `ncu --nvtx` filtering; header-only NVTX3, a no-op when no
+// tool is attached.
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 
 // Status-carrying exception; converted to nb_status at the C ABI.
 struct Error : std::runtime_error {

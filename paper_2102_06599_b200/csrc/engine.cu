@@ -839,6 +839,7 @@ void set_scaling(const NetPlan& P, const LayerPlan& lp, tc::TcArgs& a, const uin
 // per-image max |x|; out_amax (nullable) receives per-image max |y|.
 void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* x, float* y,
                  bool relu, cudaStream_t st, const uint32_t* in_amax, uint32_t* out_amax) {
+  Range range("conv_fprop");
   const ConvGeom& g = lp.geom;
   float* base = lp.wbase;
   bool direct = false;
@@ -900,6 +901,7 @@ void fprop_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* 
 void dgrad_layer(nb_ctx* c, const NetPlan& P, const LayerPlan& lp, const float* dpre,
                  const float* a_prev, bool relu_prev, float* dpre_out, float* g_out,
                  double* partial, cudaStream_t st, const uint32_t* in_amax, uint32_t* out_amax) {
+  Range range("conv_dgrad");
   const ConvGeom& g = lp.geom;
   float* base = lp.wbase;
   const double prev_floats = double(g.N) * g.H * g.W * g.Ci;
@@ -1028,6 +1030,7 @@ void reserve_run(nb_ctx* c, const NetPlan& P, int64_t N, int64_t K, int64_t L, b
 
 void run_enqueue(nb_session* s, const NetDesc& net, const nb_weights* w, nb_precision prec,
                  bool backward, const RunOut& out, Pending& pend, NetPlan* pre) {
+  Range range(backward ? "fisher_enqueue" : "forward_enqueue");
   nb_ctx* c = s->ctx;
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   ctx_activate(c);
@@ -1664,6 +1667,7 @@ nb_status nb_session_fisher(nb_session* s, const nb_network* net, const nb_weigh
 nb_status nb_fisher_sharded(nb_session* const* shards, int32_t count, const nb_network* net,
                             const nb_weights* w, nb_precision prec, nb_fisher_out* out) {
   return guard([&] {
+    Range range("nb_fisher_sharded");
     need(shards, "shards");
     need(out, "output");
     if (count < 1) fail(NB_ERR_CONFIG, "need at least one shard");

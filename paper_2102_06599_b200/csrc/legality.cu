@@ -260,6 +260,7 @@ using namespace nb;
 extern "C" nb_status nb_semantic_legality(nb_ctx* ctx, const nb_legal_nest* original,
                                           const nb_legal_nest* transformed, nb_legal_out* out) {
   return guard([&] {
+    Range range("nb_semantic_legality");
     if (!ctx || !original || !transformed || !out) fail(NB_ERR_CONFIG, "null argument");
     std::memset(out, 0, sizeof(*out));
     std::vector<int64_t> code;

@@ -189,6 +189,7 @@ using namespace nb;
 extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t is_int,
                                      const void* in, const void* w, void* out) {
   return guard([&] {
+    Range range("nb_nest_execute");
     if (!ctx || !nest || !in || !w || !out) fail(NB_ERR_CONFIG, "null argument");
     if (nest->out_rank > kMaxRank || nest->in_rank > kMaxRank || nest->w_rank > kMaxRank)
       fail(NB_ERR_UNSUPPORTED, "tensor rank above 4");
@@ -245,6 +246,7 @@ extern "C" nb_status nb_nest_execute(nb_ctx* ctx, const nb_nest* nest, int32_t i
 extern "C" nb_status nb_nest_cells(nb_ctx* ctx, const nb_nest* nest, int32_t* ci_lo,
                                    int32_t* ci_hi, int64_t* count) {
   return guard([&] {
+    Range range("nb_nest_cells");
     if (!ctx || !nest || !ci_lo || !ci_hi || !count) fail(NB_ERR_CONFIG, "null argument");
     if (nest->out_rank > kMaxRank || nest->in_rank > kMaxRank || nest->w_rank > kMaxRank)
       fail(NB_ERR_UNSUPPORTED, "tensor rank above 4");

@@ -56,6 +56,7 @@ extern "C" nb_status nb_evaluate(nb_session* const* sessions, int32_t num_sessio
                                  const nb_network* nets, int64_t count, nb_precision prec,
                                  nb_fisher_out* outs, nb_eval_stats* stats) {
   return guard([&] {
+    Range range("nb_evaluate");
     if (num_sessions < 1 || !sessions) fail(NB_ERR_CONFIG, "need at least one session");
     if (count < 0 || (count > 0 && (!nets || !outs))) fail(NB_ERR_CONFIG, "null candidates");
     // every session holds the same batch on its own context: a context's
