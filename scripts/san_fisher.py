@@ -7,6 +7,7 @@ prec = {"simt": Precision.SIMT, "fp32": Precision.FP32, "tf32": Precision.TF32}[
 net = Network([
     Layer(ConvSpec(3, 32, 16, 16, 3, 3, 1, 1)),
     Layer(ConvSpec(32, 64, 16, 16, 3, 3, 1, 1)),
+    Layer(ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, groups=64)),
     Layer(ConvSpec(64, 64, 16, 16, 3, 3, 1, 1, groups=2)),
     Layer(ConvSpec(64, 128, 16, 16, 3, 3, 2, 1)),
     Layer(ConvSpec(128, 128, 8, 8, 3, 3, 1, 1, bottleneck_out=2)),
