@@ -156,7 +156,27 @@ class Clocks:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        """NVML directly: a sample every ~5 ms (the timed region can be ~0.1 s)."""
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+                ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)]
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active"
+                                                       for _, b in bits])
+            self._stop.wait(0.005)
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index),
