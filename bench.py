@@ -294,11 +294,17 @@ def cpu_baseline_sample(timed, threads):
     subtracted (oracle/refbench.py).  The candidate's N=1 thread-seconds,
     x128 by the reference's exact linearity in N (I/nnet.hpp:184, 206), give
     candidates/s on `threads` cores (extrapolated)."""
-    from oracle.refbench import RefArm, candidate_seconds_by_slices
-    net = timed[0]
+    from oracle.refbench import RefArm, candidate_seconds_by_slices, fisher_macs
+    # the timed-pool candidate of median Fisher MACs (candidate 0 can be an
+    # early crop whose whole network runs at 2x2: 50x cheaper than most)
+    order = sorted(range(len(timed)), key=lambda i: fisher_macs(timed[i], 1))
+    pick = order[len(order) // 2]
+    net = timed[pick]
     sec, wall, parts = candidate_seconds_by_slices(RefArm(), net, threads)
     v = threads / (sec * N_BATCH)
-    return v, (f"reference fisher_potential (oracle/_ref) on timed-pool candidate 0 at N=1, "
+    return v, (f"reference fisher_potential (oracle/_ref) on timed-pool candidate {pick} "
+               f"(median Fisher MACs of the pool, {fisher_macs(net, 1) / 1e9:.2f} GMAC per "
+               f"example) at N=1, "
                f"cut into {parts} layer slices run concurrently on {threads} host threads "
                f"({wall:.1f} s wall); {sec:.1f} thread-s per N=1 evaluation x{N_BATCH} "
                f"examples (exact linearity in N), {threads} candidates in flight (extrapolated)")
@@ -306,36 +312,70 @@ def cpu_baseline_sample(timed, threads):
 
 def run_reference(args):
     """--impl reference: the reference's own CPU path on this box's host
-    cores, through oracle/refbench.py only (the product is never imported):
-    each step is one timed-pool candidate's fisher_potential at N=1 (example
-    0 of the bench batch: make_batch's prefix property), the K steps
-    self-scheduled on every host thread exactly as evaluate_all does
-    (I/search.hpp:315-334).  value = K/128 candidates per timed second: a
+    cores, through oracle/refbench.py only (the product is never imported).
+    A whole candidate at N=1 costs the reference ~100-200 thread-seconds
+    (55-100 ns/MAC), so each step is a bounded sample: one
+    MAC-balanced layer slice of a timed-pool candidate (the candidates in
+    pool order, each cut into `threads` slices, slices() in
+    oracle/refbench.py), scored at N=1 by the reference's fisher_potential,
+    the K steps self-scheduled on every host thread as evaluate_all does
+    (I/search.hpp:315-334).  Every slice but a candidate's first starts one
+    layer early so that its first layer's dgrad runs; that layer's extra
+    forward is timed (layer_forward) and subtracted.  value = threads x
+    (candidates the K slices cover) / (128 x their thread-seconds): a
     candidate at N=128 is 128 such evaluations (I/nnet.hpp:184, 206),
     labelled extrapolated."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.refbench import RefArm
+    from oracle.refbench import RefArm, slices
     threads = os.cpu_count() or 1
     world = int(os.environ.get("WORLD_SIZE", "1"))
     _, warm, timed, spare = timed_pool(args.steps, args.warmup, world)
-    timed = timed[:args.steps]
     arm = RefArm()
-    # warm-up: W untimed evaluations of the cheapest spare candidates (the
-    # CPU path has no caches to fill; this only pages the code in)
-    cheap = sorted(spare, key=lambda n: sum(_macs(l) for l in n["layers"]))[:max(1, args.warmup)]
-    arm.fisher_jobs(cheap, 1, threads)
-    totals, secs, wall = arm.fisher_jobs(timed, 1, threads)
-    v = len(timed) / N_BATCH / wall
-    sample = (f"reference fisher_potential (oracle/_ref, evaluate_all's thread pool) on the "
-              f"{len(timed)} timed-pool candidates, each whole network at N=1 (example 0 of "
-              f"the batch), on {threads} host threads: {wall:.1f} s wall, "
-              f"{statistics.mean(secs):.1f} s mean per evaluation; x{N_BATCH} examples per "
-              f"candidate (exact linearity in N, extrapolated)")
+
+    def cut(net):
+        out = []
+        sl = slices(net, threads)
+        for k, (a, b) in enumerate(sl):
+            lo = a - 1 if k > 0 else a
+            out.append(({"schema_version": 1, "seed": net.get("seed", 42),
+                         "num_classes": net.get("num_classes", 10),
+                         "layers": [dict(l) for l in net["layers"][lo:b + 1]]},
+                        net["layers"][a - 1] if k > 0 else None, 1.0 / len(sl)))
+        return out
+
+    steps, ci = [], 0
+    while len(steps) < args.steps:
+        steps += cut(timed[ci % len(timed)])
+        ci += 1
+    steps = steps[:args.steps]
+    # warm-up: W untimed slices of the cheapest spare candidate (the CPU path
+    # has no caches to fill; this only pages the code in)
+    cheap = min(spare or warm, key=lambda n: sum(_macs(l) for l in n["layers"]))
+    wsteps = cut(cheap)[:max(1, args.warmup)]
+    arm.fisher_jobs([x[0] for x in wsteps], 1, threads)
+    totals, secs, wall = arm.fisher_jobs([x[0] for x in steps], 1, threads)
+    fwd = {}
+    extra = 0.0
+    for _, ov, _ in steps:
+        if ov is not None:
+            key = json.dumps(ov, sort_keys=True)
+            if key not in fwd:
+                fwd[key] = arm.layer_forward_seconds(ov)
+            extra += fwd[key]
+    thread_s = sum(secs) - extra
+    cands = sum(x[2] for x in steps)
+    v = threads * cands / (N_BATCH * thread_s)
+    sample = (f"reference fisher_potential (oracle/_ref, evaluate_all's thread pool) on "
+              f"{len(steps)} MAC-balanced layer slices of the first {ci} timed-pool candidates "
+              f"({cands:.2f} candidates' worth), each at N=1 (example 0 of the batch), on "
+              f"{threads} host threads: {wall:.1f} s wall, {thread_s:.1f} thread-s after the "
+              f"overlap layers' forwards; {thread_s / cands:.1f} thread-s per candidate at N=1, "
+              f"x{N_BATCH} examples (exact linearity in N, extrapolated)")
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": len(timed), "warmup": len(cheap),
-            "ms_per_step": 1e3 * wall / len(timed), "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": len(steps), "warmup": len(wsteps),
+            "ms_per_step": 1e3 * wall / len(steps), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(args.steps, args.streams, world),
             "precision": "fp64 (the reference's double arithmetic)",
