@@ -1306,12 +1306,21 @@ void launch_fprop_direct(const ConvGeom& g, int range, const float* x, const flo
       return e && std::atoi(e) == 1 ? 1 : 2;
     }();
     // NB_DW3_OWB: output columns per thread (1, 2, 4 or 8 with V=2)
-    static const int OWB = [] {
+    // NB_DW3_OWB fixes it; by default the widest of 8, 4, 2, 1 whose grid
+    // still has a wave of 512 threads per SM (small batches / images need the
+    // parallelism more than the reuse)
+    static const int OWB_ENV = [] {
       const char* e = std::getenv("NB_DW3_OWB");
-      const int v = e ? std::atoi(e) : 8;
-      return v == 1 || v == 2 || v == 4 ? v : 8;
+      const int v = e ? std::atoi(e) : 0;
+      return v == 1 || v == 2 || v == 4 || v == 8 ? v : 0;
     }();
-    const DwShape d = dw3_shape(g.N, g.OH, g.OW, r.len / V, OWB);
+    int OWB = OWB_ENV ? OWB_ENV : 8;
+    DwShape d = dw3_shape(g.N, g.OH, g.OW, r.len / V, OWB);
+    while (!OWB_ENV && OWB > 1 &&
+           int64_t(d.grid.x) * d.grid.y * d.grid.z * d.block.x * d.block.y < int64_t(148) * 512) {
+      OWB /= 2;
+      d = dw3_shape(g.N, g.OH, g.OW, r.len / V, OWB);
+    }
     auto go = [&](auto kern) { kern<<<d.grid, d.block, 0, st>>>(g, range, x, wbase, y, relu, d.strip); };
     if (V == 2) {
       if (OWB == 8) go(k_dw3_nhwc<2, 8>);
