@@ -735,17 +735,17 @@ void launch_tc(nb_ctx* c, const TcPlan& tp, const tc::TcArgs& args, bool split3,
   const int ch = convh >= 0 ? convh : (bf3 ? 0 : 1);
   L.args.conv_halves = ch == 1 || (ch == 2 && tp.kwf) ? 1 : 0;
   L.num_sms = c->num_sms;
-  // Halo mode (NB_TC_HALO=1): a split-converter launch over a
-  // stride-1 A operand with several taps per phase loads one halo box per
-  // 32-channel chunk (tile + the taps' offsets) and its converters form the
-  // shifted rows of every tap from it, when the box fits the kernel's halo
-  // buffers.
-  // (off by default: on the R34 bench it moves nothing -- the split
-  // converters, not the A operand's L2 traffic, bound these launches --
-  // profiles/r02_kernels.md)
+  // Halo mode (default; NB_TC_HALO=0 turns it off): a split-converter launch
+  // over a stride-1 A operand with several taps per phase loads one halo box
+  // per 32-channel chunk (tile + the taps' offsets) and its converters form
+  // the shifted rows of every tap from it, when the box fits the kernel's
+  // halo buffers.  A's L2 -> SM bytes per 3x3 stage drop from 16 KB to ~3 KB.
+  // It tied with the row-per-tap A operand while the converters were slower;
+  // after the late-round-2 epilogue work it is ahead (origin Fisher 2.79 ->
+  // 2.62 ms, same-box A/B, profiles/r02_kernels.md section 6).
   static const bool halo_on = [] {
     const char* e = std::getenv("NB_TC_HALO");
-    return e && std::atoi(e) != 0;
+    return !e || std::atoi(e) != 0;
   }();
   L.args.halo = 0;
   if (halo_on && split3 && !tp.pair && args.S == 1) {

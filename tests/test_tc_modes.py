@@ -1,8 +1,8 @@
 """The tcgen05 kernel's experimental launch modes (environment switches read
 once per process, so each runs in a subprocess with a deadline): CTA pairs,
 multicast-B clusters, converter stage alternation, no split-K, no PDL, the
-kw-fused plans switched off, the 3xTF32 / 3xBF16 splits, the halo-tile A
-operand, the 256-wide single-accumulator tile and the kw-fused dgrad with one
+kw-fused plans switched off, the 3xTF32 / 3xBF16 splits, the row-per-tap A
+operand (halo tiles off), the 256-wide single-accumulator tile and the kw-fused dgrad with one
 epilogue column group (debug bit 2^21).  Each must reproduce reference_conv<int64>
 bit for bit on tensor-core-shaped layers (including a kw-fused shape) and
 finish -- a hang here is a barrier-count bug."""
@@ -44,10 +44,9 @@ print("ok")
 MODES = ["NB_TC_SPLIT=tf32,NB_TC_PAIR=1", "NB_TC_SPLIT=tf32,NB_TC_PAIR=2", "NB_TC_MC=1",
          "NB_TC_MC=2", "NB_TC_SPLIT=tf32,NB_TC_MC=1", "NB_TC_CONVH=0", "NB_TC_CONVH=1",
          "NB_TC_CONVH=2", "NB_TC_KSPLIT=0", "NB_TC_PDL=0", "NB_TC_KWF=0", "NB_TC_SPLIT=tf32",
-         "NB_TC_SPLIT=bf16", "NB_TC_HALO=1", "NB_TC_HALO=1,NB_TC_CONVH=1",
-         "NB_TC_HALO=1,NB_TC_SPLIT=tf32", "NB_TC_BN3=256", "NB_TC_SPLIT=tf32,NB_TC_BN3=256",
-         "NB_TC_HALO=1,NB_TC_MC=1", "NB_TC_DEBUG=16384",
-         "NB_TC_DEBUG=2097152"]
+         "NB_TC_SPLIT=bf16", "NB_TC_HALO=0", "NB_TC_HALO=0,NB_TC_CONVH=1",
+         "NB_TC_HALO=0,NB_TC_SPLIT=tf32", "NB_TC_BN3=256", "NB_TC_SPLIT=tf32,NB_TC_BN3=256",
+         "NB_TC_HALO=0,NB_TC_MC=1", "NB_TC_DEBUG=16384,NB_TC_HALO=0", "NB_TC_DEBUG=2097152"]
 
 
 @pytest.mark.gpu
