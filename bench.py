@@ -313,11 +313,12 @@ def cpu_baseline_sample(timed, threads):
 def run_reference(args):
     """--impl reference: the reference's own CPU path on this box's host
     cores, through oracle/refbench.py only (the product is never imported).
-    A whole candidate at N=1 costs the reference ~100-200 thread-seconds
-    (55-100 ns/MAC), so each step is a bounded sample: one
-    MAC-balanced layer slice of a timed-pool candidate (the candidates in
-    pool order, each cut into `threads` slices, slices() in
-    oracle/refbench.py), scored at N=1 by the reference's fisher_potential,
+    A whole candidate at N=1 costs the reference ~50-200 thread-seconds
+    (55-100 ns/MAC), so each step is a bounded sample: step k is
+    one MAC-balanced layer slice of timed candidate k (each candidate cut into
+    `threads` slices, slices() in oracle/refbench.py; slice k mod the count),
+    so the K steps sample the nb200 arm's K timed candidates once each,
+    scored at N=1 by the reference's fisher_potential,
     the K steps self-scheduled on every host thread as evaluate_all does
     (I/search.hpp:315-334).  Every slice but a candidate's first starts one
     layer early so that its first layer's dgrad runs; that layer's extra
@@ -345,11 +346,13 @@ def run_reference(args):
                         net["layers"][a - 1] if k > 0 else None, 1.0 / len(sl)))
         return out
 
-    steps, ci = [], 0
-    while len(steps) < args.steps:
-        steps += cut(timed[ci % len(timed)])
-        ci += 1
-    steps = steps[:args.steps]
+    # step k: one slice of timed candidate k (slice k mod its slice count), so
+    # the K steps sample every timed candidate of the nb200 arm once
+    steps = []
+    for k in range(args.steps):
+        parts = cut(timed[k % len(timed)])
+        steps.append(parts[k % len(parts)])
+    ci = min(args.steps, len(timed))
     # warm-up: W untimed slices of the cheapest spare candidate (the CPU path
     # has no caches to fill; this only pages the code in)
     cheap = min(spare or warm, key=lambda n: sum(_macs(l) for l in n["layers"]))
@@ -368,8 +371,8 @@ def run_reference(args):
     cands = sum(x[2] for x in steps)
     v = threads * cands / (N_BATCH * thread_s)
     sample = (f"reference fisher_potential (oracle/_ref, evaluate_all's thread pool) on "
-              f"{len(steps)} MAC-balanced layer slices of the first {ci} timed-pool candidates "
-              f"({cands:.2f} candidates' worth), each at N=1 (example 0 of the batch), on "
+              f"{len(steps)} MAC-balanced layer slices, one of each of the {ci} timed "
+              f"candidates ({cands:.2f} candidates' worth), each at N=1 (example 0 of the batch), on "
               f"{threads} host threads: {wall:.1f} s wall, {thread_s:.1f} thread-s after the "
               f"overlap layers' forwards; {thread_s / cands:.1f} thread-s per candidate at N=1, "
               f"x{N_BATCH} examples (exact linearity in N, extrapolated)")
